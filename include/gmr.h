@@ -1,0 +1,184 @@
+/*
+ * gmr.h — C ABI of the B200-native Gaussian Mesh Renderer hot path.
+ *
+ * Replaces the reference's numpy render path (meshsplat, pure Python; see
+ * SURVEY.md §8b).  Every entry point is stream-ordered on a caller-supplied
+ * cudaStream_t (passed as void*), takes plain device pointers, never
+ * allocates and never frees: the caller owns every buffer, including the
+ * workspace, whose size the *_workspace_size functions report.
+ *
+ *   reference entry point (file:line)               replaced by
+ *   render.py:441-450  render_mesh                   gmr_render_forward  (+ gmr_status)
+ *   render.py:453-467  render_backward               gmr_render_backward (+ gmr_topology_build)
+ *   render.py:272-291  rasterize                     gmr_rasterize_forward
+ *   render.py:294-361  rasterize_backward            gmr_rasterize_backward
+ *   render.py:103-145  project_cloud                 fused into gmr_render_forward (K1)
+ *   render.py:364-402  project_cloud_backward        fused into gmr_render_backward (K5)
+ *   convert.py:313-368 convert_mesh (embed route)    gmr_convert
+ *   convert.py:371-437 convert_backward              gmr_convert_backward
+ *   losses.py:151-162  total_loss view loop          B views per gmr_render_* call
+ *
+ * Scalars: every floating-point buffer is either float32 (GMR_F32, the fast
+ * path; `fit`'s default dtype, reference optim.py:161) or float64
+ * (GMR_F64, the parity path; render_mesh's default dtype, render.py:442).
+ * Indices are int32.  Errors: functions return GMR_OK (0) or a negative
+ * code; gmr_last_error() returns a thread-local message.
+ */
+#ifndef GMR_H_
+#define GMR_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  GMR_OK = 0,
+  GMR_EINVAL = -1,      /* bad argument (shape, null pointer, dtype)          */
+  GMR_ENONFINITE = -2,  /* a kept splat has a non-finite parameter            */
+  GMR_EWORKSPACE = -3,  /* workspace too small for the declared sizes         */
+  GMR_ECUDA = -4,       /* a CUDA runtime call failed                         */
+  GMR_ECAPACITY = -5    /* tile entries exceeded entry_capacity (see status)  */
+};
+
+enum { GMR_F32 = 0, GMR_F64 = 1 };
+
+#define GMR_MAX_VIEWS_PER_CALL 4096
+
+/* Pinhole camera (reference camera.py:15-58): p_cam = R p_world + t,
+ * pixel centres at integer coordinates.  Host memory, always float64. */
+typedef struct {
+  double R[9];   /* row-major world->camera rotation */
+  double t[3];
+  double fx, fy, cx, cy;
+  double near_plane, far_plane;
+} GmrCamera;
+
+/* Device-resident mesh (reference mesh.py:46-130). positions/colors are
+ * V*3 scalars of the call's dtype; faces are F*3 int32. */
+typedef struct {
+  const void* positions;
+  const void* colors;
+  const int32_t* faces;
+  int64_t num_vertices;
+  int64_t num_faces;
+} GmrMesh;
+
+/* Raster settings shared by a batch of views. */
+typedef struct {
+  int32_t width, height;   /* all views of one call share W x H           */
+  double background[3];    /* constant background colour (render.py:288) */
+  int32_t dtype;           /* GMR_F32 or GMR_F64                          */
+  int32_t rescale;         /* convert.py:313 rescale flag (default 1)     */
+  int32_t flags;           /* GMR_FLAG_* below                            */
+} GmrRaster;
+
+/* GmrRaster.flags: keep each item's (radius, depth) for gmr_copy_splats. */
+#define GMR_FLAG_DEBUG_AUX 1
+
+/* Result of a forward pass, read back by gmr_status (synchronises). */
+typedef struct {
+  int64_t entries;          /* tile entries E summed over the views         */
+  int64_t entry_capacity;   /* capacity the forward was planned with        */
+  int64_t kept;             /* splats that survived depth+screen culling    */
+  int32_t overflow;         /* 1: entries > capacity; outputs not written   */
+  int32_t nonfinite_field;  /* -1, or 0..5 = mean2d,cov2d,conic,depth,color,opacity */
+  int64_t nonfinite_item;   /* first offending item (view*F + face) or -1   */
+} GmrStatus;
+
+const char* gmr_last_error(void);
+const char* gmr_version(void);
+
+/* ---- mesh path: B views in one call --------------------------------- */
+
+/* Bytes of workspace for F faces, B views of W x H, and up to
+ * entry_capacity tile entries (summed over views). */
+int gmr_render_workspace_size(int64_t num_faces, int32_t num_views, int32_t width,
+                              int32_t height, int64_t entry_capacity, int32_t dtype,
+                              size_t* bytes);
+
+/* Forward: rgb [B,H,W,3], alpha [B,H,W] (dtype).  The workspace carries the
+ * per-view splat records, sorted tile entries, tile ranges and final
+ * transmittance to gmr_render_backward and must not be touched between the
+ * two calls. */
+int gmr_render_forward(const GmrMesh* mesh, const GmrCamera* cameras, int32_t num_views,
+                       const GmrRaster* raster, void* rgb, void* alpha, void* workspace,
+                       size_t workspace_bytes, int64_t entry_capacity, void* stream);
+
+/* Synchronise `stream` and read the status of the last forward that used
+ * `workspace`.  Returns GMR_ECAPACITY / GMR_ENONFINITE as appropriate. */
+int gmr_status(const void* workspace, GmrStatus* status, void* stream);
+
+/* Static face->vertex scatter plan (CSR in the reference's np.add.at order,
+ * convert.py:427-436).  Built once per topology. */
+int gmr_topology_size(int64_t num_faces, int64_t num_vertices, size_t* bytes);
+int gmr_topology_build(const int32_t* faces, int64_t num_faces, int64_t num_vertices,
+                       void* topology, size_t topology_bytes, void* stream);
+
+/* Backward of sum(g_rgb*rgb) + sum(g_alpha*alpha) over all B views:
+ * grad_positions / grad_colors [V,3] (dtype) are OVERWRITTEN with the sum
+ * over views (reference losses.py:160-162 semantics when the caller
+ * pre-scales g by w/n).  `rgb` is the forward's output. */
+int gmr_render_backward(const GmrMesh* mesh, const GmrCamera* cameras, int32_t num_views,
+                        const GmrRaster* raster, const void* rgb, const void* grad_rgb,
+                        const void* grad_alpha, void* grad_positions, void* grad_colors,
+                        const void* topology, void* workspace, size_t workspace_bytes,
+                        int64_t entry_capacity, void* stream);
+
+/* ---- splat path (rasterize / rasterize_backward stage functions) ------ */
+
+/* K splats: mean2d [K,2], cov2d [K,2,2], depth [K], color [K,3],
+ * opacity [K] (dtype), already in tie-break (source) order. */
+typedef struct {
+  const void* mean2d;
+  const void* cov2d;
+  const void* depth;
+  const void* color;
+  const void* opacity;
+  int64_t count;
+} GmrSplats;
+
+int gmr_raster_workspace_size(int64_t num_splats, int32_t width, int32_t height,
+                              int64_t entry_capacity, int32_t dtype, size_t* bytes);
+int gmr_rasterize_forward(const GmrSplats* splats, const GmrRaster* raster, void* rgb,
+                          void* alpha, void* workspace, size_t workspace_bytes,
+                          int64_t entry_capacity, void* stream);
+/* Outputs g_mean2d [K,2], g_cov2d [K,2,2], g_color [K,3], g_opacity [K]. */
+int gmr_rasterize_backward(const GmrSplats* splats, const GmrRaster* raster, const void* rgb,
+                           const void* grad_rgb, const void* grad_alpha, void* g_mean2d,
+                           void* g_cov2d, void* g_color, void* g_opacity, void* workspace,
+                           size_t workspace_bytes, int64_t entry_capacity, void* stream);
+
+/* Inspection (bit-exact binning checks).  `items_per_view` is F (mesh
+ * path, mesh_path=1) or K (splat path, views=1); sizes as in the forward.
+ * gmr_copy_entries: the sorted tile entries (item = view*F + face, or splat
+ * index; `entries` from gmr_status) and the (views*T + 1) tile bounds.
+ * gmr_copy_splats: per item, the screen record [8] (mean_x, mean_y,
+ * conic a, b, c, ext_x, ext_y, radius; dtype), tile rect (uint2:
+ * tx0|ty0<<16, tx1|ty1<<16), tile count (uint32, 0 = culled) and, when
+ * the forward ran with GMR_FLAG_DEBUG_AUX, aux [2] = (radius, depth). */
+int gmr_copy_entries(const void* workspace, int64_t items_per_view, int32_t views,
+                     const GmrRaster* raster, int64_t entry_capacity, int32_t mesh_path,
+                     uint32_t* entry_items, uint32_t* bounds, void* stream);
+int gmr_copy_splats(const void* workspace, int64_t items_per_view, int32_t views,
+                    const GmrRaster* raster, int64_t entry_capacity, int32_t mesh_path,
+                    void* records, void* rects, uint32_t* counts, void* aux, void* stream);
+
+/* ---- single-stage entry points ----------------------------------------- */
+
+/* convert_mesh embed route: means [F,3], cov3d [F,3,3], colors [F,3]. */
+int gmr_convert(const GmrMesh* mesh, int32_t rescale, int32_t dtype, void* means, void* cov3d,
+                void* colors, uint8_t* degenerate, void* stream);
+/* convert_backward: vertex grads [V,3] from facet grads (overwrites). */
+int gmr_convert_backward(const GmrMesh* mesh, int32_t rescale, int32_t dtype,
+                         const void* grad_means, const void* grad_cov3d,
+                         const void* grad_colors, void* grad_positions, void* grad_colors_v,
+                         const void* topology, void* scratch, size_t scratch_bytes, void* stream);
+int gmr_convert_scratch_size(int64_t num_faces, int32_t dtype, size_t* bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GMR_H_ */

@@ -1,0 +1,393 @@
+"""Drop-in numpy API of the GMR hot path, backed by libgmr.so on the GPU.
+
+Same names, signatures, dtypes and error behaviour as the reference
+(`meshsplat`): render.py:441-467 (`render_mesh`, `render_backward`),
+render.py:272-361 (`rasterize`, `rasterize_backward`), convert.py:313-437
+(`convert_mesh`, `convert_backward`) and losses.py:43-174 (`total_loss`
+and its terms).  Inputs are copied to the current CUDA device, all compute
+runs in the CUDA library, results come back as numpy arrays.  There is no
+CPU fallback: without a CUDA device every call raises.
+"""
+
+from __future__ import annotations
+
+import weakref
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import engine
+from .camera import Camera
+
+TILE = 16
+ALPHA_CLAMP = 0.99
+CONTRIB_FLOOR = 1.0 / 255.0
+TRANSMITTANCE_STOP = 1e-4
+DILATION = 0.3
+BCE_CLAMP = 1e-6
+
+_TORCH = {np.dtype(np.float32): torch.float32, np.dtype(np.float64): torch.float64}
+
+
+def _torch_dtype(dtype):
+    dt = np.dtype(dtype)
+    if dt not in _TORCH:
+        raise ValueError(f"dtype must be float32 or float64, got {dt}")
+    return _TORCH[dt]
+
+
+def _device():
+    engine.L.load()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+_mesh_cache: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+
+
+def _device_mesh(mesh, dtype):
+    """(pos, col, faces int32) on the device for an immutable mesh object."""
+    tdt = _torch_dtype(dtype)
+    dev = _device()
+    try:
+        per = _mesh_cache.setdefault(mesh, {})
+    except TypeError:
+        per = {}
+    hit = per.get(tdt)
+    if hit is None:
+        pos = torch.as_tensor(np.ascontiguousarray(mesh.vertices), dtype=tdt).to(dev)
+        col = torch.as_tensor(np.ascontiguousarray(mesh.colors), dtype=tdt).to(dev)
+        faces = per.get("faces")
+        if faces is None:
+            faces = torch.as_tensor(np.ascontiguousarray(mesh.facets), dtype=torch.int32).to(dev)
+            per["faces"] = faces
+        hit = per[tdt] = (pos, col, faces)
+    return hit
+
+
+@dataclass(frozen=True)
+class RenderOutput:
+    rgb: np.ndarray
+    alpha: np.ndarray
+    background: np.ndarray
+
+
+@dataclass
+class RenderContext:
+    """Everything render_backward needs (reference render.py:429-438); the
+    device part (sorted tile entries, tile ranges, T_final) lives in
+    `state.ws` so the backward never re-bins."""
+    mesh: object
+    camera: Camera
+    output: RenderOutput
+    dtype: type
+    rescale: bool
+    state: engine.ForwardState
+    rgb_device: torch.Tensor
+
+
+def _kept_rank(state, num_faces):
+    def to_index(item):
+        _, _, cnt, _ = engine.copy_splats(state, num_faces, True)
+        c = cnt.cpu().numpy()
+        return int(np.count_nonzero(c[:item] > 0))
+    return to_index
+
+
+def render_mesh(mesh, camera, background=(0.0, 0.0, 0.0), rescale: bool = True,
+                dtype=np.float64, return_ctx: bool = False):
+    """convert -> project -> rasterize on the GPU (reference render.py:441-450)."""
+    pos, col, faces = _device_mesh(mesh, dtype)
+    bg = np.asarray(background, dtype=dtype)
+    rgb, alpha, state = engine.render_forward(
+        pos, col, faces, [camera], camera.width, camera.height, bg, rescale,
+        item_to_index=None)
+    out = RenderOutput(rgb=rgb[0].cpu().numpy(), alpha=alpha[0].cpu().numpy(), background=bg)
+    if not return_ctx:
+        return out
+    return out, RenderContext(mesh=mesh, camera=camera, output=out, dtype=dtype, rescale=rescale,
+                              state=state, rgb_device=rgb)
+
+
+def render_backward(ctx: RenderContext, grad_rgb, grad_alpha):
+    """Pixel gradients -> (grad_vertices (V,3), grad_vertex_colors (V,3)),
+    float64 like the reference (render.py:453-467)."""
+    cam = ctx.camera
+    grad_rgb = np.asarray(grad_rgb)
+    grad_alpha = np.asarray(grad_alpha)
+    if grad_rgb.shape != (cam.height, cam.width, 3) or grad_alpha.shape != (cam.height, cam.width):
+        raise ValueError("upstream gradient shapes do not match the image")
+    pos, col, faces = _device_mesh(ctx.mesh, ctx.dtype)
+    tdt = _torch_dtype(ctx.dtype)
+    dev = pos.device
+    g_rgb = torch.as_tensor(np.ascontiguousarray(grad_rgb), dtype=tdt).to(dev)[None]
+    g_a = torch.as_tensor(np.ascontiguousarray(grad_alpha), dtype=tdt).to(dev)[None]
+    gp, gc = engine.render_backward(ctx.state, pos, col, faces, ctx.rgb_device, g_rgb, g_a)
+    return gp.cpu().numpy().astype(np.float64), gc.cpu().numpy().astype(np.float64)
+
+
+# ---------------------------------------------------------------------------
+# splat path: rasterize / rasterize_backward (render.py:168-188, 272-361)
+# ---------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class Splat2D:
+    mean2d: np.ndarray
+    cov2d_screen: np.ndarray
+    depth: float
+    color: np.ndarray
+    opacity: float
+    source: int = -1
+
+
+def _splat_arrays(splats, dtype):
+    if hasattr(splats, "mean2d") and not isinstance(splats, (list, tuple)):
+        k = len(splats.depth)
+        src = np.asarray(getattr(splats, "source", np.arange(k)), dtype=np.int64)
+        return (np.asarray(splats.mean2d, dtype).reshape(k, 2), np.asarray(splats.cov2d, dtype).reshape(k, 2, 2),
+                np.asarray(splats.depth, dtype).reshape(k), np.asarray(splats.color, dtype).reshape(k, 3),
+                np.asarray(splats.opacity, dtype).reshape(k), src)
+    k = len(splats)
+    if k == 0:
+        z = lambda *s: np.zeros(s, dtype=dtype)
+        return z(0, 2), z(0, 2, 2), z(0), z(0, 3), z(0), np.zeros(0, np.int64)
+    return (np.stack([np.asarray(s.mean2d, dtype=dtype) for s in splats]),
+            np.stack([np.asarray(s.cov2d_screen, dtype=dtype) for s in splats]),
+            np.array([s.depth for s in splats], dtype=dtype),
+            np.stack([np.asarray(s.color, dtype=dtype) for s in splats]),
+            np.array([s.opacity for s in splats], dtype=dtype),
+            np.array([s.source if s.source >= 0 else i for i, s in enumerate(splats)], dtype=np.int64))
+
+
+def _check_finite_host(arrays):
+    """render.py:191-197 for the caller's inputs (conic is checked on the device)."""
+    names = ("mean2d", "cov2d", None, "depth", "color", "opacity")
+    vals = dict(zip(("mean2d", "cov2d", "depth", "color", "opacity"), arrays[:5]))
+    for name in names:
+        if name is None:
+            continue
+        bad = ~np.isfinite(vals[name])
+        if bad.any():
+            raise ValueError(f"non-finite splat parameter {name!r} at splat {int(np.argwhere(bad)[0][0])}")
+
+
+def _raster_device(splats, camera, background, dtype):
+    arrs = _splat_arrays(splats, dtype)
+    _check_finite_host(arrs)
+    order = np.argsort(arrs[5], kind="stable")   # tie-break by source (render.py:227)
+    tdt = _torch_dtype(dtype)
+    dev = _device()
+    t = [torch.as_tensor(np.ascontiguousarray(a[order]), dtype=tdt).to(dev) for a in arrs[:5]]
+    rgb, alpha, state = engine.rasterize_forward(*t, camera.width, camera.height,
+                                                 np.asarray(background, dtype=np.float64))
+    return t, order, rgb, alpha, state
+
+
+def rasterize(splats, camera, background=(0.0, 0.0, 0.0), dtype=np.float64) -> RenderOutput:
+    """Front-to-back compositing of splats on the GPU (render.py:272-291)."""
+    _, _, rgb, alpha, _ = _raster_device(splats, camera, background, dtype)
+    return RenderOutput(rgb=rgb.cpu().numpy(), alpha=alpha.cpu().numpy(),
+                        background=np.asarray(background, dtype=dtype))
+
+
+def rasterize_backward(splats, camera, output, grad_rgb, grad_alpha, dtype=np.float64):
+    """(g_mean2d, g_cov2d, g_color, g_opacity) in the caller's splat order
+    (render.py:294-361)."""
+    w, h = camera.width, camera.height
+    grad_rgb = np.asarray(grad_rgb, dtype=dtype)
+    grad_alpha = np.asarray(grad_alpha, dtype=dtype)
+    if grad_rgb.shape != (h, w, 3) or grad_alpha.shape != (h, w):
+        raise ValueError("upstream gradient shapes do not match the image")
+    bg = np.asarray(output.background, dtype=np.float64)
+    t, order, rgb, _, state = _raster_device(splats, camera, bg, dtype)
+    tdt = _torch_dtype(dtype)
+    g = [torch.as_tensor(np.ascontiguousarray(x), dtype=tdt).to(rgb.device) for x in (grad_rgb, grad_alpha)]
+    gm, gc, gcol, gop = engine.rasterize_backward(state, *t, rgb, g[0], g[1])
+    inv = np.empty_like(order)
+    inv[order] = np.arange(len(order))
+    return tuple(x.cpu().numpy()[inv] for x in (gm, gc, gcol, gop))
+
+
+# ---------------------------------------------------------------------------
+# conversion stage (convert.py:313-437, embed route)
+# ---------------------------------------------------------------------------
+
+@dataclass
+class GaussianCloud:
+    means: np.ndarray
+    cov3d: np.ndarray
+    colors: np.ndarray
+    opacities: np.ndarray
+    degenerate: np.ndarray
+    path: str = "embed"
+    rescale: bool = True
+
+    def __len__(self):
+        return len(self.means)
+
+
+def convert_mesh(mesh, path: str = "embed", rescale: bool = True) -> GaussianCloud:
+    """Facet -> Gaussian, embed route, float64 (convert.py:313-343)."""
+    if path not in ("embed", "eigen"):
+        raise ValueError(f"unknown conversion path {path!r}")
+    if path == "eigen":
+        raise ValueError("the eigen route is a CPU validation path; only 'embed' runs on the device")
+    pos, col, faces = _device_mesh(mesh, np.float64)
+    means, cov, colors, degen = engine.convert(pos, col, faces, rescale)
+    m = len(mesh.facets)
+    return GaussianCloud(means=means.cpu().numpy(), cov3d=cov.cpu().numpy(), colors=colors.cpu().numpy(),
+                         opacities=np.ones(m), degenerate=degen.cpu().numpy(), path="embed", rescale=rescale)
+
+
+def convert_backward(mesh, cloud, grad_means, grad_cov3ds, grad_colors):
+    """Facet grads -> vertex grads in np.add.at order (convert.py:371-437)."""
+    if getattr(cloud, "path", "embed") != "embed":
+        raise ValueError("convert_backward differentiates the embed path only")
+    m = len(mesh.facets)
+    gm = np.asarray(grad_means, dtype=np.float64)
+    gc = np.asarray(grad_cov3ds, dtype=np.float64)
+    gcol = np.asarray(grad_colors, dtype=np.float64)
+    if gm.shape != (m, 3) or gc.shape != (m, 3, 3) or gcol.shape != (m, 3):
+        raise ValueError(f"gradient shapes {gm.shape}, {gc.shape}, {gcol.shape} do not match {m} facets")
+    pos, col, faces = _device_mesh(mesh, np.float64)
+    dev = pos.device
+    gp, gcv = engine.convert_backward(pos, col, faces, torch.as_tensor(gm).to(dev), torch.as_tensor(gc).to(dev),
+                                      torch.as_tensor(gcol).to(dev), getattr(cloud, "rescale", True))
+    return gp.cpu().numpy(), gcv.cpu().numpy()
+
+
+# ---------------------------------------------------------------------------
+# objective (losses.py:23-174): B views per device call
+# ---------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class LossWeights:
+    color: float = 1.0
+    silhouette: float = 1.0
+    edge: float = 0.1
+    laplacian: float = 0.1
+
+
+@dataclass(frozen=True)
+class LossReport:
+    color: float
+    silhouette: float
+    edge: float
+    laplacian: float
+    total: float
+    n_views: int
+
+
+def color_loss(rendered, target):
+    """MSE and its gradient (losses.py:43-56)."""
+    rendered = np.asarray(rendered, dtype=np.float64)
+    target = np.asarray(target, dtype=np.float64)
+    if rendered.shape != target.shape:
+        raise ValueError(f"shape mismatch: {rendered.shape} vs {target.shape}")
+    diff = rendered - target
+    return float(np.mean(diff * diff)), (2.0 / diff.size) * diff
+
+
+def silhouette_loss(alpha, mask):
+    """Clamped BCE and its gradient (losses.py:59-73)."""
+    alpha = np.asarray(alpha, dtype=np.float64)
+    mask = np.asarray(mask, dtype=np.float64)
+    if alpha.shape != mask.shape:
+        raise ValueError(f"shape mismatch: {alpha.shape} vs {mask.shape}")
+    p = np.clip(alpha, BCE_CLAMP, 1.0 - BCE_CLAMP)
+    value = float(-np.mean(mask * np.log(p) + (1.0 - mask) * np.log1p(-p)))
+    inside = (alpha > BCE_CLAMP) & (alpha < 1.0 - BCE_CLAMP)
+    return value, np.where(inside, (-mask / p + (1.0 - mask) / (1.0 - p)) / alpha.size, 0.0)
+
+
+def _edges(facets):
+    return np.unique(np.sort(np.asarray(facets)[:, [0, 1, 1, 2, 2, 0]].reshape(-1, 2), axis=1), axis=0)
+
+
+def edge_length_loss(mesh, vertices=None):
+    """losses.py:76-97 (mesh regulariser; evaluated once per objective)."""
+    verts = np.asarray(mesh.vertices if vertices is None else vertices, dtype=np.float64)
+    edges = _edges(mesh.facets) if len(mesh.facets) else np.zeros((0, 2), np.int64)
+    if len(edges) == 0:
+        return 0.0, np.zeros_like(verts)
+    vec = verts[edges[:, 1]] - verts[edges[:, 0]]
+    length = np.linalg.norm(vec, axis=1)
+    dev = length - length.mean()
+    coeff = (2.0 / len(edges)) * dev / np.maximum(length, 1e-12)
+    grad = np.zeros_like(verts)
+    np.add.at(grad, edges[:, 1], coeff[:, None] * vec)
+    np.add.at(grad, edges[:, 0], -coeff[:, None] * vec)
+    return float(np.mean(dev * dev)), grad
+
+
+def laplacian_loss(mesh, vertices=None):
+    """losses.py:100-123 (uniform Laplacian regulariser)."""
+    verts = np.asarray(mesh.vertices if vertices is None else vertices, dtype=np.float64)
+    nv = len(verts)
+    e = _edges(mesh.facets) if len(mesh.facets) else np.zeros((0, 2), np.int64)
+    both = np.concatenate([e, e[:, ::-1]]) if len(e) else np.zeros((0, 2), np.int64)
+    both = both[np.lexsort((both[:, 1], both[:, 0]))]
+    deg = np.bincount(both[:, 0], minlength=nv).astype(np.float64)
+    owner = both[:, 0]
+    has = deg > 0
+    nbr = np.zeros_like(verts)
+    np.add.at(nbr, owner, verts[both[:, 1]])
+    lap = np.zeros_like(verts)
+    lap[has] = verts[has] - nbr[has] / deg[has, None]
+    value = float(np.mean(np.sum(lap * lap, axis=1)))
+    scaled = np.where(has[:, None], lap / np.maximum(deg, 1.0)[:, None], 0.0)
+    back = np.zeros_like(verts)
+    np.add.at(back, both[:, 1], scaled[owner])
+    return value, (2.0 / nv) * lap - (2.0 / nv) * back
+
+
+def total_loss(mesh, cameras: Sequence[Camera], target_rgb, target_mask, weights: LossWeights = LossWeights(),
+               background=(0.0, 0.0, 0.0), rescale: bool = True, dtype=np.float64):
+    """Weighted objective over a batch of views (losses.py:126-174).  All
+    views of one resolution are rendered and differentiated in ONE device
+    call; per-view image grads are scaled by w/n exactly as the reference."""
+    if not (len(cameras) == len(target_rgb) == len(target_mask)):
+        raise ValueError("cameras and targets must have matching lengths")
+    if len(cameras) == 0:
+        raise ValueError("need at least one view")
+    n = len(cameras)
+    pos, col, faces = _device_mesh(mesh, dtype)
+    dev = pos.device
+    tdt = _torch_dtype(dtype)
+    groups = {}
+    for i, c in enumerate(cameras):
+        groups.setdefault((c.width, c.height), []).append(i)
+    grad_v = np.zeros((len(mesh.vertices), 3))
+    grad_c = np.zeros((len(mesh.vertices), 3))
+    cval = np.zeros(n)
+    sval = np.zeros(n)
+    bg = np.asarray(background, dtype=np.float64)
+    for (w, h), idx in groups.items():
+        cams = [cameras[i] for i in idx]
+        rgb, alpha, state = engine.render_forward(pos, col, faces, cams, w, h, bg, rescale)
+        t_rgb = torch.as_tensor(np.stack([np.asarray(target_rgb[i], np.float64) for i in idx])).to(dev)
+        t_m = torch.as_tensor(np.stack([np.asarray(target_mask[i], np.float64) for i in idx])).to(dev)
+        if t_rgb.shape != rgb.shape or t_m.shape != alpha.shape:
+            raise ValueError("shape mismatch between renders and targets")
+        r64, a64 = rgb.double(), alpha.double()
+        diff = r64 - t_rgb
+        cval[idx] = (diff * diff).mean(dim=(1, 2, 3)).cpu().numpy()
+        g_rgb = (2.0 / diff[0].numel()) * diff * (weights.color / n)
+        p = a64.clamp(BCE_CLAMP, 1.0 - BCE_CLAMP)
+        sval[idx] = (-(t_m * torch.log(p) + (1.0 - t_m) * torch.log1p(-p))).mean(dim=(1, 2)).cpu().numpy()
+        inside = (a64 > BCE_CLAMP) & (a64 < 1.0 - BCE_CLAMP)
+        g_a = torch.where(inside, (-t_m / p + (1.0 - t_m) / (1.0 - p)) / a64[0].numel(),
+                          torch.zeros_like(a64)) * (weights.silhouette / n)
+        gp, gc = engine.render_backward(state, pos, col, faces, rgb, g_rgb.to(tdt), g_a.to(tdt))
+        grad_v += gp.double().cpu().numpy()
+        grad_c += gc.double().cpu().numpy()
+    color_val = float(cval.sum() / n)
+    sil_val = float(sval.sum() / n)
+    edge_val, g_edge = edge_length_loss(mesh)
+    lap_val, g_lap = laplacian_loss(mesh)
+    grad_v += weights.edge * g_edge + weights.laplacian * g_lap
+    total = (weights.color * color_val + weights.silhouette * sil_val
+             + weights.edge * edge_val + weights.laplacian * lap_val)
+    return LossReport(color=color_val, silhouette=sil_val, edge=edge_val, laplacian=lap_val,
+                      total=total, n_views=n), grad_v, grad_c

@@ -1,0 +1,626 @@
+// gmr_capi.cu — extern "C" entry points of libgmr.so (see include/gmr.h).
+//
+// Host-side sequencing of the kernels in gmr_kernels.cuh.  The library
+// never allocates: every buffer lives in the caller's workspace, carved by
+// `plan()` identically for the size query, the forward and the backward.
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+
+#include "gmr_kernels.cuh"
+
+using namespace gmr;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define GMR_CUDA(call)                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess) return fail(GMR_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+#define GMR_LAUNCHED()                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = cudaGetLastError();                                                 \
+    if (e_ != cudaSuccess) return fail(GMR_ECUDA, "launch: %s (%s:%d)", cudaGetErrorString(e_), __FILE__, __LINE__); \
+  } while (0)
+
+inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+inline int ceil_log2(uint64_t x) {
+  int b = 0;
+  while ((1ull << b) < x) ++b;
+  return b;
+}
+inline unsigned grid_for(uint64_t n, unsigned block) { return (unsigned)std::max<uint64_t>(1, (n + block - 1) / block); }
+
+// Workspace layout (byte offsets).
+struct Layout {
+  size_t status, splat, col4, rect, count, dkey[2], ditem[2], offs, entry_off, bsum, nent;
+  size_t ekey[2], eval[2], bounds, t_final, hist, partial, partial_op, face_acc, corner, aux;
+  size_t total;
+  uint64_t items, faces, bins, pixels, ecap;
+  int views, tiles_x, tiles_y, tiles;
+  int depth_bits, entry_bits;
+};
+
+Layout plan(uint64_t faces, int views, int W, int H, uint64_t ecap, int dtype, bool mesh) {
+  Layout L{};
+  const size_t s = dtype == GMR_F64 ? 8 : 4;
+  L.faces = faces;
+  L.views = views;
+  L.items = faces * (uint64_t)views;
+  L.tiles_x = (W + kTile - 1) / kTile;
+  L.tiles_y = (H + kTile - 1) / kTile;
+  L.tiles = L.tiles_x * L.tiles_y;
+  L.bins = (uint64_t)L.tiles * views;
+  L.pixels = (uint64_t)W * H * views;
+  L.ecap = ecap;
+  L.depth_bits = dtype == GMR_F64 ? 64 : 32;
+  L.entry_bits = std::max(1, ceil_log2(L.bins));
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + std::max<size_t>(bytes, 1)); return r; };
+  const size_t ks = dtype == GMR_F64 ? 8 : 4;
+  L.status = take(sizeof(DevStatus));
+  L.splat = take(L.items * 8 * s);
+  L.col4 = take(faces * 4 * s);
+  L.rect = take(L.items * 8);
+  L.count = take(L.items * 4);
+  L.dkey[0] = take(L.items * ks);
+  L.dkey[1] = take(L.items * ks);
+  L.ditem[0] = take(L.items * 4);
+  L.ditem[1] = take(L.items * 4);
+  L.offs = take(L.items * 4);
+  L.entry_off = take(L.items * 4);
+  L.bsum = take(((L.items + kScanTile - 1) / kScanTile + 1) * 4);
+  L.nent = take(16);
+  L.ekey[0] = take(ecap * 4);
+  L.ekey[1] = take(ecap * 4);
+  L.eval[0] = take(ecap * 4);
+  L.eval[1] = take(ecap * 4);
+  L.bounds = take((L.bins + 1) * 4);
+  L.t_final = take(L.pixels * s);
+  L.hist = take(std::max(radix_hist_words((uint32_t)std::min<uint64_t>(L.items, 0xffffffffu)),
+                         radix_hist_words((uint32_t)std::min<uint64_t>(ecap, 0xffffffffu))) * 4);
+  L.partial = take(ecap * 8 * s);
+  L.partial_op = take(mesh ? 0 : ecap * s);
+  L.face_acc = take(mesh ? faces * 12 * s : 0);
+  L.corner = take(mesh ? faces * 18 * s : 0);
+  L.aux = take(mesh ? L.items * 2 * s : 0);
+  L.total = o;
+  return L;
+}
+
+template <typename T> inline T* at(void* ws, size_t off) { return reinterpret_cast<T*>((char*)ws + off); }
+
+int check_raster(const GmrRaster* r) {
+  if (!r) return fail(GMR_EINVAL, "raster settings are null");
+  if (r->width < 1 || r->height < 1) return fail(GMR_EINVAL, "width and height must be >= 1");
+  if ((int64_t)r->width > 16 * 65535 || (int64_t)r->height > 16 * 65535)
+    return fail(GMR_EINVAL, "image too large");
+  if (r->dtype != GMR_F32 && r->dtype != GMR_F64) return fail(GMR_EINVAL, "dtype must be GMR_F32 or GMR_F64");
+  return GMR_OK;
+}
+
+template <typename S>
+CamBatch<S> make_cams(const GmrCamera* cams, int v0, int nv) {
+  CamBatch<S> b;
+  memset(&b, 0, sizeof(b));
+  b.count = nv;
+  for (int i = 0; i < nv; ++i) {
+    const GmrCamera& c = cams[v0 + i];
+    Cam<S>& d = b.cam[i];
+    for (int k = 0; k < 9; ++k) d.R[k] = (S)c.R[k];
+    for (int k = 0; k < 3; ++k) d.t[k] = (S)c.t[k];
+    d.fx = (S)c.fx; d.fy = (S)c.fy; d.cx = (S)c.cx; d.cy = (S)c.cy;
+    d.near_plane = (S)c.near_plane; d.far_plane = (S)c.far_plane;
+  }
+  return b;
+}
+
+// Binning (K2) + blend forward (K3) over prepared item records.
+template <typename S>
+int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void* alpha,
+                  cudaStream_t st) {
+  typedef typename KeyOf<S>::type K;
+  const uint32_t items = (uint32_t)L.items;
+  // depth order of all items (stable: ties keep item = (view, face) order)
+  K* dk[2] = {at<K>(ws, L.dkey[0]), at<K>(ws, L.dkey[1])};
+  uint32_t* di[2] = {at<uint32_t>(ws, L.ditem[0]), at<uint32_t>(ws, L.ditem[1])};
+  int cur = radix_sort_pairs<K>(dk, di, nullptr, items, items, L.depth_bits, at<uint32_t>(ws, L.hist), st);
+  GMR_LAUNCHED();
+  const uint32_t* order = di[cur];
+  const uint32_t* count = at<uint32_t>(ws, L.count);
+  const int nb = (int)((items + kScanTile - 1) / kScanTile);
+  uint32_t* bsum = at<uint32_t>(ws, L.bsum);
+  uint32_t* nent = at<uint32_t>(ws, L.nent);
+  DevStatus* dst = at<DevStatus>(ws, L.status);
+  if (items) {
+    scan_reduce<<<nb, 256, 0, st>>>(order, count, items, bsum);
+    GMR_LAUNCHED();
+  }
+  scan_top<<<1, 256, 0, st>>>(bsum, nb, dst, (unsigned long long)L.ecap, nent);
+  GMR_LAUNCHED();
+  if (items) {
+    scan_apply<<<nb, 256, 0, st>>>(order, count, items, bsum, at<uint32_t>(ws, L.offs),
+                                   at<uint32_t>(ws, L.entry_off));
+    GMR_LAUNCHED();
+  }
+  uint32_t* ek[2] = {at<uint32_t>(ws, L.ekey[0]), at<uint32_t>(ws, L.ekey[1])};
+  uint32_t* ev[2] = {at<uint32_t>(ws, L.eval[0]), at<uint32_t>(ws, L.eval[1])};
+  if (items) {
+    emit_entries<<<grid_for(items, 256), 256, 0, st>>>(order, count, at<uint32_t>(ws, L.offs),
+                                                       at<uint2>(ws, L.rect), items,
+                                                       (uint32_t)L.faces, L.tiles_x, (uint32_t)L.tiles,
+                                                       nent, ek[0], ev[0]);
+    GMR_LAUNCHED();
+  }
+  const uint32_t ecap = (uint32_t)std::min<uint64_t>(L.ecap, 0xffffffffu);
+  int ecur = radix_sort_pairs<uint32_t>(ek, ev, nent, 0, ecap, L.entry_bits, at<uint32_t>(ws, L.hist), st);
+  GMR_LAUNCHED();
+  tile_ranges<<<grid_for((uint64_t)ecap + 1, 256), 256, 0, st>>>(ek[ecur], nent, 0, (uint32_t)L.bins,
+                                                                at<uint32_t>(ws, L.bounds));
+  GMR_LAUNCHED();
+  BlendArgs<S> a{};
+  a.bounds = at<uint32_t>(ws, L.bounds);
+  a.entry_item = ev[ecur];
+  a.splat = at<Splat<S>>(ws, L.splat);
+  a.col4 = at<V4<S>>(ws, L.col4);
+  a.rect = at<uint2>(ws, L.rect);
+  a.entry_off = at<uint32_t>(ws, L.entry_off);
+  a.items_per_view = (uint32_t)L.faces;
+  a.tiles_x = L.tiles_x;
+  a.tiles_per_view = (uint32_t)L.tiles;
+  a.W = r->width;
+  a.H = r->height;
+  a.bg0 = (S)r->background[0];
+  a.bg1 = (S)r->background[1];
+  a.bg2 = (S)r->background[2];
+  a.rgb = (S*)rgb;
+  a.alpha = (S*)alpha;
+  a.t_final = at<S>(ws, L.t_final);
+  if (L.bins) {
+    blend_forward<S><<<(unsigned)L.bins, kBlendThreads, 0, st>>>(a);
+    GMR_LAUNCHED();
+  }
+  return GMR_OK;
+}
+
+template <typename S>
+int render_forward_t(const GmrMesh* m, const GmrCamera* cams, int B, const GmrRaster* r, void* rgb,
+                     void* alpha, void* ws, const Layout& L, cudaStream_t st) {
+  reset_status<<<1, 1, 0, st>>>(at<DevStatus>(ws, L.status));
+  GMR_LAUNCHED();
+  const uint64_t F = L.faces;
+  for (int v0 = 0; v0 < B; v0 += kMaxViewsPerLaunch) {
+    const int nv = std::min(kMaxViewsPerLaunch, B - v0);
+    MeshFwdArgs<S> a{};
+    a.pos = (const S*)m->positions;
+    a.col = (const S*)m->colors;
+    a.faces = m->faces;
+    a.F = (int64_t)F;
+    a.view0 = v0;
+    a.nviews = nv;
+    a.W = r->width;
+    a.H = r->height;
+    a.tiles_x = L.tiles_x;
+    a.tiles_y = L.tiles_y;
+    a.rescale = r->rescale;
+    a.splat = at<Splat<S>>(ws, L.splat);
+    a.col4 = at<V4<S>>(ws, L.col4);
+    a.rect = at<uint2>(ws, L.rect);
+    a.count = at<uint32_t>(ws, L.count);
+    a.dkey = at<typename KeyOf<S>::type>(ws, L.dkey[0]);
+    a.ditem = at<uint32_t>(ws, L.ditem[0]);
+    a.aux = (r->flags & GMR_FLAG_DEBUG_AUX) ? at<S>(ws, L.aux) : nullptr;
+    a.st = at<DevStatus>(ws, L.status);
+    if (F) {
+      mesh_to_splats<S><<<grid_for(F, 256), 256, 0, st>>>(a, make_cams<S>(cams, v0, nv));
+      GMR_LAUNCHED();
+    }
+  }
+  return bin_and_blend<S>(L, ws, r, rgb, alpha, st);
+}
+
+template <typename S, bool kOpacity>
+int blend_backward_launch(const Layout& L, void* ws, const GmrRaster* r, const void* rgb,
+                          const void* g_rgb, const void* g_alpha, cudaStream_t st) {
+  const uint32_t ecur = (uint32_t)(((L.entry_bits + 7) / 8) & 1);
+  BlendArgs<S> a{};
+  a.bounds = at<uint32_t>(ws, L.bounds);
+  a.entry_item = at<uint32_t>(ws, L.eval[ecur]);
+  a.splat = at<Splat<S>>(ws, L.splat);
+  a.col4 = at<V4<S>>(ws, L.col4);
+  a.rect = at<uint2>(ws, L.rect);
+  a.entry_off = at<uint32_t>(ws, L.entry_off);
+  a.items_per_view = (uint32_t)L.faces;
+  a.tiles_x = L.tiles_x;
+  a.tiles_per_view = (uint32_t)L.tiles;
+  a.W = r->width;
+  a.H = r->height;
+  a.bg0 = (S)r->background[0];
+  a.bg1 = (S)r->background[1];
+  a.bg2 = (S)r->background[2];
+  a.rgb = (S*)rgb;
+  a.t_final = at<S>(ws, L.t_final);
+  a.g_rgb = (const S*)g_rgb;
+  a.g_alpha = (const S*)g_alpha;
+  a.partial = at<S>(ws, L.partial);
+  a.partial_op = kOpacity ? at<S>(ws, L.partial_op) : nullptr;
+  const size_t dyn = (size_t)8 * kBlendThreads * 8 * sizeof(S) + (kOpacity ? (size_t)8 * kBlendThreads * sizeof(S) : 0);
+  GMR_CUDA(cudaFuncSetAttribute(blend_backward<S, kOpacity>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+  if (L.bins) {
+    blend_backward<S, kOpacity><<<(unsigned)L.bins, kBlendThreads, dyn, st>>>(a);
+    GMR_LAUNCHED();
+  }
+  return GMR_OK;
+}
+
+template <typename S>
+int render_backward_t(const GmrMesh* m, const GmrCamera* cams, int B, const GmrRaster* r,
+                      const void* rgb, const void* g_rgb, const void* g_alpha, void* g_pos,
+                      void* g_col, const void* topo, void* ws, const Layout& L, cudaStream_t st) {
+  int rc = blend_backward_launch<S, false>(L, ws, r, rgb, g_rgb, g_alpha, st);
+  if (rc) return rc;
+  const uint64_t F = L.faces, V = (uint64_t)m->num_vertices;
+  for (int v0 = 0; v0 < B; v0 += kMaxViewsPerLaunch) {
+    const int nv = std::min(kMaxViewsPerLaunch, B - v0);
+    FaceBwdArgs<S> a{};
+    a.pos = (const S*)m->positions;
+    a.faces = m->faces;
+    a.F = (int64_t)F;
+    a.view0 = v0;
+    a.nviews = nv;
+    a.rescale = r->rescale;
+    a.count = at<uint32_t>(ws, L.count);
+    a.entry_off = at<uint32_t>(ws, L.entry_off);
+    a.splat = at<Splat<S>>(ws, L.splat);
+    a.partial = at<S>(ws, L.partial);
+    a.face_acc = at<S>(ws, L.face_acc);
+    if (F) {
+      face_views_backward<S><<<grid_for(F, 128), 128, 0, st>>>(a, make_cams<S>(cams, v0, nv));
+      GMR_LAUNCHED();
+    }
+  }
+  if (F) {
+    face_convert_backward<S><<<grid_for(F, 128), 128, 0, st>>>((const S*)m->positions, m->faces, (int64_t)F,
+                                                               r->rescale, at<S>(ws, L.face_acc),
+                                                               at<S>(ws, L.corner));
+    GMR_LAUNCHED();
+  }
+  const uint32_t* vstart = (const uint32_t*)topo;
+  const uint32_t* slots = vstart + align_up((V + 1) * 4) / 4;
+  if (V) {
+    vertex_gather<S><<<grid_for(V, 256), 256, 0, st>>>(vstart, slots, (int64_t)V, (int64_t)F,
+                                                       at<S>(ws, L.corner), (S*)g_pos, (S*)g_col);
+    GMR_LAUNCHED();
+  }
+  return GMR_OK;
+}
+
+int check_mesh(const GmrMesh* m) {
+  if (!m) return fail(GMR_EINVAL, "mesh is null");
+  if (m->num_faces < 0 || m->num_vertices < 0) return fail(GMR_EINVAL, "negative mesh sizes");
+  if (m->num_faces > 0 && (!m->positions || !m->faces || !m->colors))
+    return fail(GMR_EINVAL, "mesh buffers are null");
+  if (m->num_vertices >= (1ll << 31) || 3 * m->num_faces >= (1ll << 31))
+    return fail(GMR_EINVAL, "mesh too large for 32-bit indices");
+  return GMR_OK;
+}
+
+template <typename S>
+int rasterize_forward_t(const GmrSplats* sp, const GmrRaster* r, void* rgb, void* alpha, void* ws,
+                        const Layout& L, cudaStream_t st) {
+  reset_status<<<1, 1, 0, st>>>(at<DevStatus>(ws, L.status));
+  GMR_LAUNCHED();
+  PackArgs<S> a{};
+  a.mean2d = (const S*)sp->mean2d;
+  a.cov2d = (const S*)sp->cov2d;
+  a.depth = (const S*)sp->depth;
+  a.color = (const S*)sp->color;
+  a.opacity = (const S*)sp->opacity;
+  a.K = sp->count;
+  a.tiles_x = L.tiles_x;
+  a.tiles_y = L.tiles_y;
+  a.splat = at<Splat<S>>(ws, L.splat);
+  a.col4 = at<V4<S>>(ws, L.col4);
+  a.rect = at<uint2>(ws, L.rect);
+  a.count = at<uint32_t>(ws, L.count);
+  a.dkey = at<typename KeyOf<S>::type>(ws, L.dkey[0]);
+  a.ditem = at<uint32_t>(ws, L.ditem[0]);
+  a.st = at<DevStatus>(ws, L.status);
+  if (sp->count) {
+    pack_splats<S><<<grid_for(sp->count, 256), 256, 0, st>>>(a);
+    GMR_LAUNCHED();
+  }
+  return bin_and_blend<S>(L, ws, r, rgb, alpha, st);
+}
+
+int check_splats(const GmrSplats* sp) {
+  if (!sp || sp->count < 0) return fail(GMR_EINVAL, "bad splats");
+  if (sp->count && (!sp->mean2d || !sp->cov2d || !sp->depth || !sp->color || !sp->opacity))
+    return fail(GMR_EINVAL, "splat buffers are null");
+  if (sp->count >= (1ll << 31)) return fail(GMR_EINVAL, "too many splats");
+  return GMR_OK;
+}
+
+template <typename S>
+int rasterize_backward_t(const GmrSplats* sp, const GmrRaster* r, const void* rgb, const void* g_rgb,
+                         const void* g_alpha, void* gm, void* gc, void* gcol, void* gop, void* ws,
+                         const Layout& L, cudaStream_t st) {
+  int rc = blend_backward_launch<S, true>(L, ws, r, rgb, g_rgb, g_alpha, st);
+  if (rc) return rc;
+  if (sp->count) {
+    splat_grads<S><<<grid_for(sp->count, 256), 256, 0, st>>>(
+        at<uint32_t>(ws, L.count), at<uint32_t>(ws, L.entry_off), at<Splat<S>>(ws, L.splat),
+        at<S>(ws, L.partial), at<S>(ws, L.partial_op), sp->count, (S*)gm, (S*)gc, (S*)gcol, (S*)gop);
+    GMR_LAUNCHED();
+  }
+  return GMR_OK;
+}
+
+template <typename S>
+int convert_backward_t(const GmrMesh* m, int rescale, const void* gm, const void* gc, const void* gcol, void* gp,
+                       void* gcv, const void* topo, void* scratch, cudaStream_t st) {
+  const int64_t F = m->num_faces, V = m->num_vertices;
+  S* acc = (S*)scratch;
+  S* corner = (S*)((char*)scratch + align_up(F * 12 * sizeof(S)));
+  if (F) {
+    pack_face_grads<S><<<grid_for(F, 256), 256, 0, st>>>((const S*)gm, (const S*)gc, (const S*)gcol, F, acc);
+    GMR_LAUNCHED();
+    face_convert_backward<S><<<grid_for(F, 128), 128, 0, st>>>((const S*)m->positions, m->faces, F, rescale, acc, corner);
+    GMR_LAUNCHED();
+  }
+  const uint32_t* vstart = (const uint32_t*)topo;
+  const uint32_t* slots = vstart + align_up((V + 1) * 4) / 4;
+  if (V) {
+    vertex_gather<S><<<grid_for(V, 256), 256, 0, st>>>(vstart, slots, V, F, corner, (S*)gp, (S*)gcv);
+    GMR_LAUNCHED();
+  }
+  return GMR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* gmr_last_error(void) { return g_err.c_str(); }
+const char* gmr_version(void) { return "gmr-b200 0.1 (sm_100a)"; }
+
+int gmr_render_workspace_size(int64_t F, int32_t B, int32_t W, int32_t H, int64_t ecap, int32_t dtype,
+                              size_t* bytes) {
+  if (!bytes || F < 0 || B < 1 || W < 1 || H < 1 || ecap < 0) return fail(GMR_EINVAL, "bad workspace sizes");
+  if ((uint64_t)F * B >= 0xffffffffull) return fail(GMR_EINVAL, "faces*views must be < 2^32");
+  if (dtype != GMR_F32 && dtype != GMR_F64) return fail(GMR_EINVAL, "bad dtype");
+  *bytes = plan((uint64_t)F, B, W, H, (uint64_t)ecap, dtype, true).total;
+  return GMR_OK;
+}
+
+int gmr_render_forward(const GmrMesh* mesh, const GmrCamera* cams, int32_t B, const GmrRaster* r,
+                       void* rgb, void* alpha, void* ws, size_t ws_bytes, int64_t ecap, void* stream) {
+  int rc = check_mesh(mesh);
+  if (rc) return rc;
+  if ((rc = check_raster(r))) return rc;
+  if (!cams || B < 1 || B > GMR_MAX_VIEWS_PER_CALL) return fail(GMR_EINVAL, "need 1..%d cameras", GMR_MAX_VIEWS_PER_CALL);
+  if (!rgb || !alpha || !ws) return fail(GMR_EINVAL, "output or workspace pointer is null");
+  if ((uint64_t)mesh->num_faces * B >= 0xffffffffull) return fail(GMR_EINVAL, "faces*views must be < 2^32");
+  const Layout L = plan((uint64_t)mesh->num_faces, B, r->width, r->height, (uint64_t)ecap, r->dtype, true);
+  if (ws_bytes < L.total) return fail(GMR_EWORKSPACE, "workspace has %zu bytes, needs %zu", ws_bytes, L.total);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (r->dtype == GMR_F64) return render_forward_t<double>(mesh, cams, B, r, rgb, alpha, ws, L, st);
+  return render_forward_t<float>(mesh, cams, B, r, rgb, alpha, ws, L, st);
+}
+
+int gmr_status(const void* ws, GmrStatus* out, void* stream) {
+  if (!ws || !out) return fail(GMR_EINVAL, "null argument");
+  DevStatus h;
+  GMR_CUDA(cudaMemcpyAsync(&h, ws, sizeof(h), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  GMR_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  out->entries = (int64_t)h.entries;
+  out->kept = (int64_t)h.kept;
+  out->overflow = (int32_t)h.overflow;
+  out->entry_capacity = -1;
+  out->nonfinite_field = -1;
+  out->nonfinite_item = -1;
+  for (int i = 0; i < 6; ++i)
+    if (h.bad_item[i] != 0xffffffffu) {
+      out->nonfinite_field = i;
+      out->nonfinite_item = h.bad_item[i];
+      break;
+    }
+  if (out->nonfinite_field >= 0)
+    return fail(GMR_ENONFINITE, "non-finite splat parameter (field %d) at item %lld", out->nonfinite_field,
+                (long long)out->nonfinite_item);
+  if (h.overflow)
+    return fail(GMR_ECAPACITY, "%llu tile entries exceed the capacity", (unsigned long long)h.entries);
+  return GMR_OK;
+}
+
+int gmr_topology_size(int64_t F, int64_t V, size_t* bytes) {
+  if (!bytes || F < 0 || V < 0) return fail(GMR_EINVAL, "bad topology sizes");
+  const uint64_t n = 3 * (uint64_t)F;
+  size_t o = align_up((V + 1) * 4) + align_up(n * 4);            // vstart, slots (result)
+  o += 4 * align_up(n * 4) + align_up(radix_hist_words((uint32_t)n) * 4);  // sort scratch
+  *bytes = o;
+  return GMR_OK;
+}
+
+int gmr_topology_build(const int32_t* faces, int64_t F, int64_t V, void* topo, size_t bytes, void* stream) {
+  size_t need;
+  int rc = gmr_topology_size(F, V, &need);
+  if (rc) return rc;
+  if (bytes < need) return fail(GMR_EWORKSPACE, "topology buffer has %zu bytes, needs %zu", bytes, need);
+  if (F > 0 && !faces) return fail(GMR_EINVAL, "faces is null");
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint64_t n = 3 * (uint64_t)F;
+  char* base = (char*)topo;
+  uint32_t* vstart = (uint32_t*)base;
+  uint32_t* slots = (uint32_t*)(base + align_up((V + 1) * 4));
+  char* scratch = (char*)slots + align_up(n * 4);
+  uint32_t* k[2] = {(uint32_t*)scratch, (uint32_t*)(scratch + align_up(n * 4))};
+  uint32_t* v[2] = {(uint32_t*)(scratch + 2 * align_up(n * 4)), (uint32_t*)(scratch + 3 * align_up(n * 4))};
+  uint32_t* hist = (uint32_t*)(scratch + 4 * align_up(n * 4));
+  if (n) {
+    topo_keys<<<grid_for(n, 256), 256, 0, st>>>(faces, F, k[0], v[0]);
+    GMR_LAUNCHED();
+  }
+  const int bits = std::max(1, ceil_log2((uint64_t)std::max<int64_t>(V, 1)));
+  int cur = radix_sort_pairs<uint32_t>(k, v, nullptr, (uint32_t)n, (uint32_t)n, bits, hist, st);
+  GMR_LAUNCHED();
+  tile_ranges<<<grid_for(n + 1, 256), 256, 0, st>>>(k[cur], nullptr, (uint32_t)n, (uint32_t)V, vstart);
+  GMR_LAUNCHED();
+  GMR_CUDA(cudaMemcpyAsync(slots, v[cur], n * 4, cudaMemcpyDeviceToDevice, st));
+  return GMR_OK;
+}
+
+int gmr_render_backward(const GmrMesh* mesh, const GmrCamera* cams, int32_t B, const GmrRaster* r,
+                        const void* rgb, const void* g_rgb, const void* g_alpha, void* g_pos, void* g_col,
+                        const void* topo, void* ws, size_t ws_bytes, int64_t ecap, void* stream) {
+  int rc = check_mesh(mesh);
+  if (rc) return rc;
+  if ((rc = check_raster(r))) return rc;
+  if (!cams || B < 1 || B > GMR_MAX_VIEWS_PER_CALL) return fail(GMR_EINVAL, "need 1..%d cameras", GMR_MAX_VIEWS_PER_CALL);
+  if (!rgb || !g_rgb || !g_alpha || !g_pos || !g_col || !topo || !ws) return fail(GMR_EINVAL, "null pointer argument");
+  const uint64_t F = (uint64_t)mesh->num_faces;
+  const Layout L = plan(F, B, r->width, r->height, (uint64_t)ecap, r->dtype, true);
+  if (ws_bytes < L.total) return fail(GMR_EWORKSPACE, "workspace has %zu bytes, needs %zu", ws_bytes, L.total);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (r->dtype == GMR_F64)
+    return render_backward_t<double>(mesh, cams, B, r, rgb, g_rgb, g_alpha, g_pos, g_col, topo, ws, L, st);
+  return render_backward_t<float>(mesh, cams, B, r, rgb, g_rgb, g_alpha, g_pos, g_col, topo, ws, L, st);
+}
+
+// ---- splat path ----------------------------------------------------------
+
+int gmr_raster_workspace_size(int64_t K, int32_t W, int32_t H, int64_t ecap, int32_t dtype, size_t* bytes) {
+  if (!bytes || K < 0 || W < 1 || H < 1 || ecap < 0) return fail(GMR_EINVAL, "bad workspace sizes");
+  if (dtype != GMR_F32 && dtype != GMR_F64) return fail(GMR_EINVAL, "bad dtype");
+  *bytes = plan((uint64_t)K, 1, W, H, (uint64_t)ecap, dtype, false).total;
+  return GMR_OK;
+}
+
+int gmr_rasterize_forward(const GmrSplats* sp, const GmrRaster* r, void* rgb, void* alpha, void* ws,
+                          size_t ws_bytes, int64_t ecap, void* stream) {
+  int rc = check_splats(sp);
+  if (rc) return rc;
+  if ((rc = check_raster(r))) return rc;
+  if (!rgb || !alpha || !ws) return fail(GMR_EINVAL, "output or workspace pointer is null");
+  const Layout L = plan((uint64_t)sp->count, 1, r->width, r->height, (uint64_t)ecap, r->dtype, false);
+  if (ws_bytes < L.total) return fail(GMR_EWORKSPACE, "workspace has %zu bytes, needs %zu", ws_bytes, L.total);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (r->dtype == GMR_F64) return rasterize_forward_t<double>(sp, r, rgb, alpha, ws, L, st);
+  return rasterize_forward_t<float>(sp, r, rgb, alpha, ws, L, st);
+}
+
+int gmr_rasterize_backward(const GmrSplats* sp, const GmrRaster* r, const void* rgb, const void* g_rgb,
+                           const void* g_alpha, void* gm, void* gc, void* gcol, void* gop, void* ws,
+                           size_t ws_bytes, int64_t ecap, void* stream) {
+  int rc = check_splats(sp);
+  if (rc) return rc;
+  if ((rc = check_raster(r))) return rc;
+  if (!rgb || !g_rgb || !g_alpha || !gm || !gc || !gcol || !gop || !ws) return fail(GMR_EINVAL, "null pointer argument");
+  const uint64_t K = (uint64_t)sp->count;
+  const Layout L = plan(K, 1, r->width, r->height, (uint64_t)ecap, r->dtype, false);
+  if (ws_bytes < L.total) return fail(GMR_EWORKSPACE, "workspace has %zu bytes, needs %zu", ws_bytes, L.total);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (r->dtype == GMR_F64) return rasterize_backward_t<double>(sp, r, rgb, g_rgb, g_alpha, gm, gc, gcol, gop, ws, L, st);
+  return rasterize_backward_t<float>(sp, r, rgb, g_rgb, g_alpha, gm, gc, gcol, gop, ws, L, st);
+}
+
+// ---- inspection ------------------------------------------------------------
+
+int gmr_copy_entries(const void* ws, int64_t items_per_view, int32_t views, const GmrRaster* r, int64_t ecap,
+                     int32_t mesh_path, uint32_t* entry_items, uint32_t* bounds, void* stream) {
+  int rc = check_raster(r);
+  if (rc) return rc;
+  if (!ws || !entry_items || !bounds || views < 1) return fail(GMR_EINVAL, "bad arguments");
+  const Layout L = plan((uint64_t)items_per_view, views, r->width, r->height, (uint64_t)ecap, r->dtype, mesh_path != 0);
+  DevStatus h;
+  cudaStream_t st = (cudaStream_t)stream;
+  GMR_CUDA(cudaMemcpyAsync(&h, ws, sizeof(h), cudaMemcpyDeviceToHost, st));
+  GMR_CUDA(cudaStreamSynchronize(st));
+  if (h.overflow) return fail(GMR_ECAPACITY, "forward overflowed its entry capacity");
+  const uint32_t ecur = (uint32_t)(((L.entry_bits + 7) / 8) & 1);
+  if (h.entries)
+    GMR_CUDA(cudaMemcpyAsync(entry_items, (const char*)ws + L.eval[ecur], h.entries * 4, cudaMemcpyDeviceToDevice, st));
+  GMR_CUDA(cudaMemcpyAsync(bounds, (const char*)ws + L.bounds, (L.bins + 1) * 4, cudaMemcpyDeviceToDevice, st));
+  return GMR_OK;
+}
+
+int gmr_copy_splats(const void* ws, int64_t items_per_view, int32_t views, const GmrRaster* r, int64_t ecap,
+                    int32_t mesh_path, void* records, void* rects, uint32_t* counts, void* aux, void* stream) {
+  int rc = check_raster(r);
+  if (rc) return rc;
+  if (!ws || !records || !rects || !counts || views < 1) return fail(GMR_EINVAL, "bad arguments");
+  const Layout L = plan((uint64_t)items_per_view, views, r->width, r->height, (uint64_t)ecap, r->dtype, mesh_path != 0);
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t s = r->dtype == GMR_F64 ? 8 : 4;
+  GMR_CUDA(cudaMemcpyAsync(records, (const char*)ws + L.splat, L.items * 8 * s, cudaMemcpyDeviceToDevice, st));
+  GMR_CUDA(cudaMemcpyAsync(rects, (const char*)ws + L.rect, L.items * 8, cudaMemcpyDeviceToDevice, st));
+  GMR_CUDA(cudaMemcpyAsync(counts, (const char*)ws + L.count, L.items * 4, cudaMemcpyDeviceToDevice, st));
+  if (aux && mesh_path)
+    GMR_CUDA(cudaMemcpyAsync(aux, (const char*)ws + L.aux, L.items * 2 * s, cudaMemcpyDeviceToDevice, st));
+  return GMR_OK;
+}
+
+// ---- single stages ---------------------------------------------------------
+
+int gmr_convert(const GmrMesh* mesh, int32_t rescale, int32_t dtype, void* means, void* cov3d, void* colors,
+                uint8_t* degenerate, void* stream) {
+  int rc = check_mesh(mesh);
+  if (rc) return rc;
+  if (dtype != GMR_F32 && dtype != GMR_F64) return fail(GMR_EINVAL, "bad dtype");
+  if (!means || !cov3d || !colors) return fail(GMR_EINVAL, "null output");
+  const int64_t F = mesh->num_faces;
+  if (!F) return GMR_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == GMR_F64)
+    convert_forward<double><<<grid_for(F, 128), 128, 0, st>>>((const double*)mesh->positions, (const double*)mesh->colors,
+                                                              mesh->faces, F, rescale, (double*)means, (double*)cov3d,
+                                                              (double*)colors, degenerate);
+  else
+    convert_forward<float><<<grid_for(F, 128), 128, 0, st>>>((const float*)mesh->positions, (const float*)mesh->colors,
+                                                             mesh->faces, F, rescale, (float*)means, (float*)cov3d,
+                                                             (float*)colors, degenerate);
+  GMR_LAUNCHED();
+  return GMR_OK;
+}
+
+int gmr_convert_scratch_size(int64_t F, int32_t dtype, size_t* bytes) {
+  if (!bytes || F < 0) return fail(GMR_EINVAL, "bad sizes");
+  const size_t s = dtype == GMR_F64 ? 8 : 4;
+  *bytes = align_up(F * 12 * s) + align_up(F * 18 * s);
+  return GMR_OK;
+}
+
+int gmr_convert_backward(const GmrMesh* mesh, int32_t rescale, int32_t dtype, const void* gm, const void* gc,
+                         const void* gcol, void* gp, void* gcv, const void* topo, void* scratch, size_t scratch_bytes,
+                         void* stream) {
+  int rc = check_mesh(mesh);
+  if (rc) return rc;
+  size_t need;
+  if ((rc = gmr_convert_scratch_size(mesh->num_faces, dtype, &need))) return rc;
+  if (scratch_bytes < need) return fail(GMR_EWORKSPACE, "scratch too small");
+  if (!gm || !gc || !gcol || !gp || !gcv || !topo) return fail(GMR_EINVAL, "null pointer argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == GMR_F64) return convert_backward_t<double>(mesh, rescale, gm, gc, gcol, gp, gcv, topo, scratch, st);
+  return convert_backward_t<float>(mesh, rescale, gm, gc, gcol, gp, gcv, topo, scratch, st);
+}
+
+}  // extern "C"

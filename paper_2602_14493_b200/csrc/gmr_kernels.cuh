@@ -1,0 +1,1071 @@
+// gmr_kernels.cuh — the GMR hot path as sm_100a CUDA kernels.
+//
+//   K1 mesh_to_splats      convert.py:239-276,321-326 + render.py:103-145
+//   K1' pack_splats        render.py:168-188 (rasterize() stage input)
+//   K2 depth sort -> count scan -> emit_entries -> tile sort -> tile_ranges
+//                          render.py:200-229 (_RasterPlan)
+//   K3 blend_forward       render.py:244-291
+//   K4 blend_backward      render.py:294-361
+//   K5 face_views_backward render.py:364-402 (+ conic->cov, :349-360)
+//      face_convert_backward convert.py:393-425
+//   K6 vertex_gather       convert.py:427-436 (np.add.at order, via CSR)
+//
+// Items: item = view * F + face (mesh path) or the splat index (splat path).
+#pragma once
+
+#include "gmr_common.cuh"
+#include "radix_sort.cuh"
+
+namespace gmr {
+
+// ---------------------------------------------------------------------------
+// status
+// ---------------------------------------------------------------------------
+
+__global__ void reset_status(DevStatus* st) {
+  st->entries = 0;
+  st->kept = 0;
+  for (int i = 0; i < 6; ++i) st->bad_item[i] = 0xffffffffu;
+  st->overflow = 0;
+}
+
+__device__ __forceinline__ void flag_bad(DevStatus* st, int field, uint32_t item) {
+  atomicMin(&st->bad_item[field], item);
+}
+
+// order-preserving key of a float / double (total order; -0 == +0)
+__device__ __forceinline__ uint32_t order_key(float d) {
+  if (d == 0.0f) d = 0.0f;
+  uint32_t b = __float_as_uint(d);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ unsigned long long order_key(double d) {
+  if (d == 0.0) d = 0.0;
+  unsigned long long b = (unsigned long long)__double_as_longlong(d);
+  return (b >> 63) ? ~b : (b | (1ull << 63));
+}
+
+// ---------------------------------------------------------------------------
+// K1: facet -> Gaussian -> EWA projection -> cull -> screen record
+// ---------------------------------------------------------------------------
+
+template <typename S> struct FaceGeo {
+  S e[3][3];      // e1 = b-a, e2 = c-a, e3 = c-b
+  S n[3];         // unit normal (u / |u|, or u when degenerate)
+  S nu;           // |u| (1 when degenerate)
+  S area, kappa;
+  S mean[3];
+  bool degenerate, clamped;
+};
+
+template <typename S>
+__device__ __forceinline__ void load_face(const S* __restrict__ pos, const int32_t* __restrict__ faces,
+                                          int64_t f, int rescale, FaceGeo<S>& g, int32_t idx[3]) {
+  idx[0] = faces[3 * f + 0];
+  idx[1] = faces[3 * f + 1];
+  idx[2] = faces[3 * f + 2];
+  S v[3][3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) v[c][k] = pos[3 * (int64_t)idx[c] + k];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    g.e[0][k] = v[1][k] - v[0][k];
+    g.e[1][k] = v[2][k] - v[0][k];
+    g.e[2][k] = v[2][k] - v[1][k];
+    g.mean[k] = (v[0][k] + v[1][k] + v[2][k]) / S(3);
+  }
+  S u0 = g.e[0][1] * g.e[1][2] - g.e[0][2] * g.e[1][1];
+  S u1 = g.e[0][2] * g.e[1][0] - g.e[0][0] * g.e[1][2];
+  S u2 = g.e[0][0] * g.e[1][1] - g.e[0][1] * g.e[1][0];
+  S nu = sqrt_s(u0 * u0 + u1 * u1 + u2 * u2);
+  g.area = S(0.5) * nu;
+  g.degenerate = g.area < S(kDegenerateArea);
+  g.nu = g.degenerate ? S(1) : nu;
+  g.n[0] = u0 / g.nu;
+  g.n[1] = u1 / g.nu;
+  g.n[2] = u2 / g.nu;
+  S det2d = g.area * g.area / S(108);
+  g.clamped = det2d < S(kDetEps);
+  if (rescale) {
+    // unclamped: area / (pi sqrt(area^2/108)) == sqrt(108)/pi exactly
+    g.kappa = g.clamped ? g.area / (S(kPi) * S(1e-7)) : S(3.3080430866842937);
+  } else {
+    g.kappa = S(1);
+  }
+}
+
+// world cov3d (upper triangle xx,xy,xz,yy,yz,zz) of the embed route
+template <typename S>
+__device__ __forceinline__ void face_cov3d(const FaceGeo<S>& g, S c[6]) {
+  if (g.degenerate) {
+    c[0] = c[3] = c[5] = S(kSz2);
+    c[1] = c[2] = c[4] = S(0);
+    return;
+  }
+  const int ii[6] = {0, 0, 0, 1, 1, 2}, jj[6] = {0, 1, 2, 1, 2, 2};
+#pragma unroll
+  for (int q = 0; q < 6; ++q) {
+    const int i = ii[q], j = jj[q];
+    S c3 = (g.e[0][i] * g.e[0][j] + g.e[1][i] * g.e[1][j] + g.e[2][i] * g.e[2][j]) / S(36);
+    c[q] = g.kappa * c3 + S(kSz2) * g.n[i] * g.n[j];
+  }
+}
+
+template <typename S>
+__device__ __forceinline__ void cam_point(const Cam<S>& cam, const S p[3], S t[3]) {
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+    t[r] = cam.R[3 * r + 0] * p[0] + cam.R[3 * r + 1] * p[1] + cam.R[3 * r + 2] * p[2] + cam.t[r];
+}
+
+// M2 = J R (render.py:91-100,115)
+template <typename S>
+__device__ __forceinline__ void cam_m2(const Cam<S>& cam, const S t[3], S m2[2][3]) {
+  const S iz = S(1) / t[2];
+  const S j00 = cam.fx * iz, j02 = -cam.fx * t[0] * iz * iz;
+  const S j11 = cam.fy * iz, j12 = -cam.fy * t[1] * iz * iz;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    m2[0][k] = j00 * cam.R[k] + j02 * cam.R[6 + k];
+    m2[1][k] = j11 * cam.R[3 + k] + j12 * cam.R[6 + k];
+  }
+}
+
+template <typename S> struct MeshFwdArgs {
+  const S* pos;
+  const S* col;
+  const int32_t* faces;
+  int64_t F;
+  int view0, nviews;
+  int W, H, tiles_x, tiles_y;
+  int rescale;
+  Splat<S>* splat;
+  V4<S>* col4;
+  uint2* rect;
+  uint32_t* count;
+  typename KeyOf<S>::type* dkey;
+  uint32_t* ditem;
+  S* aux;   // optional [items][2] = (radius, depth)
+  DevStatus* st;
+};
+
+template <typename S>
+__global__ void __launch_bounds__(256) mesh_to_splats(MeshFwdArgs<S> p, const __grid_constant__ CamBatch<S> cams) {
+  const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = f < p.F;
+  uint32_t kept = 0;
+  if (live) {
+    FaceGeo<S> g;
+    int32_t idx[3];
+    load_face(p.pos, p.faces, f, p.rescale, g, idx);
+    if (p.view0 == 0) {
+      V4<S> c;
+      c.x = (p.col[3 * (int64_t)idx[0] + 0] + p.col[3 * (int64_t)idx[1] + 0] + p.col[3 * (int64_t)idx[2] + 0]) / S(3);
+      c.y = (p.col[3 * (int64_t)idx[0] + 1] + p.col[3 * (int64_t)idx[1] + 1] + p.col[3 * (int64_t)idx[2] + 1]) / S(3);
+      c.z = (p.col[3 * (int64_t)idx[0] + 2] + p.col[3 * (int64_t)idx[1] + 2] + p.col[3 * (int64_t)idx[2] + 2]) / S(3);
+      c.w = S(1);  // opacity (convert.py:326)
+      p.col4[f] = c;
+    }
+    // projected-edge form of M2 (kappa c3 + s_z^2 n n^T) M2^T
+    for (int vv = 0; vv < p.nviews; ++vv) {
+      const Cam<S>& cam = cams.cam[vv];
+      const int64_t item = (int64_t)(p.view0 + vv) * p.F + f;
+      S t[3];
+      cam_point(cam, g.mean, t);
+      Splat<S> rec;
+      uint32_t cnt = 0;
+      uint2 rc = make_uint2(0, 0);
+      typename KeyOf<S>::type key = ~(typename KeyOf<S>::type)0;
+      if (t[2] > cam.near_plane && t[2] < cam.far_plane) {
+        S m2[2][3];
+        cam_m2(cam, t, m2);
+        S a, b, c;
+        if (g.degenerate) {
+          a = S(kSz2) * (m2[0][0] * m2[0][0] + m2[0][1] * m2[0][1] + m2[0][2] * m2[0][2]);
+          b = S(kSz2) * (m2[0][0] * m2[1][0] + m2[0][1] * m2[1][1] + m2[0][2] * m2[1][2]);
+          c = S(kSz2) * (m2[1][0] * m2[1][0] + m2[1][1] * m2[1][1] + m2[1][2] * m2[1][2]);
+        } else {
+          S pa = 0, pb = 0, pc = 0;
+#pragma unroll
+          for (int i = 0; i < 3; ++i) {
+            S x = m2[0][0] * g.e[i][0] + m2[0][1] * g.e[i][1] + m2[0][2] * g.e[i][2];
+            S y = m2[1][0] * g.e[i][0] + m2[1][1] * g.e[i][1] + m2[1][2] * g.e[i][2];
+            pa += x * x;
+            pb += x * y;
+            pc += y * y;
+          }
+          S nx = m2[0][0] * g.n[0] + m2[0][1] * g.n[1] + m2[0][2] * g.n[2];
+          S ny = m2[1][0] * g.n[0] + m2[1][1] * g.n[1] + m2[1][2] * g.n[2];
+          const S k36 = g.kappa / S(36);
+          a = k36 * pa + S(kSz2) * nx * nx;
+          b = k36 * pb + S(kSz2) * nx * ny;
+          c = k36 * pc + S(kSz2) * ny * ny;
+        }
+        a = add_rn(a, Const<S>::dilation());
+        c = add_rn(c, Const<S>::dilation());
+        const S mx = add_rn(div_rn(mul_rn(cam.fx, t[0]), t[2]), cam.cx);
+        const S my = add_rn(div_rn(mul_rn(cam.fy, t[1]), t[2]), cam.cy);
+        S ca, cb, cc, r, ex, ey;
+        screen_shape(a, b, c, S(1), ca, cb, cc, r, ex, ey);
+        const bool on = add_rn(mx, r) >= S(-0.5) && sub_rn(mx, r) <= S(p.W) - S(0.5) &&
+                        add_rn(my, r) >= S(-0.5) && sub_rn(my, r) <= S(p.H) - S(0.5);
+        rec.a.x = mx; rec.a.y = my; rec.a.z = ca; rec.a.w = cb;
+        rec.b.x = cc; rec.b.y = ex; rec.b.z = ey; rec.b.w = r;
+        if (p.aux) {
+          p.aux[2 * item] = r;
+          p.aux[2 * item + 1] = t[2];
+        }
+        if (on) {
+          int tx0, ty0, tx1, ty1;
+          tile_rect(mx, my, r, p.tiles_x, p.tiles_y, tx0, ty0, tx1, ty1);
+          cnt = (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
+          rc = make_uint2((uint32_t)tx0 | ((uint32_t)ty0 << 16), (uint32_t)tx1 | ((uint32_t)ty1 << 16));
+          key = order_key(t[2]);
+          ++kept;
+          // render.py:191-197 on kept splats
+          if (!(finite_s(mx) && finite_s(my))) flag_bad(p.st, 0, (uint32_t)item);
+          if (!(finite_s(a) && finite_s(b) && finite_s(c))) flag_bad(p.st, 1, (uint32_t)item);
+          if (!(finite_s(ca) && finite_s(cb) && finite_s(cc))) flag_bad(p.st, 2, (uint32_t)item);
+          if (!finite_s(t[2])) flag_bad(p.st, 3, (uint32_t)item);
+        }
+      } else {
+        rec.a.x = rec.a.y = rec.a.z = rec.a.w = S(0);
+        rec.b.x = S(0); rec.b.y = rec.b.z = S(-1); rec.b.w = S(0);
+        if (p.aux) {
+          p.aux[2 * item] = S(NAN);
+          p.aux[2 * item + 1] = t[2];
+        }
+      }
+      p.splat[item] = rec;
+      p.rect[item] = rc;
+      p.count[item] = cnt;
+      p.dkey[item] = key;
+      p.ditem[item] = (uint32_t)item;
+    }
+  }
+  // warp-aggregated kept count
+  uint32_t tot = kept;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+  if ((threadIdx.x & 31) == 0 && tot) atomicAdd(&p.st->kept, (unsigned long long)tot);
+}
+
+// K1' — splat path: records from given (mean2d, cov2d, depth, color, opacity)
+template <typename S> struct PackArgs {
+  const S* mean2d;
+  const S* cov2d;
+  const S* depth;
+  const S* color;
+  const S* opacity;
+  int64_t K;
+  int tiles_x, tiles_y;
+  Splat<S>* splat;
+  V4<S>* col4;
+  uint2* rect;
+  uint32_t* count;
+  typename KeyOf<S>::type* dkey;
+  uint32_t* ditem;
+  DevStatus* st;
+};
+
+template <typename S>
+__global__ void __launch_bounds__(256) pack_splats(PackArgs<S> p) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= p.K) return;
+  const S mx = p.mean2d[2 * i], my = p.mean2d[2 * i + 1];
+  const S a = p.cov2d[4 * i], b = p.cov2d[4 * i + 1], c = p.cov2d[4 * i + 3];
+  const S o = p.opacity[i], d = p.depth[i];
+  V4<S> col;
+  col.x = p.color[3 * i]; col.y = p.color[3 * i + 1]; col.z = p.color[3 * i + 2]; col.w = o;
+  S ca, cb, cc, r, ex, ey;
+  screen_shape(a, b, c, o, ca, cb, cc, r, ex, ey);
+  Splat<S> rec;
+  rec.a.x = mx; rec.a.y = my; rec.a.z = ca; rec.a.w = cb;
+  rec.b.x = cc; rec.b.y = ex; rec.b.z = ey; rec.b.w = r;
+  const uint32_t item = (uint32_t)i;
+  if (!(finite_s(mx) && finite_s(my))) flag_bad(p.st, 0, item);
+  if (!(finite_s(a) && finite_s(b) && finite_s(c) && finite_s(p.cov2d[4 * i + 2]))) flag_bad(p.st, 1, item);
+  if (!(finite_s(ca) && finite_s(cb) && finite_s(cc))) flag_bad(p.st, 2, item);
+  if (!finite_s(d)) flag_bad(p.st, 3, item);
+  if (!(finite_s(col.x) && finite_s(col.y) && finite_s(col.z))) flag_bad(p.st, 4, item);
+  if (!finite_s(o)) flag_bad(p.st, 5, item);
+  int tx0 = 0, ty0 = 0, tx1 = -1, ty1 = -1;
+  if (finite_s(mx) && finite_s(my) && finite_s(r))
+    tile_rect(mx, my, r, p.tiles_x, p.tiles_y, tx0, ty0, tx1, ty1);
+  const uint32_t cnt = (tx1 >= tx0 && ty1 >= ty0) ? (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1)) : 0u;
+  p.splat[i] = rec;
+  p.col4[i] = col;
+  p.rect[i] = make_uint2((uint32_t)tx0 | ((uint32_t)ty0 << 16), (uint32_t)max(tx1, 0) | ((uint32_t)max(ty1, 0) << 16));
+  p.count[i] = cnt;
+  p.dkey[i] = order_key(d);
+  p.ditem[i] = item;
+  if (cnt) atomicAdd(&p.st->kept, 1ull);
+}
+
+// ---------------------------------------------------------------------------
+// K2: counts in depth order -> offsets -> entries -> (view, tile) sort -> ranges
+// ---------------------------------------------------------------------------
+
+constexpr int kScanTile = 4096;
+
+__global__ void __launch_bounds__(256) scan_reduce(const uint32_t* __restrict__ order,
+                                                  const uint32_t* __restrict__ count, uint32_t n,
+                                                  uint32_t* __restrict__ bsum) {
+  __shared__ uint32_t sw[8];
+  const uint32_t base = blockIdx.x * (uint32_t)kScanTile;
+  uint32_t s = 0;
+  for (uint32_t i = base + threadIdx.x; i < min(n, base + kScanTile); i += 256) s += count[order[i]];
+  uint32_t tot;
+  block_exclusive_scan_256(s, sw, &tot);
+  if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(256) scan_top(uint32_t* __restrict__ bsum, int nb, DevStatus* st,
+                                               unsigned long long capacity, uint32_t* n_entries) {
+  __shared__ uint32_t sw[8];
+  unsigned long long carry = 0;
+  for (int base = 0; base < nb; base += 256) {
+    int i = base + threadIdx.x;
+    uint32_t v = i < nb ? bsum[i] : 0;
+    uint32_t tot;
+    uint32_t ex = block_exclusive_scan_256(v, sw, &tot);
+    if (i < nb) bsum[i] = (uint32_t)(carry + ex);
+    carry += tot;
+  }
+  if (threadIdx.x == 0) {
+    st->entries = carry;
+    const bool over = carry > capacity || carry > 0xffffffffull;
+    st->overflow = over ? 1u : 0u;
+    *n_entries = over ? 0u : (uint32_t)carry;
+  }
+}
+
+__global__ void __launch_bounds__(256) scan_apply(const uint32_t* __restrict__ order,
+                                                 const uint32_t* __restrict__ count, uint32_t n,
+                                                 const uint32_t* __restrict__ bsum,
+                                                 uint32_t* __restrict__ offs_sorted,
+                                                 uint32_t* __restrict__ entry_off) {
+  __shared__ uint32_t sw[8];
+  const uint32_t base = blockIdx.x * (uint32_t)kScanTile;
+  uint32_t carry = bsum[blockIdx.x];
+  for (uint32_t b0 = base; b0 < min(n, base + kScanTile); b0 += 256 * 4) {
+    uint32_t it[4], c[4], s = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      uint32_t i = b0 + threadIdx.x * 4 + k;
+      bool ok = i < n && i < base + kScanTile;
+      it[k] = ok ? order[i] : 0u;
+      c[k] = ok ? count[it[k]] : 0u;
+      s += c[k];
+    }
+    uint32_t tot;
+    uint32_t run = carry + block_exclusive_scan_256(s, sw, &tot);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      uint32_t i = b0 + threadIdx.x * 4 + k;
+      if (i < n && i < base + kScanTile) {
+        offs_sorted[i] = run;
+        entry_off[it[k]] = run;
+      }
+      run += c[k];
+    }
+    carry += tot;
+  }
+}
+
+// one thread per depth-sorted splat: write its tile entries row-major over
+// its rectangle (render.py:218-226); key = view * T + tile, value = item
+__global__ void __launch_bounds__(256) emit_entries(const uint32_t* __restrict__ order,
+                                                   const uint32_t* __restrict__ count,
+                                                   const uint32_t* __restrict__ offs_sorted,
+                                                   const uint2* __restrict__ rect, uint32_t n,
+                                                   uint32_t items_per_view, int tiles_x,
+                                                   uint32_t tiles_per_view,
+                                                   const uint32_t* __restrict__ n_entries,
+                                                   uint32_t* __restrict__ key,
+                                                   uint32_t* __restrict__ val) {
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n || *n_entries == 0) return;
+  const uint32_t item = order[r];
+  const uint32_t cnt = count[item];
+  if (!cnt) return;
+  const uint32_t off = offs_sorted[r];
+  const uint2 rc = rect[item];
+  const int tx0 = rc.x & 0xffff, ty0 = rc.x >> 16, tx1 = rc.y & 0xffff;
+  const int nx = tx1 - tx0 + 1;
+  const uint32_t vbase = (item / items_per_view) * tiles_per_view;
+  for (uint32_t k = 0; k < cnt; ++k) {
+    const int ty = ty0 + (int)k / nx, tx = tx0 + (int)k % nx;
+    key[off + k] = vbase + (uint32_t)(ty * tiles_x + tx);
+    val[off + k] = item;
+  }
+}
+
+// bounds[g] = first entry with key >= g (searchsorted left, render.py:229)
+__global__ void __launch_bounds__(256) tile_ranges(const uint32_t* __restrict__ key,
+                                                  const uint32_t* n_dev, uint32_t n_host,
+                                                  uint32_t num_bins, uint32_t* __restrict__ bounds) {
+  const uint32_t n = n_dev ? *n_dev : n_host;
+  const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s > n) return;
+  const long long prev = s > 0 ? (long long)key[s - 1] : -1ll;
+  const long long cur = s < n ? (long long)key[s] : (long long)num_bins;
+  for (long long g = prev + 1; g <= cur && g <= (long long)num_bins; ++g) bounds[g] = s;
+}
+
+// ---------------------------------------------------------------------------
+// K3 / K4: per-tile blending
+// ---------------------------------------------------------------------------
+
+template <typename S> struct BlendArgs {
+  const uint32_t* bounds;
+  const uint32_t* entry_item;
+  const Splat<S>* splat;
+  const V4<S>* col4;
+  const uint2* rect;
+  const uint32_t* entry_off;
+  uint32_t items_per_view;   // F (mesh) or K (splats)
+  int tiles_x;
+  uint32_t tiles_per_view;
+  int W, H;
+  S bg0, bg1, bg2;
+  // forward outputs / backward inputs
+  S* rgb;
+  S* alpha;
+  S* t_final;
+  // backward
+  const S* g_rgb;
+  const S* g_alpha;
+  S* partial;        // [E][8] at pre-sort slots
+  S* partial_op;     // [E] (splat path only) or null
+};
+
+template <typename S> struct BlendSmem {
+  V4<S> geo[kBlendThreads];   // mx, my, ca, cb
+  V4<S> geo2[kBlendThreads];  // cc, opacity, -, -
+  V4<S> col[kBlendThreads];   // r, g, b, -
+  uint16_t list[8][kBlendThreads];
+  uint8_t mask[kBlendThreads];
+};
+
+// Load one batch of entries into shared memory; per entry, the 8-bit mask
+// of warp sub-rectangles (8x4 px) its alpha >= 1/255 box touches.
+template <typename S>
+__device__ __forceinline__ void blend_load(const BlendArgs<S>& p, BlendSmem<S>& sm, uint32_t base,
+                                           int n, uint32_t vbase_item, int tile_x0, int tile_y0,
+                                           uint32_t& my_item) {
+  const int i = threadIdx.x;
+  if (i < n) {
+    const uint32_t item = p.entry_item[base + i];
+    my_item = item;
+    const Splat<S> s = p.splat[item];
+    const V4<S> c = p.col4[item - vbase_item];
+    V4<S> g2;
+    g2.x = s.b.x; g2.y = c.w; g2.z = S(0); g2.w = S(0);
+    sm.geo[i] = s.a;
+    sm.geo2[i] = g2;
+    sm.col[i] = c;
+    uint32_t m = 0;
+    const S ex = s.b.y, ey = s.b.z;
+    if (ex >= S(0)) {
+      const S x0 = s.a.x - ex, x1 = s.a.x + ex, y0 = s.a.y - ey, y1 = s.a.y + ey;
+      uint32_t cols = 0, rows = 0;
+#pragma unroll
+      for (int cx = 0; cx < 2; ++cx) {
+        const S wx0 = S(tile_x0 + cx * 8), wx1 = wx0 + S(7);
+        if (x1 >= wx0 && x0 <= wx1) cols |= 1u << cx;
+      }
+#pragma unroll
+      for (int ry = 0; ry < 4; ++ry) {
+        const S wy0 = S(tile_y0 + ry * 4), wy1 = wy0 + S(3);
+        if (y1 >= wy0 && y0 <= wy1) rows |= 1u << ry;
+      }
+#pragma unroll
+      for (int w = 0; w < 8; ++w)
+        if (((cols >> (w & 1)) & 1u) && ((rows >> (w >> 1)) & 1u)) m |= 1u << w;
+    }
+    sm.mask[i] = (uint8_t)m;
+  }
+}
+
+// compact the batch entries whose mask has this warp's bit, in order
+template <typename S>
+__device__ __forceinline__ int blend_warp_list(BlendSmem<S>& sm, int n, int warp, int lane) {
+  int cnt = 0;
+#pragma unroll
+  for (int c = 0; c < kBlendThreads / 32; ++c) {
+    const int j = c * 32 + lane;
+    const bool hit = j < n && ((sm.mask[j] >> warp) & 1u);
+    const unsigned b = __ballot_sync(0xffffffffu, hit);
+    if (hit) sm.list[warp][cnt + __popc(b & lanemask_lt())] = (uint16_t)j;
+    cnt += __popc(b);
+  }
+  __syncwarp();
+  return cnt;
+}
+
+template <typename S>
+__global__ void __launch_bounds__(kBlendThreads) blend_forward(BlendArgs<S> p) {
+  __shared__ BlendSmem<S> sm;
+  const uint32_t g = blockIdx.x;
+  const uint32_t view = g / p.tiles_per_view, t = g % p.tiles_per_view;
+  const int tx = (int)(t % (uint32_t)p.tiles_x), ty = (int)(t / (uint32_t)p.tiles_x);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int px = tx * kTile + (warp & 1) * 8 + (lane & 7);
+  const int py = ty * kTile + (warp >> 1) * 4 + (lane >> 3);
+  const bool inside = px < p.W && py < p.H;
+  const S fpx = S(px), fpy = S(py);
+  const S one = S(1);
+  S T = one, ar = 0, ag = 0, ab = 0;
+  bool done = !inside;
+  const uint32_t start = p.bounds[g], end = p.bounds[g + 1];
+  const uint32_t vbase_item = view * p.items_per_view;
+  for (uint32_t base = start; base < end; base += kBlendThreads) {
+    if (__syncthreads_count(done) == kBlendThreads) break;
+    const int n = (int)min((uint32_t)kBlendThreads, end - base);
+    uint32_t my_item;
+    blend_load(p, sm, base, n, vbase_item, tx * kTile, ty * kTile, my_item);
+    __syncthreads();
+    const int cnt = blend_warp_list(sm, n, warp, lane);
+    for (int k = 0; k < cnt; ++k) {
+      if (__all_sync(0xffffffffu, done)) break;
+      const int j = sm.list[warp][k];
+      if (!done) {
+        const V4<S> ge = sm.geo[j];
+        const V4<S> g2 = sm.geo2[j];
+        const S dx = sub_rn(fpx, ge.x), dy = sub_rn(fpy, ge.y);
+        const S q = add_rn(mul_rn(mul_rn(ge.z, dx), dx), mul_rn(mul_rn(g2.x, dy), dy));
+        const S power = sub_rn(mul_rn(S(-0.5), q), mul_rn(mul_rn(ge.w, dx), dy));
+        const S raw = mul_rn(g2.y, exp_s(power));
+        const S a = raw < Const<S>::alpha_clamp() ? raw : Const<S>::alpha_clamp();
+        if (a >= Const<S>::contrib_floor()) {
+          const S test = mul_rn(T, sub_rn(one, a));
+          if (test < Const<S>::t_stop()) {
+            done = true;
+          } else {
+            const V4<S> c = sm.col[j];
+            const S w = mul_rn(a, T);
+            ar += w * c.x;
+            ag += w * c.y;
+            ab += w * c.z;
+            T = test;
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (inside) {
+    const size_t pix = ((size_t)view * p.H + py) * p.W + px;
+    p.rgb[3 * pix + 0] = ar + T * p.bg0;
+    p.rgb[3 * pix + 1] = ag + T * p.bg1;
+    p.rgb[3 * pix + 2] = ab + T * p.bg2;
+    p.alpha[pix] = one - T;
+    p.t_final[pix] = T;
+  }
+}
+
+// Butterfly-transpose reduction of 8 per-lane values over the warp:
+// 9 shuffles.  Returns, in every lane, the total of value index
+// ((lane>>4)&1)*4 + ((lane>>3)&1)*2 + ((lane>>2)&1).
+template <typename S>
+__device__ __forceinline__ S warp_reduce8(const S v[8], int lane) {
+  S a[4], c[2];
+  const bool h4 = lane & 16, h3 = lane & 8, h2 = lane & 4;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const S send = h4 ? v[i] : v[i + 4];
+    const S keep = h4 ? v[i + 4] : v[i];
+    a[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const S send = h3 ? a[i] : a[i + 2];
+    const S keep = h3 ? a[i + 2] : a[i];
+    c[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  const S send = h2 ? c[0] : c[1];
+  const S keep = h2 ? c[1] : c[0];
+  S d = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  d += __shfl_xor_sync(0xffffffffu, d, 2);
+  d += __shfl_xor_sync(0xffffffffu, d, 1);
+  return d;
+}
+
+template <typename S>
+__device__ __forceinline__ S warp_sum(S v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Front-to-back re-scan (same decisions as K3).  With C = g.(rgb - T_f bg)
+// = sum_j (g.c_j) w_j, the suffix S_k = C - sum_{j<=k} (g.c_j) w_j, so
+//   dL/dalpha_k = (g.c_k) T_k - (S_k + (g.bg - g_a) T_f) / (1 - alpha_k)
+// (render.py:327-334).  Per (warp, entry) the 8 sums
+//   [sum dp dx, dp dy, dp dx^2, dp dx dy, dp dy^2, w g_r, w g_g, w g_b]
+// are reduced in fixed order; warps are summed in warp order; each entry's
+// sums land in its pre-sort slot, so accumulation is deterministic.
+template <typename S, bool kOpacity>
+__global__ void __launch_bounds__(kBlendThreads) blend_backward(BlendArgs<S> p) {
+  __shared__ BlendSmem<S> sm;
+  extern __shared__ __align__(16) unsigned char dyn[];
+  S* part = reinterpret_cast<S*>(dyn);                       // [8 warps][256][8]
+  S* part_op = part + 8 * kBlendThreads * 8;                  // [8][256] (kOpacity)
+  const uint32_t g = blockIdx.x;
+  const uint32_t view = g / p.tiles_per_view, t = g % p.tiles_per_view;
+  const int tx = (int)(t % (uint32_t)p.tiles_x), ty = (int)(t / (uint32_t)p.tiles_x);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int px = tx * kTile + (warp & 1) * 8 + (lane & 7);
+  const int py = ty * kTile + (warp >> 1) * 4 + (lane >> 3);
+  const bool inside = px < p.W && py < p.H;
+  const S fpx = S(px), fpy = S(py);
+  const S one = S(1);
+  S gr = 0, gg = 0, gb = 0, Ctot = 0, bterm = 0;
+  if (inside) {
+    const size_t pix = ((size_t)view * p.H + py) * p.W + px;
+    gr = p.g_rgb[3 * pix]; gg = p.g_rgb[3 * pix + 1]; gb = p.g_rgb[3 * pix + 2];
+    const S ga = p.g_alpha[pix];
+    const S tf = p.t_final[pix];
+    const S gbg = gr * p.bg0 + gg * p.bg1 + gb * p.bg2;
+    Ctot = gr * p.rgb[3 * pix] + gg * p.rgb[3 * pix + 1] + gb * p.rgb[3 * pix + 2] - gbg * tf;
+    bterm = (gbg - ga) * tf;
+  }
+  S T = one, P = 0;
+  bool done = !inside;
+  const uint32_t start = p.bounds[g], end = p.bounds[g + 1];
+  const uint32_t vbase_item = view * p.items_per_view;
+  const int holder = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+  uint32_t base = start;
+  for (; base < end; base += kBlendThreads) {
+    const bool all_done = __syncthreads_count(done) == kBlendThreads;
+    const int n = (int)min((uint32_t)kBlendThreads, end - base);
+    uint32_t my_item = 0;
+    if (all_done) break;
+    blend_load(p, sm, base, n, vbase_item, tx * kTile, ty * kTile, my_item);
+    __syncthreads();
+    const int cnt = blend_warp_list(sm, n, warp, lane);
+    int k = 0;
+    for (; k < cnt; ++k) {
+      if (__all_sync(0xffffffffu, done)) break;
+      const int j = sm.list[warp][k];
+      S v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = S(0);
+      S vop = S(0);
+      if (!done) {
+        const V4<S> ge = sm.geo[j];
+        const V4<S> g2 = sm.geo2[j];
+        const S dx = sub_rn(fpx, ge.x), dy = sub_rn(fpy, ge.y);
+        const S q = add_rn(mul_rn(mul_rn(ge.z, dx), dx), mul_rn(mul_rn(g2.x, dy), dy));
+        const S power = sub_rn(mul_rn(S(-0.5), q), mul_rn(mul_rn(ge.w, dx), dy));
+        const S ep = exp_s(power);
+        const S raw = mul_rn(g2.y, ep);
+        const S a = raw < Const<S>::alpha_clamp() ? raw : Const<S>::alpha_clamp();
+        if (a >= Const<S>::contrib_floor()) {
+          const S om = sub_rn(one, a);
+          const S test = mul_rn(T, om);
+          if (test < Const<S>::t_stop()) {
+            done = true;
+          } else {
+            const V4<S> c = sm.col[j];
+            const S w = mul_rn(a, T);
+            const S gdc = gr * c.x + gg * c.y + gb * c.z;
+            P += gdc * w;
+            const S suffix = Ctot - P;
+            const S d_alpha = gdc * T - (suffix + bterm) / om;
+            if (raw < Const<S>::alpha_clamp()) {
+              const S dp = d_alpha * a;
+              v[0] = dp * dx;
+              v[1] = dp * dy;
+              v[2] = v[0] * dx;
+              v[3] = v[0] * dy;
+              v[4] = v[1] * dy;
+              vop = d_alpha * ep;
+            }
+            v[5] = w * gr;
+            v[6] = w * gg;
+            v[7] = w * gb;
+            T = test;
+          }
+        }
+      }
+      const S r = warp_reduce8(v, lane);
+      if ((lane & 3) == 0) part[((size_t)warp * kBlendThreads + j) * 8 + holder] = r;
+      if (kOpacity) {
+        const S ro = warp_sum(vop);
+        if (lane == 0) part_op[warp * kBlendThreads + j] = ro;
+      }
+    }
+    // entries this warp skipped after finishing contribute zero
+    for (int kk = k + lane; kk < cnt; kk += 32) {
+      const int j = sm.list[warp][kk];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) part[((size_t)warp * kBlendThreads + j) * 8 + q] = S(0);
+      if (kOpacity) part_op[warp * kBlendThreads + j] = S(0);
+    }
+    __syncthreads();
+    // per entry: sum over the warps in its mask, in warp order
+    if ((int)threadIdx.x < n) {
+      const int j = threadIdx.x;
+      const uint32_t m = sm.mask[j];
+      S acc[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q] = S(0);
+      S aop = S(0);
+      for (int w = 0; w < 8; ++w) {
+        if (!((m >> w) & 1u)) continue;
+        const S* src = part + ((size_t)w * kBlendThreads + j) * 8;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] += src[q];
+        if (kOpacity) aop += part_op[w * kBlendThreads + j];
+      }
+      const uint2 rc = p.rect[my_item];
+      const int tx0 = rc.x & 0xffff, ty0 = rc.x >> 16, tx1 = rc.y & 0xffff;
+      const uint32_t slot = p.entry_off[my_item] + (uint32_t)((ty - ty0) * (tx1 - tx0 + 1) + (tx - tx0));
+      V4<S>* dst = reinterpret_cast<V4<S>*>(p.partial + (size_t)slot * 8);
+      V4<S> lo, hi;
+      lo.x = acc[0]; lo.y = acc[1]; lo.z = acc[2]; lo.w = acc[3];
+      hi.x = acc[4]; hi.y = acc[5]; hi.z = acc[6]; hi.w = acc[7];
+      dst[0] = lo;
+      dst[1] = hi;
+      if (kOpacity) p.partial_op[slot] = aop;
+    }
+    __syncthreads();
+  }
+  // the tile finished early: entries never loaded still own a partial slot,
+  // which must hold zeros (every slot is written exactly once)
+  for (uint32_t e = base + threadIdx.x; e < end; e += kBlendThreads) {
+    const uint32_t item = p.entry_item[e];
+    const uint2 rc = p.rect[item];
+    const int tx0 = rc.x & 0xffff, ty0 = rc.x >> 16, tx1 = rc.y & 0xffff;
+    const uint32_t slot = p.entry_off[item] + (uint32_t)((ty - ty0) * (tx1 - tx0 + 1) + (tx - tx0));
+    V4<S>* dst = reinterpret_cast<V4<S>*>(p.partial + (size_t)slot * 8);
+    V4<S> z;
+    z.x = z.y = z.z = z.w = S(0);
+    dst[0] = z;
+    dst[1] = z;
+    if (kOpacity) p.partial_op[slot] = S(0);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K5: per face — screen grads (summed over its entries, tile order) ->
+// projection backward per view -> accumulate over views -> conversion backward
+// ---------------------------------------------------------------------------
+
+template <typename S>
+__device__ __forceinline__ void sum_entries(const S* __restrict__ partial, uint32_t off, uint32_t cnt,
+                                            S acc[8]) {
+#pragma unroll
+  for (int q = 0; q < 8; ++q) acc[q] = S(0);
+  const V4<S>* src = reinterpret_cast<const V4<S>*>(partial + (size_t)off * 8);
+  for (uint32_t e = 0; e < cnt; ++e) {
+    const V4<S> lo = src[2 * e], hi = src[2 * e + 1];
+    acc[0] += lo.x; acc[1] += lo.y; acc[2] += lo.z; acc[3] += lo.w;
+    acc[4] += hi.x; acc[5] += hi.y; acc[6] += hi.z; acc[7] += hi.w;
+  }
+}
+
+// conic sums -> (g_mean2d, g_cov2d) (render.py:344-360)
+template <typename S>
+__device__ __forceinline__ void conic_to_cov_grad(const S acc[8], S ca, S cb, S cc, S gm[2], S gcov[3]) {
+  gm[0] = ca * acc[0] + cb * acc[1];
+  gm[1] = cc * acc[1] + cb * acc[0];
+  const S q00 = S(-0.5) * acc[2], q01 = S(-0.5) * acc[3], q11 = S(-0.5) * acc[4];
+  // -M Q M with M = [[ca, cb], [cb, cc]], Q = [[q00, q01], [q01, q11]]
+  const S mq00 = ca * q00 + cb * q01, mq01 = ca * q01 + cb * q11;
+  const S mq10 = cb * q00 + cc * q01, mq11 = cb * q01 + cc * q11;
+  gcov[0] = -(mq00 * ca + mq01 * cb);
+  gcov[1] = -(mq00 * cb + mq01 * cc);
+  gcov[2] = -(mq10 * cb + mq11 * cc);
+}
+
+template <typename S> struct FaceBwdArgs {
+  const S* pos;
+  const int32_t* faces;
+  int64_t F;
+  int view0, nviews;
+  int rescale;
+  const uint32_t* count;
+  const uint32_t* entry_off;
+  const Splat<S>* splat;
+  const S* partial;
+  S* face_acc;   // [F][12]: g_mean3 (3), g_cov3 sym (6), g_col (3)
+};
+
+template <typename S>
+__global__ void __launch_bounds__(128) face_views_backward(FaceBwdArgs<S> p, const __grid_constant__ CamBatch<S> cams) {
+  const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= p.F) return;
+  FaceGeo<S> g;
+  int32_t idx[3];
+  load_face(p.pos, p.faces, f, p.rescale, g, idx);
+  S cov[6];
+  face_cov3d(g, cov);
+  S acc[12];
+  if (p.view0 == 0) {
+#pragma unroll
+    for (int q = 0; q < 12; ++q) acc[q] = S(0);
+  } else {
+#pragma unroll
+    for (int q = 0; q < 12; ++q) acc[q] = p.face_acc[f * 12 + q];
+  }
+  for (int vv = 0; vv < p.nviews; ++vv) {
+    const int64_t item = (int64_t)(p.view0 + vv) * p.F + f;
+    const uint32_t cnt = p.count[item];
+    if (!cnt) continue;
+    S s[8];
+    sum_entries(p.partial, p.entry_off[item], cnt, s);
+    const Splat<S> rec = p.splat[item];
+    S gm[2], g2[3];
+    conic_to_cov_grad(s, rec.a.z, rec.a.w, rec.b.x, gm, g2);
+    const Cam<S>& cam = cams.cam[vv];
+    S t[3], m2[2][3];
+    cam_point(cam, g.mean, t);
+    cam_m2(cam, t, m2);
+    // g_cov3d += M2^T G M2 (render.py:382), G = [[g0, g1], [g1, g2]]
+    const int ii[6] = {0, 0, 0, 1, 1, 2}, jj[6] = {0, 1, 2, 1, 2, 2};
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      const int i = ii[q], j = jj[q];
+      acc[3 + q] += m2[0][i] * (g2[0] * m2[0][j] + g2[1] * m2[1][j]) +
+                    m2[1][i] * (g2[1] * m2[0][j] + g2[2] * m2[1][j]);
+    }
+    // g_M2 = (G + G^T) M2 Sigma (render.py:383-384)
+    S ms[2][3];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      ms[r][0] = m2[r][0] * cov[0] + m2[r][1] * cov[1] + m2[r][2] * cov[2];
+      ms[r][1] = m2[r][0] * cov[1] + m2[r][1] * cov[3] + m2[r][2] * cov[4];
+      ms[r][2] = m2[r][0] * cov[2] + m2[r][1] * cov[4] + m2[r][2] * cov[5];
+    }
+    S gM[2][3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      gM[0][k] = S(2) * (g2[0] * ms[0][k] + g2[1] * ms[1][k]);
+      gM[1][k] = S(2) * (g2[1] * ms[0][k] + g2[2] * ms[1][k]);
+    }
+    // g_J = g_M2 R^T (render.py:385)
+    S gJ[2][3];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+        gJ[r][k] = gM[r][0] * cam.R[3 * k] + gM[r][1] * cam.R[3 * k + 1] + gM[r][2] * cam.R[3 * k + 2];
+    const S iz = S(1) / t[2], iz2 = iz * iz;
+    S gt0 = -cam.fx * iz2 * gJ[0][2] + gm[0] * cam.fx * iz;
+    S gt1 = -cam.fy * iz2 * gJ[1][2] + gm[1] * cam.fy * iz;
+    S gt2 = -cam.fx * iz2 * gJ[0][0] - cam.fy * iz2 * gJ[1][1] +
+            S(2) * cam.fx * t[0] * iz2 * iz * gJ[0][2] + S(2) * cam.fy * t[1] * iz2 * iz * gJ[1][2] -
+            gm[0] * cam.fx * t[0] * iz2 - gm[1] * cam.fy * t[1] * iz2;
+    // g_mean3d = g_t R (render.py:401)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) acc[k] += gt0 * cam.R[k] + gt1 * cam.R[3 + k] + gt2 * cam.R[6 + k];
+    acc[9] += s[5];
+    acc[10] += s[6];
+    acc[11] += s[7];
+  }
+#pragma unroll
+  for (int q = 0; q < 12; ++q) p.face_acc[f * 12 + q] = acc[q];
+}
+
+// conversion backward per face (convert.py:393-425) -> per-corner
+// contributions corner[f][c][6] = (g_pos xyz, g_col rgb)
+template <typename S>
+__global__ void __launch_bounds__(128) face_convert_backward(const S* __restrict__ pos,
+                                                             const int32_t* __restrict__ faces,
+                                                             int64_t F, int rescale,
+                                                             const S* __restrict__ face_acc,
+                                                             S* __restrict__ corner) {
+  const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= F) return;
+  FaceGeo<S> g;
+  int32_t idx[3];
+  load_face(pos, faces, f, rescale, g, idx);
+  S a[12];
+#pragma unroll
+  for (int q = 0; q < 12; ++q) a[q] = face_acc[f * 12 + q];
+  // G symmetric (xx,xy,xz,yy,yz,zz); gsym = 2G
+  const S G[3][3] = {{a[3], a[4], a[5]}, {a[4], a[6], a[7]}, {a[5], a[7], a[8]}};
+  S ge[3][3];   // g_e1, g_e2, g_e3
+  if (!g.degenerate) {
+    const S sk = g.kappa * S(2) / S(36);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        const S* e = g.e[i == 2 ? 2 : i];
+        ge[i][r] = sk * (G[r][0] * e[0] + G[r][1] * e[1] + G[r][2] * e[2]);
+      }
+    }
+    S d_area = S(0);
+    if (rescale && g.clamped) {
+      S dk = 0;
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          dk += G[r][c] * (g.e[0][r] * g.e[0][c] + g.e[1][r] * g.e[1][c] + g.e[2][r] * g.e[2][c]) / S(36);
+      d_area = dk / (S(kPi) * S(1e-7));
+    }
+    S gn[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) gn[r] = S(kSz2) * S(2) * (G[r][0] * g.n[0] + G[r][1] * g.n[1] + G[r][2] * g.n[2]);
+    const S nd = g.n[0] * gn[0] + g.n[1] * gn[1] + g.n[2] * gn[2];
+    S gu[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) gu[r] = (gn[r] - g.n[r] * nd) / g.nu + S(0.5) * d_area * g.n[r];
+    // g_e1 += e2 x g_u ; g_e2 += g_u x e1
+    const S* e1 = g.e[0];
+    const S* e2 = g.e[1];
+    ge[0][0] += e2[1] * gu[2] - e2[2] * gu[1];
+    ge[0][1] += e2[2] * gu[0] - e2[0] * gu[2];
+    ge[0][2] += e2[0] * gu[1] - e2[1] * gu[0];
+    ge[1][0] += gu[1] * e1[2] - gu[2] * e1[1];
+    ge[1][1] += gu[2] * e1[0] - gu[0] * e1[2];
+    ge[1][2] += gu[0] * e1[1] - gu[1] * e1[0];
+  } else {
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int r = 0; r < 3; ++r) ge[i][r] = S(0);
+  }
+  S* out = corner + f * 18;
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    const S third = a[r] / S(3);
+    out[0 + r] = third - ge[0][r] - ge[1][r];
+    out[6 + r] = third + ge[0][r] - ge[2][r];
+    out[12 + r] = third + ge[1][r] + ge[2][r];
+    const S gc = a[9 + r] / S(3);
+    out[3 + r] = gc;
+    out[9 + r] = gc;
+    out[15 + r] = gc;
+  }
+}
+
+// K6: per vertex, sum its (face, corner) contributions in the reference's
+// np.add.at order (all corner-0 faces ascending, then corner 1, then 2)
+template <typename S>
+__global__ void __launch_bounds__(256) vertex_gather(const uint32_t* __restrict__ vstart,
+                                                    const uint32_t* __restrict__ slots, int64_t V,
+                                                    int64_t F, const S* __restrict__ corner,
+                                                    S* __restrict__ g_pos, S* __restrict__ g_col) {
+  const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= V) return;
+  S gp[3] = {0, 0, 0}, gc[3] = {0, 0, 0};
+  const uint32_t b = vstart[v], e = vstart[v + 1];
+  for (uint32_t k = b; k < e; ++k) {
+    const uint32_t s = slots[k];
+    const uint32_t c = (uint32_t)(s / (uint64_t)F);
+    const uint64_t f = s - (uint64_t)c * F;
+    const S* src = corner + f * 18 + c * 6;
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      gp[r] += src[r];
+      gc[r] += src[3 + r];
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    g_pos[3 * v + r] = gp[r];
+    g_col[3 * v + r] = gc[r];
+  }
+}
+
+// splat path: per splat screen grads (render.py:338-360)
+template <typename S>
+__global__ void __launch_bounds__(256) splat_grads(const uint32_t* __restrict__ count,
+                                                  const uint32_t* __restrict__ entry_off,
+                                                  const Splat<S>* __restrict__ splat,
+                                                  const S* __restrict__ partial,
+                                                  const S* __restrict__ partial_op, int64_t K,
+                                                  S* g_mean2d, S* g_cov2d, S* g_color, S* g_opacity) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= K) return;
+  const uint32_t cnt = count[i];
+  S s[8];
+  S op = S(0);
+  if (cnt) {
+    const uint32_t off = entry_off[i];
+    sum_entries(partial, off, cnt, s);
+    for (uint32_t e = 0; e < cnt; ++e) op += partial_op[off + e];
+  } else {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s[q] = S(0);
+  }
+  const Splat<S> rec = splat[i];
+  S gm[2], gc[3];
+  conic_to_cov_grad(s, rec.a.z, rec.a.w, rec.b.x, gm, gc);
+  if (!cnt) { gm[0] = gm[1] = gc[0] = gc[1] = gc[2] = S(0); }
+  g_mean2d[2 * i] = gm[0];
+  g_mean2d[2 * i + 1] = gm[1];
+  g_cov2d[4 * i] = gc[0];
+  g_cov2d[4 * i + 1] = gc[1];
+  g_cov2d[4 * i + 2] = gc[1];
+  g_cov2d[4 * i + 3] = gc[2];
+  g_color[3 * i] = s[5];
+  g_color[3 * i + 1] = s[6];
+  g_color[3 * i + 2] = s[7];
+  g_opacity[i] = op;
+}
+
+// topology: slot s = c * F + f -> key faces[3f + c]
+__global__ void topo_keys(const int32_t* __restrict__ faces, int64_t F, uint32_t* key, uint32_t* val) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= 3 * F) return;
+  const int64_t c = s / F, f = s - c * F;
+  key[s] = (uint32_t)faces[3 * f + c];
+  val[s] = (uint32_t)s;
+}
+
+// ---------------------------------------------------------------------------
+// single-stage helpers (convert_mesh / convert_backward stage functions)
+// ---------------------------------------------------------------------------
+
+template <typename S>
+__global__ void __launch_bounds__(128) convert_forward(const S* __restrict__ pos, const S* __restrict__ col,
+                                                       const int32_t* __restrict__ faces, int64_t F,
+                                                       int rescale, S* means, S* cov3d, S* colors,
+                                                       uint8_t* degenerate) {
+  const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= F) return;
+  FaceGeo<S> g;
+  int32_t idx[3];
+  load_face(pos, faces, f, rescale, g, idx);
+  S c[6];
+  face_cov3d(g, c);
+  const int map[9] = {0, 1, 2, 1, 3, 4, 2, 4, 5};
+#pragma unroll
+  for (int k = 0; k < 9; ++k) cov3d[f * 9 + k] = c[map[k]];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    means[3 * f + k] = g.mean[k];
+    colors[3 * f + k] = (col[3 * (int64_t)idx[0] + k] + col[3 * (int64_t)idx[1] + k] + col[3 * (int64_t)idx[2] + k]) / S(3);
+  }
+  if (degenerate) degenerate[f] = g.degenerate ? 1 : 0;
+}
+
+template <typename S>
+__global__ void __launch_bounds__(256) pack_face_grads(const S* __restrict__ gm, const S* __restrict__ gcov,
+                                                      const S* __restrict__ gcol, int64_t F,
+                                                      S* __restrict__ face_acc) {
+  const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= F) return;
+  const S* G = gcov + f * 9;
+  S* o = face_acc + f * 12;
+  o[0] = gm[3 * f]; o[1] = gm[3 * f + 1]; o[2] = gm[3 * f + 2];
+  // only (G + G^T)/2 matters (gsym and <G, c3> with c3 symmetric)
+  o[3] = G[0];
+  o[4] = S(0.5) * (G[1] + G[3]);
+  o[5] = S(0.5) * (G[2] + G[6]);
+  o[6] = G[4];
+  o[7] = S(0.5) * (G[5] + G[7]);
+  o[8] = G[8];
+  o[9] = gcol[3 * f]; o[10] = gcol[3 * f + 1]; o[11] = gcol[3 * f + 2];
+}
+
+}  // namespace gmr

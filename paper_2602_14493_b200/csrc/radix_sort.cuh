@@ -1,0 +1,208 @@
+// radix_sort.cuh — stable LSD radix sort of (key, u32 value) pairs, 8-bit digits.
+//
+// Used three times on the GMR path: the per-view depth order of splats
+// (u32 float bits / u64 double bits), the (view, tile) bucketing of tile
+// entries (render.py:227 lexsort by (tile, depth, source)),
+// and the face->vertex scatter plan.  The element count may live in device
+// memory (`n_dev`), so the pipeline never waits on the host for E: grids are
+// sized for the capacity and surplus blocks exit.
+//
+// One pass = upsweep (per-block digit histogram) + scan (per digit over
+// blocks) + downsweep (stable in-block rank with warp match_any, scatter).
+// Each block owns 4096 consecutive items; each warp a contiguous 512.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace gmr {
+
+constexpr int kSortThreads = 256;
+constexpr int kSortPerThread = 16;
+constexpr int kSortTile = kSortThreads * kSortPerThread;  // 4096
+constexpr int kSortWarps = kSortThreads / 32;
+
+__device__ __forceinline__ unsigned lanemask_lt_sort() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+__device__ __forceinline__ uint32_t sort_count(const uint32_t* n_dev, uint32_t n_host) {
+  return n_dev ? *n_dev : n_host;
+}
+
+template <typename K>
+__global__ void __launch_bounds__(kSortThreads) radix_upsweep(const K* __restrict__ keys,
+                                                              const uint32_t* n_dev,
+                                                              uint32_t n_host, int shift,
+                                                              uint32_t* __restrict__ hist,
+                                                              int nblocks) {
+  __shared__ uint32_t h[kSortWarps][256];
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < kSortWarps * 256; i += kSortThreads) (&h[0][0])[i] = 0;
+  __syncthreads();
+  const uint32_t n = sort_count(n_dev, n_host);
+  const uint32_t base = blockIdx.x * (uint32_t)kSortTile;
+  if (base < n) {
+    const uint32_t end = min(n, base + (uint32_t)kSortTile);
+    for (uint32_t i = base + tid; i < end; i += kSortThreads) {
+      uint32_t d = (uint32_t)(keys[i] >> shift) & 255u;
+      atomicAdd(&h[warp][d], 1u);
+    }
+  }
+  __syncthreads();
+  uint32_t s = 0;
+#pragma unroll
+  for (int w = 0; w < kSortWarps; ++w) s += h[w][tid];
+  hist[(size_t)tid * nblocks + blockIdx.x] = s;
+}
+
+// block-wide exclusive scan of one value per thread (256 threads)
+__device__ __forceinline__ uint32_t block_exclusive_scan_256(uint32_t v, uint32_t* smem_warp,
+                                                             uint32_t* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) smem_warp[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t w = lane < kSortWarps ? smem_warp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < kSortWarps; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < kSortWarps) smem_warp[lane] = w;  // inclusive per warp
+  }
+  __syncthreads();
+  uint32_t warp_prefix = warp ? smem_warp[warp - 1] : 0;
+  if (total) *total = smem_warp[kSortWarps - 1];
+  uint32_t r = warp_prefix + x - v;
+  __syncthreads();
+  return r;
+}
+
+// One block per digit: exclusive scan of hist[d][0..nblocks) in place,
+// digit total into totals[d].
+__global__ void __launch_bounds__(kSortThreads) radix_scan(uint32_t* __restrict__ hist,
+                                                           uint32_t* __restrict__ totals,
+                                                           int nblocks) {
+  __shared__ uint32_t sw[kSortWarps];
+  uint32_t* row = hist + (size_t)blockIdx.x * nblocks;
+  uint32_t carry = 0;
+  for (int base = 0; base < nblocks; base += kSortThreads * 4) {
+    uint32_t v[4], s = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      int i = base + threadIdx.x * 4 + k;
+      v[k] = i < nblocks ? row[i] : 0;
+      s += v[k];
+    }
+    uint32_t tot;
+    uint32_t ex = block_exclusive_scan_256(s, sw, &tot);
+    uint32_t run = carry + ex;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      int i = base + threadIdx.x * 4 + k;
+      if (i < nblocks) row[i] = run;
+      run += v[k];
+    }
+    carry += tot;
+  }
+  if (threadIdx.x == 0) totals[blockIdx.x] = carry;
+}
+
+template <typename K>
+__global__ void __launch_bounds__(kSortThreads) radix_downsweep(
+    const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __restrict__ kout,
+    uint32_t* __restrict__ vout, const uint32_t* n_dev, uint32_t n_host, int shift,
+    const uint32_t* __restrict__ hist, const uint32_t* __restrict__ totals, int nblocks) {
+  __shared__ uint32_t wc[kSortWarps][256];
+  __shared__ uint32_t dbase[256];
+  __shared__ uint32_t sw[kSortWarps];
+  const uint32_t n = sort_count(n_dev, n_host);
+  const uint32_t base = blockIdx.x * (uint32_t)kSortTile;
+  if (base >= n) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < kSortWarps * 256; i += kSortThreads) (&wc[0][0])[i] = 0;
+  uint32_t ex = block_exclusive_scan_256(totals[tid], sw, nullptr);
+  dbase[tid] = ex + hist[(size_t)tid * nblocks + blockIdx.x];
+  __syncthreads();
+
+  const uint32_t seg = base + (uint32_t)warp * (kSortPerThread * 32);
+  K key[kSortPerThread];
+  uint32_t val[kSortPerThread];
+  uint32_t rank[kSortPerThread];
+  const unsigned lt = lanemask_lt_sort();
+#pragma unroll
+  for (int r = 0; r < kSortPerThread; ++r) {
+    const uint32_t idx = seg + r * 32 + lane;
+    const bool valid = idx < n;
+    key[r] = valid ? kin[idx] : K(0);
+    val[r] = valid ? vin[idx] : 0u;
+    const uint32_t d = valid ? ((uint32_t)(key[r] >> shift) & 255u) : 256u;
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    const uint32_t cnt = valid ? wc[warp][d] : 0u;
+    rank[r] = cnt + __popc(peers & lt);
+    __syncwarp();
+    if (valid && (lt & peers) == 0) wc[warp][d] = cnt + __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  {
+    uint32_t run = 0;
+#pragma unroll
+    for (int w = 0; w < kSortWarps; ++w) {
+      uint32_t c = wc[w][tid];
+      wc[w][tid] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < kSortPerThread; ++r) {
+    const uint32_t idx = seg + r * 32 + lane;
+    if (idx < n) {
+      const uint32_t d = (uint32_t)(key[r] >> shift) & 255u;
+      const uint32_t pos = dbase[d] + wc[warp][d] + rank[r];
+      kout[pos] = key[r];
+      vout[pos] = val[r];
+    }
+  }
+}
+
+// Host-side driver: sorts [0, n) of (keys[0], vals[0]) by bits [0, bits).
+// Ping-pongs between buffer 0 and 1; returns the index (0/1) holding the
+// result.  `capacity` bounds n and sizes the grids; hist needs
+// 256 * blocks(capacity) + 256 words.
+template <typename K>
+inline int radix_sort_pairs(K* keys[2], uint32_t* vals[2], const uint32_t* n_dev,
+                            uint32_t n_host, uint32_t capacity, int bits, uint32_t* hist,
+                            cudaStream_t stream) {
+  const int nblocks = (int)((capacity + kSortTile - 1) / kSortTile);
+  if (nblocks == 0 || bits <= 0) return 0;
+  uint32_t* totals = hist + (size_t)256 * nblocks;
+  int cur = 0;
+  for (int shift = 0; shift < bits; shift += 8) {
+    radix_upsweep<K><<<nblocks, kSortThreads, 0, stream>>>(keys[cur], n_dev, n_host, shift, hist,
+                                                           nblocks);
+    radix_scan<<<256, kSortThreads, 0, stream>>>(hist, totals, nblocks);
+    radix_downsweep<K><<<nblocks, kSortThreads, 0, stream>>>(keys[cur], vals[cur], keys[cur ^ 1],
+                                                             vals[cur ^ 1], n_dev, n_host, shift,
+                                                             hist, totals, nblocks);
+    cur ^= 1;
+  }
+  return cur;
+}
+
+inline size_t radix_hist_words(uint32_t capacity) {
+  const size_t nblocks = (capacity + kSortTile - 1) / kSortTile;
+  return 256 * nblocks + 256;
+}
+
+}  // namespace gmr

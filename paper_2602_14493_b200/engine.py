@@ -1,0 +1,299 @@
+"""Device-side driver of libgmr: workspace planning, capacity management,
+topology caching, and the torch autograd Function over B views.
+
+PyTorch provides device memory and the current stream only; every FLOP of
+the render path runs in libgmr.so (include/gmr.h).  Callers: the numpy
+drop-in shim (`api.py`, mirroring reference render.py / convert.py /
+losses.py) and the batched torch entry `render_views`.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import lib as L
+
+_DT = {torch.float32: L.GMR_F32, torch.float64: L.GMR_F64}
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def raster_struct(width, height, background, dtype, rescale=True, flags=0) -> L.GmrRaster:
+    r = L.GmrRaster()
+    r.width, r.height = int(width), int(height)
+    bg = np.asarray(background, dtype=np.float64).reshape(3)
+    r.background[:] = [float(x) for x in bg]
+    r.dtype = _DT[dtype]
+    r.rescale = 1 if rescale else 0
+    r.flags = int(flags)
+    return r
+
+
+def mesh_struct(pos, col, faces) -> L.GmrMesh:
+    m = L.GmrMesh()
+    m.positions, m.colors, m.faces = pos.data_ptr(), col.data_ptr(), faces.data_ptr()
+    m.num_vertices, m.num_faces = int(pos.shape[0]), int(faces.shape[0])
+    return m
+
+
+class _Capacity:
+    """Entry-capacity estimate per (F, B, W, H): starts at 4 entries per
+    item and grows (x1.25 headroom) when a forward reports overflow."""
+
+    def __init__(self):
+        self._cap = {}
+
+    def get(self, key, items):
+        return self._cap.get(key, 4 * items + 4096)
+
+    def grow(self, key, needed):
+        self._cap[key] = int(needed * 1.25) + 4096
+        return self._cap[key]
+
+    def note(self, key, cap):
+        self._cap[key] = cap
+
+
+_capacity = _Capacity()
+_topologies = {}
+
+
+def topology(faces: torch.Tensor, num_vertices: int) -> torch.Tensor:
+    """Face->vertex CSR (convert.py:427-436 order), cached per faces tensor."""
+    key = (faces.data_ptr(), int(faces.shape[0]), int(num_vertices), faces._version)
+    topo = _topologies.get(key)
+    if topo is None:
+        lib = L.load()
+        nb = ctypes.c_size_t()
+        L.check(lib.gmr_topology_size(faces.shape[0], num_vertices, ctypes.byref(nb)))
+        topo = torch.empty(max(nb.value, 1), dtype=torch.uint8, device=faces.device)
+        L.check(lib.gmr_topology_build(_ptr(faces), faces.shape[0], num_vertices, _ptr(topo),
+                                       nb.value, _stream()))
+        if len(_topologies) > 16:
+            _topologies.clear()
+        _topologies[key] = (topo, faces)  # keep faces alive so the key stays valid
+        return topo
+    return topo[0]
+
+
+_FIELDS = ("mean2d", "cov2d", "conic", "depth", "color", "opacity")
+
+
+@dataclass
+class ForwardState:
+    """What a forward leaves for its backward (RenderContext device part)."""
+    ws: torch.Tensor
+    capacity: int
+    raster: L.GmrRaster
+    cams: ctypes.Array
+    views: int
+    entries: int
+    kept: int
+
+
+def _status_or_raise(ws, kind, item_to_index=None):
+    lib = L.load()
+    st = L.GmrStatus()
+    code = lib.gmr_status(_ptr(ws), ctypes.byref(st), _stream())
+    if code == L.GMR_ENONFINITE:
+        idx = st.nonfinite_item if item_to_index is None else item_to_index(st.nonfinite_item)
+        raise ValueError(f"non-finite splat parameter {_FIELDS[st.nonfinite_field]!r} at splat {idx}")
+    if code not in (L.GMR_OK, L.GMR_ECAPACITY):
+        L.check(code)
+    return st, code
+
+
+def render_forward(pos, col, faces, cams, width, height, background, rescale=True, flags=0,
+                   item_to_index=None):
+    """B-view forward.  pos/col [V,3] (f32|f64, cuda), faces [F,3] int32.
+    Returns (rgb [B,H,W,3], alpha [B,H,W], ForwardState)."""
+    lib = L.load()
+    dtype = pos.dtype
+    B, F = len(cams), int(faces.shape[0])
+    raster = raster_struct(width, height, background, dtype, rescale, flags)
+    cam_arr = L.camera_struct(cams)
+    mesh = mesh_struct(pos, col, faces)
+    key = (F, B, int(width), int(height), dtype)
+    cap = _capacity.get(key, F * B)
+    rgb = torch.empty((B, height, width, 3), dtype=dtype, device=pos.device)
+    alpha = torch.empty((B, height, width), dtype=dtype, device=pos.device)
+    for _ in range(3):
+        nb = ctypes.c_size_t()
+        L.check(lib.gmr_render_workspace_size(F, B, width, height, cap, raster.dtype, ctypes.byref(nb)))
+        ws = torch.empty(nb.value, dtype=torch.uint8, device=pos.device)
+        L.check(lib.gmr_render_forward(ctypes.byref(mesh), cam_arr, B, ctypes.byref(raster), _ptr(rgb),
+                                       _ptr(alpha), _ptr(ws), nb.value, cap, _stream()))
+        st, code = _status_or_raise(ws, "mesh", item_to_index)
+        if code == L.GMR_OK:
+            _capacity.note(key, cap)
+            return rgb, alpha, ForwardState(ws, cap, raster, cam_arr, B, st.entries, st.kept)
+        cap = _capacity.grow(key, st.entries)
+    raise RuntimeError("tile-entry capacity did not converge")
+
+
+def render_backward(state: ForwardState, pos, col, faces, rgb, g_rgb, g_alpha):
+    """Vertex position/colour grads [V,3] summed over the state's views."""
+    lib = L.load()
+    dtype = pos.dtype
+    g_rgb = g_rgb.to(dtype).contiguous()
+    g_alpha = g_alpha.to(dtype).contiguous()
+    topo = topology(faces, pos.shape[0])
+    g_pos = torch.empty_like(pos)
+    g_col = torch.empty_like(col)
+    mesh = mesh_struct(pos, col, faces)
+    L.check(lib.gmr_render_backward(ctypes.byref(mesh), state.cams, state.views,
+                                    ctypes.byref(state.raster), _ptr(rgb), _ptr(g_rgb), _ptr(g_alpha),
+                                    _ptr(g_pos), _ptr(g_col), _ptr(topo), _ptr(state.ws),
+                                    state.ws.numel(), state.capacity, _stream()))
+    return g_pos, g_col
+
+
+class GMRRender(torch.autograd.Function):
+    """rgb [B,H,W,3], alpha [B,H,W] = render(pos [V,3], col [V,3]; faces, cams)
+    with autograd to pos and col (reference render_mesh/render_backward
+    summed over views, losses.py:151-162)."""
+
+    @staticmethod
+    def forward(ctx, pos, col, faces, cams, width, height, background, rescale):
+        pos_c, col_c = pos.detach().contiguous(), col.detach().contiguous()
+        rgb, alpha, state = render_forward(pos_c, col_c, faces, cams, width, height, background, rescale)
+        ctx.state = state
+        ctx.save_for_backward(pos_c, col_c, faces, rgb)
+        return rgb, alpha
+
+    @staticmethod
+    def backward(ctx, g_rgb, g_alpha):
+        pos, col, faces, rgb = ctx.saved_tensors
+        if g_rgb is None:
+            g_rgb = torch.zeros_like(rgb)
+        if g_alpha is None:
+            g_alpha = torch.zeros(rgb.shape[:-1], dtype=rgb.dtype, device=rgb.device)
+        g_pos, g_col = render_backward(ctx.state, pos, col, faces, rgb, g_rgb, g_alpha)
+        return g_pos, g_col, None, None, None, None, None, None
+
+
+def render_views(pos, col, faces, cams, width, height, background=(0.0, 0.0, 0.0), rescale=True):
+    """Batched torch entry: B views of one mesh, differentiable in pos/col."""
+    return GMRRender.apply(pos, col, faces, list(cams), int(width), int(height),
+                           tuple(np.asarray(background, dtype=np.float64).reshape(3)), bool(rescale))
+
+
+# ---------------------------------------------------------------------------
+# splat path (rasterize / rasterize_backward stage functions)
+# ---------------------------------------------------------------------------
+
+def _splat_struct(mean2d, cov2d, depth, color, opacity):
+    s = L.GmrSplats()
+    s.mean2d, s.cov2d, s.depth = mean2d.data_ptr(), cov2d.data_ptr(), depth.data_ptr()
+    s.color, s.opacity, s.count = color.data_ptr(), opacity.data_ptr(), int(depth.shape[0])
+    return s
+
+
+def rasterize_forward(mean2d, cov2d, depth, color, opacity, width, height, background):
+    lib = L.load()
+    dtype = mean2d.dtype
+    K = int(depth.shape[0])
+    raster = raster_struct(width, height, background, dtype)
+    sp = _splat_struct(mean2d, cov2d, depth, color, opacity)
+    key = ("splats", K, int(width), int(height), dtype)
+    cap = _capacity.get(key, K)
+    rgb = torch.empty((height, width, 3), dtype=dtype, device=mean2d.device)
+    alpha = torch.empty((height, width), dtype=dtype, device=mean2d.device)
+    for _ in range(3):
+        nb = ctypes.c_size_t()
+        L.check(lib.gmr_raster_workspace_size(K, width, height, cap, raster.dtype, ctypes.byref(nb)))
+        ws = torch.empty(nb.value, dtype=torch.uint8, device=mean2d.device)
+        L.check(lib.gmr_rasterize_forward(ctypes.byref(sp), ctypes.byref(raster), _ptr(rgb), _ptr(alpha),
+                                          _ptr(ws), nb.value, cap, _stream()))
+        st, code = _status_or_raise(ws, "splats")
+        if code == L.GMR_OK:
+            _capacity.note(key, cap)
+            return rgb, alpha, ForwardState(ws, cap, raster, None, 1, st.entries, st.kept)
+        cap = _capacity.grow(key, st.entries)
+    raise RuntimeError("tile-entry capacity did not converge")
+
+
+def rasterize_backward(state, mean2d, cov2d, depth, color, opacity, rgb, g_rgb, g_alpha):
+    lib = L.load()
+    K = int(depth.shape[0])
+    dt = mean2d.dtype
+    gm = torch.empty((K, 2), dtype=dt, device=mean2d.device)
+    gc = torch.empty((K, 2, 2), dtype=dt, device=mean2d.device)
+    gcol = torch.empty((K, 3), dtype=dt, device=mean2d.device)
+    gop = torch.empty((K,), dtype=dt, device=mean2d.device)
+    sp = _splat_struct(mean2d, cov2d, depth, color, opacity)
+    L.check(lib.gmr_rasterize_backward(ctypes.byref(sp), ctypes.byref(state.raster), _ptr(rgb),
+                                       _ptr(g_rgb.to(dt).contiguous()), _ptr(g_alpha.to(dt).contiguous()),
+                                       _ptr(gm), _ptr(gc), _ptr(gcol), _ptr(gop), _ptr(state.ws),
+                                       state.ws.numel(), state.capacity, _stream()))
+    return gm, gc, gcol, gop
+
+
+# ---------------------------------------------------------------------------
+# inspection (bit-exact binning checks)
+# ---------------------------------------------------------------------------
+
+def copy_entries(state: ForwardState, items_per_view: int, mesh_path: bool):
+    lib = L.load()
+    dev = state.ws.device
+    items = torch.empty(max(state.entries, 1), dtype=torch.int32, device=dev)
+    bins = (((state.raster.width + 15) // 16) * ((state.raster.height + 15) // 16)) * state.views
+    bounds = torch.empty(bins + 1, dtype=torch.int32, device=dev)
+    L.check(lib.gmr_copy_entries(_ptr(state.ws), items_per_view, state.views, ctypes.byref(state.raster),
+                                 state.capacity, int(mesh_path), _ptr(items), _ptr(bounds), _stream()))
+    return items[:state.entries], bounds
+
+
+def copy_splats(state: ForwardState, items_per_view: int, mesh_path: bool):
+    lib = L.load()
+    dev = state.ws.device
+    dt = torch.float64 if state.raster.dtype == L.GMR_F64 else torch.float32
+    n = items_per_view * state.views
+    rec = torch.empty((n, 8), dtype=dt, device=dev)
+    rect = torch.empty((n, 2), dtype=torch.int32, device=dev)
+    cnt = torch.empty(n, dtype=torch.int32, device=dev)
+    aux = torch.empty((n, 2), dtype=dt, device=dev)
+    L.check(lib.gmr_copy_splats(_ptr(state.ws), items_per_view, state.views, ctypes.byref(state.raster),
+                                state.capacity, int(mesh_path), _ptr(rec), _ptr(rect), _ptr(cnt), _ptr(aux),
+                                _stream()))
+    return rec, rect, cnt, aux
+
+
+def convert(pos, col, faces, rescale=True):
+    lib = L.load()
+    F = int(faces.shape[0])
+    dt = pos.dtype
+    means = torch.empty((F, 3), dtype=dt, device=pos.device)
+    cov = torch.empty((F, 3, 3), dtype=dt, device=pos.device)
+    colors = torch.empty((F, 3), dtype=dt, device=pos.device)
+    degen = torch.empty(F, dtype=torch.uint8, device=pos.device)
+    mesh = mesh_struct(pos, col, faces)
+    L.check(lib.gmr_convert(ctypes.byref(mesh), int(rescale), _DT[dt], _ptr(means), _ptr(cov), _ptr(colors),
+                            _ptr(degen), _stream()))
+    return means, cov, colors, degen.bool()
+
+
+def convert_backward(pos, col, faces, g_means, g_cov, g_colors, rescale=True):
+    lib = L.load()
+    dt = pos.dtype
+    topo = topology(faces, pos.shape[0])
+    nb = ctypes.c_size_t()
+    L.check(lib.gmr_convert_scratch_size(faces.shape[0], _DT[dt], ctypes.byref(nb)))
+    scratch = torch.empty(max(nb.value, 1), dtype=torch.uint8, device=pos.device)
+    gp = torch.empty_like(pos)
+    gc = torch.empty_like(col)
+    mesh = mesh_struct(pos, col, faces)
+    L.check(lib.gmr_convert_backward(ctypes.byref(mesh), int(rescale), _DT[dt], _ptr(g_means.to(dt).contiguous()),
+                                     _ptr(g_cov.to(dt).contiguous()), _ptr(g_colors.to(dt).contiguous()),
+                                     _ptr(gp), _ptr(gc), _ptr(topo), _ptr(scratch), nb.value, _stream()))
+    return gp, gc

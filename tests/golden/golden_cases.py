@@ -1,0 +1,132 @@
+"""Deterministic inputs of the golden fixtures (shared by make_golden.py,
+which feeds them to the real reference, and by the tests, which feed them to
+the oracle and to the CUDA path).  Pure numpy + the product's own container
+types; nothing here reads /root/reference."""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+_ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+if _ROOT not in sys.path:
+    sys.path.insert(0, _ROOT)
+
+from paper_2602_14493_b200.camera import Camera, default_intrinsics, look_at  # noqa: E402
+from paper_2602_14493_b200.mesh import make_icosphere  # noqa: E402
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def load(name):
+    with np.load(os.path.join(HERE, f"{name}.npz")) as z:
+        return {k: z[k] for k in z.files}
+
+
+def identity_camera(width=32, height=32, f=40.0):
+    """reference tests/test_render.py:26-31."""
+    return Camera(rotation=np.eye(3), translation=np.zeros(3), fx=f, fy=f,
+                  cx=(width - 1) / 2, cy=(height - 1) / 2, width=width, height=height)
+
+
+def octahedron_mesh():
+    """reference tests/test_render.py:34-44."""
+    v = np.array([(1, 0, 0), (-1, 0, 0), (0, 1, 0), (0, -1, 0), (0, 0, 1), (0, 0, -1)], float)
+    f = np.array([(0, 2, 4), (2, 1, 4), (1, 3, 4), (3, 0, 4),
+                  (2, 0, 5), (1, 2, 5), (3, 1, 5), (0, 3, 5)])
+    col = np.random.default_rng(0).random((6, 3)) * 0.8 + 0.1
+    return v, f, col
+
+
+def _grads(rng, h, w):
+    return rng.normal(size=(h, w, 3)), rng.normal(size=(h, w))
+
+
+def c1_case():
+    """Config 1: icosphere L3 (1,280 F), 128^2, camera of BASELINE.md §2."""
+    m = make_icosphere(1280)
+    col = np.random.default_rng(0).uniform(0.1, 0.9, size=(m.num_vertices, 3))
+    cam = look_at((0.3, -2.4, 1.6), (0, 0, 0), **default_intrinsics(128, 128))
+    g_rgb, g_a = _grads(np.random.default_rng(0), 128, 128)
+    return dict(vertices=np.asarray(m.vertices), facets=np.asarray(m.facets), colors=col,
+                camera=cam, background=np.array([0.1, 0.1, 0.1]), g_rgb=g_rgb, g_alpha=g_a)
+
+
+def octahedron_case():
+    """reference tests/test_render.py:442-450."""
+    v, f, col = octahedron_mesh()
+    cam = look_at((1.7, -2.2, 1.4), (0, 0, 0), **default_intrinsics(32, 32))
+    g_rgb, g_a = _grads(np.random.default_rng(7), 32, 32)
+    return dict(vertices=v, facets=f, colors=col, camera=cam,
+                background=np.array([0.1, 0.1, 0.1]), g_rgb=g_rgb, g_alpha=g_a)
+
+
+def small_render_case():
+    """Non-square image with a partial tile row (reference test_render.py:236-243 camera)."""
+    m = make_icosphere(320)
+    col = np.random.default_rng(3).uniform(0.1, 0.9, size=(m.num_vertices, 3))
+    cam = look_at((0.5, -2.5, 1.5), (0, 0, 0), **default_intrinsics(64, 48))
+    g_rgb, g_a = _grads(np.random.default_rng(11), 48, 64)
+    return dict(vertices=np.asarray(m.vertices), facets=np.asarray(m.facets), colors=col,
+                camera=cam, background=np.array([0.2, 0.3, 0.4]), g_rgb=g_rgb, g_alpha=g_a)
+
+
+def splat_case():
+    """Seven random splats (reference test_render.py:326-349 generator)."""
+    rng = np.random.default_rng(5)
+    bg = rng.random(3)
+    mean2d, cov2d, depth, color, opacity = [], [], [], [], []
+    for _ in range(7):
+        a = rng.normal(size=(2, 2))
+        cov2d.append(a @ a.T + 1.5 * np.eye(2))
+        mean2d.append(rng.uniform(6, 26, size=2))
+        depth.append(float(rng.uniform(1, 5)))
+        color.append(rng.random(3))
+        opacity.append(float(rng.uniform(0.25, 0.65)))
+    g_rgb, g_a = rng.normal(size=(32, 32, 3)), rng.normal(size=(32, 32))
+    return dict(camera=identity_camera(), background=bg, mean2d=np.array(mean2d),
+                cov2d=np.array(cov2d), depth=np.array(depth), color=np.array(color),
+                opacity=np.array(opacity), source=np.arange(7), g_rgb=g_rgb, g_alpha=g_a)
+
+
+def closed_form_splat_case():
+    """Opaque red over blue at a pixel centre, a depth tie, a clamp pixel and
+    a faint splat (reference test_render.py:173-199)."""
+    mean2d = np.array([(16, 16), (16, 16), (5, 5), (5, 5), (26, 8), (8, 26)], float)
+    cov2d = np.array([np.eye(2) * 2.0] * 6)
+    depth = np.array([2.0, 1.0, 1.0, 1.0, 3.0, 1.5])
+    color = np.array([(0, 0, 1), (1, 0, 0), (1, 0, 0), (0, 0, 1), (1, 1, 1), (0.2, 0.9, 0.4)], float)
+    opacity = np.array([1.0, 1.0, 0.7, 0.7, 1.0, 0.005])
+    rng = np.random.default_rng(12)
+    return dict(camera=identity_camera(), background=np.array([0.0, 0.0, 0.0]), mean2d=mean2d,
+                cov2d=cov2d, depth=depth, color=color, opacity=opacity, source=np.arange(6),
+                g_rgb=rng.normal(size=(32, 32, 3)), g_alpha=rng.normal(size=(32, 32)))
+
+
+def loss_case():
+    """total_loss batch (reference test_losses.py:158-170 style), 3 views 16^2."""
+    v, f, col = octahedron_mesh()
+    rng = np.random.default_rng(4)
+    cams, rgbs, masks = [], [], []
+    for _ in range(3):
+        p = rng.normal(size=3)
+        cams.append(look_at(p / np.linalg.norm(p) * 2.6, (0, 0, 0), **default_intrinsics(16, 16)))
+        rgbs.append(rng.random((16, 16, 3)))
+        masks.append((rng.random((16, 16)) > 0.4).astype(float))
+    return dict(vertices=v, facets=f, colors=col, cameras=cams, target_rgb=rgbs,
+                target_mask=masks, background=np.array([0.1, 0.1, 0.1]))
+
+
+def convert_case():
+    """50 random facets plus a degenerate and a clamped-kappa facet
+    (reference test_convert.py:360-417)."""
+    rng = np.random.default_rng(42)
+    v = rng.normal(size=(150, 3))
+    f = np.arange(150).reshape(50, 3)
+    v[3:6] = [(0, 0, 0), (1, 0, 0), (2, 0, 0)]                  # collinear -> degenerate
+    v[6:9] = rng.normal(size=(3, 3)) * 1e-3                      # area ~1e-6 -> clamped
+    col = rng.random((150, 3))
+    return dict(vertices=v, facets=f, colors=col, g_means=rng.normal(size=(50, 3)),
+                g_cov3d=rng.normal(size=(50, 3, 3)), g_colors=rng.normal(size=(50, 3)))

@@ -1,0 +1,103 @@
+"""Generate golden fixtures by running the REAL reference (meshsplat).
+
+Run in the build container, where /root/reference exists:
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+
+Writes tests/golden/*.npz.  The GPU box never needs /root/reference: tests
+read these committed fixtures.  Inputs are regenerated deterministically by
+`golden_cases.py` (shared with the tests), so only outputs are stored.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REF_SRC = os.environ.get("GMR_REFERENCE_SRC", "/root/reference/pkg/src")
+sys.path.insert(0, REF_SRC)
+sys.path.insert(0, HERE)
+sys.dont_write_bytecode = True
+
+import meshsplat as ms  # noqa: E402  (the reference)
+from meshsplat.render import Splat2D, _RasterPlan, rasterize_backward  # noqa: E402
+
+import golden_cases as gc  # noqa: E402
+
+
+def ref_mesh(case):
+    return ms.TriangleMesh(case["vertices"], case["facets"], case["colors"])
+
+
+def ref_cam(c):
+    return ms.Camera(rotation=c.rotation, translation=c.translation, fx=c.fx, fy=c.fy,
+                     cx=c.cx, cy=c.cy, width=c.width, height=c.height, near=c.near, far=c.far)
+
+
+def render_case(name, case, dtypes=(np.float64, np.float32)):
+    mesh = ref_mesh(case)
+    cam = ref_cam(case["camera"])
+    out = {}
+    for dt in dtypes:
+        tag = "f64" if dt == np.float64 else "f32"
+        o, ctx = ms.render_mesh(mesh, cam, background=case["background"], dtype=dt, return_ctx=True)
+        gv, gcol = ms.render_backward(ctx, case["g_rgb"], case["g_alpha"])
+        plan = _RasterPlan(ctx.batch, cam.width, cam.height)
+        out[f"{tag}_rgb"] = o.rgb
+        out[f"{tag}_alpha"] = o.alpha
+        out[f"{tag}_grad_v"] = gv
+        out[f"{tag}_grad_c"] = gcol
+        out[f"{tag}_source"] = ctx.batch.source
+        out[f"{tag}_mean2d"] = ctx.batch.mean2d
+        out[f"{tag}_radius"] = ctx.batch.radius
+        out[f"{tag}_depth"] = ctx.batch.depth
+        out[f"{tag}_entry_source"] = ctx.batch.source[plan.entry_splat]
+        out[f"{tag}_bounds"] = plan.bounds
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+    print(name, {k: v.shape for k, v in out.items()})
+
+
+def splat_case(name, case):
+    cam = ref_cam(case["camera"])
+    sp = [Splat2D(mean2d=m, cov2d_screen=c, depth=float(d), color=col, opacity=float(o), source=int(s))
+          for m, c, d, col, o, s in zip(case["mean2d"], case["cov2d"], case["depth"],
+                                         case["color"], case["opacity"], case["source"])]
+    o = ms.rasterize(sp, cam, case["background"])
+    gm, gcv, gcol, gop = rasterize_backward(sp, cam, o, case["g_rgb"], case["g_alpha"])
+    out = dict(rgb=o.rgb, alpha=o.alpha, g_mean2d=gm, g_cov2d=gcv, g_color=gcol, g_opacity=gop)
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+    print(name, {k: v.shape for k, v in out.items()})
+
+
+def loss_case(name, case):
+    mesh = ref_mesh(case)
+    cams = [ref_cam(c) for c in case["cameras"]]
+    w = ms.LossWeights(color=1.0, silhouette=1.0, edge=0.0, laplacian=0.0)
+    rep, gv, gcol = ms.total_loss(mesh, cams, case["target_rgb"], case["target_mask"],
+                                  weights=w, background=case["background"], dtype=np.float64)
+    out = dict(color=rep.color, silhouette=rep.silhouette, grad_v=gv, grad_c=gcol)
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+    print(name, {k: np.shape(v) for k, v in out.items()})
+
+
+def convert_case(name, case):
+    mesh = ref_mesh(case)
+    cloud = ms.convert_mesh(mesh)
+    gv, gcol = ms.convert_backward(mesh, cloud, case["g_means"], case["g_cov3d"], case["g_colors"])
+    out = dict(means=cloud.means, cov3d=cloud.cov3d, colors=cloud.colors,
+               degenerate=cloud.degenerate, grad_v=gv, grad_c=gcol)
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+    print(name, {k: v.shape for k, v in out.items()})
+
+
+if __name__ == "__main__":
+    render_case("c1_icosphere1280_128", gc.c1_case())
+    render_case("octahedron_32", gc.octahedron_case())
+    render_case("icosphere320_64x48", gc.small_render_case())
+    splat_case("splats7_32", gc.splat_case())
+    splat_case("splats_closed_form_32", gc.closed_form_splat_case())
+    loss_case("loss_octa_3views_16", gc.loss_case())
+    convert_case("convert_random50", gc.convert_case())
