@@ -56,11 +56,11 @@ def _device_mesh(mesh, dtype):
         per = {}
     hit = per.get(tdt)
     if hit is None:
-        pos = torch.as_tensor(np.ascontiguousarray(mesh.vertices), dtype=tdt).to(dev)
-        col = torch.as_tensor(np.ascontiguousarray(mesh.colors), dtype=tdt).to(dev)
+        pos = torch.as_tensor(np.array(mesh.vertices, dtype=np.float64), dtype=tdt).to(dev)
+        col = torch.as_tensor(np.array(mesh.colors, dtype=np.float64), dtype=tdt).to(dev)
         faces = per.get("faces")
         if faces is None:
-            faces = torch.as_tensor(np.ascontiguousarray(mesh.facets), dtype=torch.int32).to(dev)
+            faces = torch.as_tensor(np.array(mesh.facets, dtype=np.int32)).to(dev)
             per["faces"] = faces
         hit = per[tdt] = (pos, col, faces)
     return hit

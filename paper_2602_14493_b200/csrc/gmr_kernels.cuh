@@ -89,8 +89,8 @@ __device__ __forceinline__ void load_face(const S* __restrict__ pos, const int32
   S det2d = g.area * g.area / S(108);
   g.clamped = det2d < S(kDetEps);
   if (rescale) {
-    // unclamped: area / (pi sqrt(area^2/108)) == sqrt(108)/pi exactly
-    g.kappa = g.clamped ? g.area / (S(kPi) * S(1e-7)) : S(3.3080430866842937);
+    // convert.py:267 (== sqrt(108)/pi up to rounding when unclamped)
+    g.kappa = g.area / (S(kPi) * sqrt_s(g.clamped ? S(kDetEps) : det2d));
   } else {
     g.kappa = S(1);
   }
@@ -909,7 +909,7 @@ __global__ void __launch_bounds__(128) face_convert_backward(const S* __restrict
 #pragma unroll
         for (int c = 0; c < 3; ++c)
           dk += G[r][c] * (g.e[0][r] * g.e[0][c] + g.e[1][r] * g.e[1][c] + g.e[2][r] * g.e[2][c]) / S(36);
-      d_area = dk / (S(kPi) * S(1e-7));
+      d_area = dk / (S(kPi) * sqrt_s(S(kDetEps)));
     }
     S gn[3];
 #pragma unroll
