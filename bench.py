@@ -1,0 +1,389 @@
+#!/usr/bin/env python
+"""GMR hot-path benchmark: forward+backward views/s (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl gmr|reference]
+
+A step = forward + backward of one batch of views of the config's mesh
+(device-resident inputs), ending with the vertex-gradient sum over the batch
+(and, for N > 1 ranks, an NCCL all-reduce of [grad_pos | grad_col]).  Views
+are sharded across ranks (weak scaling: `views` per GPU).  `value` = views
+of all ranks / max-over-ranks device time.  `e2e` = the same metric through
+the public torch API (`render_views` + autograd) with pinned host inputs
+copied in and gradients copied out every step.  `roofline` = the dominant
+stage's algorithmic bytes per launch / its CUDA-event time (timed live in
+the library on the launching stream), against MEASURED_PEAKS.json.
+
+`--impl reference` times the reference algorithm on the host cores (the
+pinned numpy restatement in oracle/, one process per core, one view each;
+bounded sample, see oracle/cpu_baseline.py).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "c1": dict(mesh=("icosphere", 1280), res=128, views=1,
+               desc="config1: icosphere subdiv-3 (1,280 faces), 128x128"),
+    "c2": dict(mesh=("icosphere", 81920), res=512, views=8,
+               desc="config2: icosphere subdiv-6 (81,920 faces), 512x512"),
+    "c3": dict(mesh=("geodesic", 158), res=800, views=8,
+               desc="config3: geodesic displaced sphere n=158 (499,280 faces, 249,642 vertices), 800x800"),
+    "c3b1": dict(mesh=("geodesic", 158), res=800, views=1,
+                 desc="config3 batch 1: geodesic displaced sphere n=158 (499,280 faces), 800x800"),
+    "c4": dict(mesh=("geodesic", 316), res=1024, views=8,
+               desc="config4: geodesic displaced sphere n=316 (1,997,120 faces), 1024x1024"),
+}
+METRIC = "fwd+bwd views/sec @500K faces 800x800; HBM GB/s vs peak; 1/2/4/8 GPU"
+BG = (0.1, 0.1, 0.1)
+
+
+def build_mesh(cfg):
+    import paper_2602_14493_b200 as gmr
+    kind, n = cfg["mesh"]
+    if kind == "geodesic":
+        return gmr.make_geodesic_sphere(n, seed=0)
+    m = gmr.make_icosphere(n)
+    return gmr.TriangleMesh(m.vertices, m.facets, gmr.seeded_colors(m.num_vertices, 0))
+
+
+def all_cams(cfg, total):
+    import paper_2602_14493_b200 as gmr
+    return gmr.hemisphere_cameras(total, 3.0, (cfg["res"], cfg["res"]))
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.samples = []
+        self.proc = None
+        self.window = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-i", str(gpu_index), "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 6:
+                self.samples.append((time.time(), parts))
+
+    def mark(self, t0, t1):
+        self.window = (t0, t1)
+
+    def summary(self):
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        t0, t1 = self.window or (0, 1e30)
+        inside = [p for t, p in self.samples if t0 - 0.05 <= t <= t1 + 0.05] or [p for _, p in self.samples[-3:]]
+        sm = sorted(float(p[0]) for p in inside if p[0].replace(".", "").isdigit())
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({names[i] for p in inside for i in range(4) if "Active" in p[2 + i]
+                          and "Not" not in p[2 + i]})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None,
+                "sm_max_mhz": float(inside[0][1]) if inside[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(inside)}
+
+
+def stage_bytes(F, V, B, W, H, E, bins):
+    """Algorithmic bytes per launch of each stage (fp32 values, int32 indices;
+    each array crossing the kernel boundary once)."""
+    n = F * B
+    px = W * H * B
+    entry_passes = max(1, (max(1, (bins - 1).bit_length()) + 7) // 8)
+    return {
+        "convert_project": 12 * F + 24 * V + 16 * F + 52 * n,
+        "depth_sort": 4 * 20 * n,
+        "scan_emit": 36 * n + 8 * E,
+        "tile_sort_ranges": 20 * entry_passes * E + 4 * E + 4 * bins,
+        "blend_forward": 8 * bins + 52 * E + 20 * px,
+        "blend_backward": 8 * bins + 96 * E + 32 * px,
+        "face_backward": 24 * F + 24 * V + 40 * n + 32 * E + 48 * F + 48 * F + 72 * F,
+        "vertex_gather": 4 * V + 12 * F + 72 * F + 24 * V,
+    }
+
+
+def survey_bytes_per_view(F, V, E_view, T, W, H):
+    """SURVEY §8d compulsory bytes of the whole fwd+bwd per view."""
+    return 160 * F + 60 * V + 116 * E_view + 24 * T + 48 * W * H
+
+
+def run_gmr(args, cfg):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2602_14493_b200 as gmr
+    from paper_2602_14493_b200 import engine, lib
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    L = lib.load()
+    mesh = build_mesh(cfg)
+    B, W = cfg["views"], cfg["res"]
+    H = W
+    cams = all_cams(cfg, B * world)[rank * B:(rank + 1) * B]
+    pos = torch.tensor(np.asarray(mesh.vertices), dtype=torch.float32, device=dev)
+    col = torch.tensor(np.asarray(mesh.colors), dtype=torch.float32, device=dev)
+    faces = torch.tensor(np.asarray(mesh.facets), dtype=torch.int32, device=dev)
+    F, V = faces.shape[0], pos.shape[0]
+    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+    g_rgb = torch.randn((B, H, W, 3), generator=gen, device=dev)
+    g_a = torch.randn((B, H, W), generator=gen, device=dev)
+
+    state = {}
+
+    def step():
+        rgb, alpha, st = engine.render_forward(pos, col, faces, cams, W, H, BG)
+        gp, gc = engine.render_backward(st, pos, col, faces, rgb, g_rgb, g_a)
+        if world > 1:
+            buf = torch.cat([gp, gc], dim=1)
+            dist.all_reduce(buf)
+        state["st"] = st
+        return gp
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local) if rank == 0 else None
+    time.sleep(0.3 if sampler else 0)
+    L.gmr_timing_enable(1)
+    L.gmr_timing_read(None, None, 0, 1)
+    n0 = L.gmr_launch_count()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    wall0 = time.time()
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    wall1 = time.time()
+    if world > 1:
+        dist.barrier()
+    launches = (L.gmr_launch_count() - n0) // args.steps
+    ms = e0.elapsed_time(e1)
+    import ctypes
+    sms = (ctypes.c_double * 8)()
+    scnt = (ctypes.c_int64 * 8)()
+    L.gmr_timing_read(sms, scnt, 8, 1)
+    L.gmr_timing_enable(0)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    if sampler:
+        sampler.mark(wall0, wall1)
+    st = state["st"]
+    E = int(st.entries)
+    bins = ((W + 15) // 16) * ((H + 15) // 16) * B
+    value = B * world * args.steps / (ms / 1e3)
+
+    # ---- end to end through the public torch API, host buffers -------------
+    pin = lambda t: t.cpu().pin_memory()
+    h_pos, h_col, h_g, h_a = pin(pos), pin(col), pin(g_rgb), pin(g_a)
+    o_gp, o_gc = torch.empty_like(h_pos).pin_memory(), torch.empty_like(h_col).pin_memory()
+    d_g, d_a = torch.empty_like(g_rgb), torch.empty_like(g_a)
+
+    def e2e_step():
+        p = h_pos.to(dev, non_blocking=True).requires_grad_(True)
+        c = h_col.to(dev, non_blocking=True).requires_grad_(True)
+        d_g.copy_(h_g, non_blocking=True)
+        d_a.copy_(h_a, non_blocking=True)
+        rgb, alpha = gmr.render_views(p, c, faces, cams, W, H, BG)
+        torch.autograd.backward([rgb, alpha], [d_g, d_a])
+        gp, gc = p.grad, c.grad
+        if world > 1:
+            buf = torch.cat([gp, gc], dim=1)
+            dist.all_reduce(buf)
+            gp, gc = buf[:, :3], buf[:, 3:]
+        o_gp.copy_(gp, non_blocking=True)
+        o_gc.copy_(gc, non_blocking=True)
+
+    for _ in range(max(1, args.warmup)):
+        e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    k_e2e = max(3, args.steps // 2)
+    e0.record()
+    for _ in range(k_e2e):
+        e2e_step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms_e2e = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms_e2e], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t.item())
+    h2d = (h_pos.numel() + h_col.numel() + h_g.numel() + h_a.numel()) * 4
+    d2h = (o_gp.numel() + o_gc.numel()) * 4
+    clocks = sampler.summary() if sampler else None
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return None
+
+    # ---- roofline of the dominant stage ------------------------------------
+    peak, peak_src = load_peaks()
+    names = lib.STAGES
+    sb = stage_bytes(F, V, B, W, H, E, bins)
+    stages = {}
+    for i, nm in enumerate(names):
+        if scnt[i]:
+            per = sms[i] / scnt[i]
+            stages[nm] = {"ms_per_launch": round(per, 4), "launches_per_step": scnt[i] // args.steps,
+                          "GBs": round(sb[nm] / (per / 1e3) / 1e9, 1)}
+    dom = max(stages, key=lambda k: stages[k]["ms_per_launch"] * stages[k]["launches_per_step"])
+    dper = stages[dom]["ms_per_launch"]
+    achieved = sb[dom] / (dper / 1e3) / 1e9
+    step_bytes = survey_bytes_per_view(F, V, E / B, (W // 16) * (H // 16), W, H) * B
+    step_gbs = step_bytes / (ms / args.steps / 1e3) / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "traffic_r01.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(dom)
+        except Exception:
+            traffic = None
+
+    # ---- CPU baseline (rank 0, N = 1, bounded sample) -----------------------
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        from oracle.cpu_baseline import ViewWorkers
+        wk = ViewWorkers(mesh.vertices, mesh.facets, mesh.colors, all_cams(cfg, max(8, B)), BG)
+        vps, det = wk.step(face_stride=1, tile_stride=args.cpu_tile_stride)
+        wk.close()
+        cpu = {"value": round(vps, 5), "unit": "views/s", "cores": wk.procs, "kind": "port",
+               "sample": (f"{wk.procs} concurrent views (one process per core), numpy restatement of the "
+                          f"reference (oracle/gmr_oracle.py) in fp32: all per-face stages and binning in "
+                          f"full, blend loops on every {args.cpu_tile_stride}th tile scaled to all tiles; "
+                          f"{det['per_view_s']:.1f} s per view extrapolated")}
+
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "views/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (procedural mesh, seeded vertex colours, N(0,1) upstream image grads)",
+        "config": {"workload": cfg["desc"] + f", {B} views per GPU per step (hemisphere cameras r=3)",
+                   "faces": F, "vertices": V, "views_per_gpu": B, "resolution": [W, H],
+                   "tile_entries_per_step": E, "l2": "inputs+workspace per step > 126 MB L2 (no flush needed)",
+                   "parallelism": f"views sharded over {world} GPU(s), NCCL all-reduce of vertex grads"},
+        "e2e": {"value": round(B * world * k_e2e / (ms_e2e / 1e3), 2), "unit": "views/s",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "api": "paper_2602_14493_b200.render_views + torch.autograd.backward, pinned host buffers"},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "peak_source": peak_src},
+        "step_roofline": {"bytes_per_step": int(step_bytes), "achieved_GBs": round(step_gbs, 1),
+                          "frac": round(step_gbs / peak, 4),
+                          "model": "SURVEY 8d: 160F+60V+116E+24T+48WH per view"},
+        "stages": stages,
+        "clocks": clocks,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return line
+
+
+def run_reference(args, cfg):
+    """CPU arm: the reference algorithm on the host cores (bounded samples)."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return None
+    import numpy as np
+    from oracle.cpu_baseline import ViewWorkers
+    mesh = build_mesh(cfg)
+    B = cfg["views"]
+    wk = ViewWorkers(mesh.vertices, mesh.facets, mesh.colors, all_cams(cfg, max(8, B * world)), BG)
+    for _ in range(args.warmup):
+        wk.step(face_stride=64, tile_stride=512)
+    t0 = time.perf_counter()
+    vals = []
+    for _ in range(args.steps):
+        v, det = wk.step(face_stride=args.ref_face_stride, tile_stride=args.ref_tile_stride)
+        vals.append(v)
+    wall = time.perf_counter() - t0
+    wk.close()
+    value = float(np.mean(vals))
+    sample = (f"{wk.procs} concurrent views (one process per host core), reference algorithm (numpy "
+              f"restatement pinned to meshsplat) in fp32; per step every {args.ref_face_stride}th face for "
+              f"the per-face stages and every {args.ref_tile_stride}th tile for the blend loops, binning in "
+              f"full, times scaled to whole views")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 5), "unit": "views/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * (B * world) / value, 1), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": cfg["desc"] + f", {B} views per GPU-equivalent step", "sampled_wall_s": round(wall, 1)},
+        "cpu_baseline": {"value": round(value, 5), "unit": "views/s", "cores": wk.procs, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": round(value, 5), "unit": "views/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return line
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="gmr", choices=["gmr", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    ap.add_argument("--cpu-tile-stride", type=int, default=16)
+    ap.add_argument("--ref-face-stride", type=int, default=8)
+    ap.add_argument("--ref-tile-stride", type=int, default=32)
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_gmr(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -91,6 +91,17 @@ typedef struct {
 const char* gmr_last_error(void);
 const char* gmr_version(void);
 
+/* Per-stage device timers (CUDA events on the launching stream; calling
+ * thread only).  Stages: 0 convert+project, 1 depth sort, 2 count scan +
+ * entry emission, 3 tile sort + ranges, 4 blend forward, 5 blend backward,
+ * 6 face backward (projection + conversion), 7 vertex gather.
+ * gmr_timing_read waits for the recorded events and returns the number of
+ * stages; ms / launches may be null. */
+void gmr_timing_enable(int32_t on);
+/* Number of kernels this thread has launched through the library. */
+int64_t gmr_launch_count(void);
+int gmr_timing_read(double* ms, int64_t* launches, int32_t n, int32_t reset);
+
 /* ---- mesh path: B views in one call --------------------------------- */
 
 /* Bytes of workspace for F faces, B views of W x H, and up to

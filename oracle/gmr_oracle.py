@@ -245,9 +245,11 @@ def _blend_terms(s: Splats, ids, uu, vv):
                 weight=weight, t_final=keep[:, -1])
 
 
-def composite(s: Splats, width, height, background=(0.0, 0.0, 0.0), dtype=np.float64):
+def composite(s: Splats, width, height, background=(0.0, 0.0, 0.0), dtype=np.float64,
+              tiles=None):
     """Front-to-back blend over a constant background (render.py:272-291).
-    Returns (rgb HxWx3, alpha HxW)."""
+    Returns (rgb HxWx3, alpha HxW).  `tiles` (timing only) restricts the
+    per-tile loop to a subset of tile ids."""
     check_finite(s)
     bg = np.asarray(background, dtype=dtype)
     rgb = np.empty((height, width, 3), dtype=dtype)
@@ -255,7 +257,7 @@ def composite(s: Splats, width, height, background=(0.0, 0.0, 0.0), dtype=np.flo
     alpha = np.zeros((height, width), dtype=dtype)
     ntx = (width + TILE - 1) // TILE
     entry, bounds = bin_splats(s.mean2d, s.radius, s.depth, s.source, width, height)
-    for tid in range(len(bounds) - 1):
+    for tid in (range(len(bounds) - 1) if tiles is None else tiles):
         ids = entry[bounds[tid]:bounds[tid + 1]]
         if len(ids) == 0:
             continue
@@ -268,7 +270,7 @@ def composite(s: Splats, width, height, background=(0.0, 0.0, 0.0), dtype=np.flo
 
 
 def composite_backward(s: Splats, width, height, background, grad_rgb, grad_alpha,
-                       dtype=np.float64):
+                       dtype=np.float64, tiles=None):
     """Screen-space gradients (g_mean2d, g_cov2d, g_color, g_opacity) of
     sum(g_rgb*rgb)+sum(g_alpha*alpha), tile-major accumulation
     (render.py:294-361)."""
@@ -285,7 +287,7 @@ def composite_backward(s: Splats, width, height, background, grad_rgb, grad_alph
     g_op = np.zeros(k, dtype=dtype)
     ntx = (width + TILE - 1) // TILE
     entry, bounds = bin_splats(s.mean2d, s.radius, s.depth, s.source, width, height)
-    for tid in range(len(bounds) - 1):
+    for tid in (range(len(bounds) - 1) if tiles is None else tiles):
         ids = entry[bounds[tid]:bounds[tid + 1]]
         if len(ids) == 0:
             continue

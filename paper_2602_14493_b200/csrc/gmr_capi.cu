@@ -10,6 +10,8 @@
 
 #include <algorithm>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "gmr_kernels.cuh"
 
@@ -36,11 +38,44 @@ int fail(int code, const char* fmt, ...) {
     if (e_ != cudaSuccess) return fail(GMR_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
   } while (0)
 
+thread_local long long g_launches = 0;   // kernels launched by this thread (bench evidence)
+
 #define GMR_LAUNCHED()                                                                   \
   do {                                                                                   \
+    ++g_launches;                                                                        \
     cudaError_t e_ = cudaGetLastError();                                                 \
     if (e_ != cudaSuccess) return fail(GMR_ECUDA, "launch: %s (%s:%d)", cudaGetErrorString(e_), __FILE__, __LINE__); \
   } while (0)
+
+// Optional per-stage CUDA-event timers (gmr_timing_enable / gmr_timing_read):
+// events are recorded on the launching stream around each stage, so bench.py
+// can attribute device time to kernels inside its own timed region.
+enum Stage { kStProject = 0, kStDepthSort, kStEmit, kStTileSort, kStBlendFwd, kStBlendBwd, kStFaceBwd,
+             kStVertex, kNumStages };
+struct StageTimer {
+  bool on = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending[kNumStages];
+  double ms[kNumStages] = {0};
+  long long calls[kNumStages] = {0};
+};
+thread_local StageTimer g_timer;
+
+struct StageScope {
+  int stage;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr, b = nullptr;
+  StageScope(int s, cudaStream_t stream) : stage(s), st(stream) {
+    if (!g_timer.on) return;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, st);
+  }
+  ~StageScope() {
+    if (!a) return;
+    cudaEventRecord(b, st);
+    g_timer.pending[stage].emplace_back(a, b);
+  }
+};
 
 inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 inline int ceil_log2(uint64_t x) {
@@ -143,8 +178,14 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
   // depth order of all items (stable: ties keep item = (view, face) order)
   K* dk[2] = {at<K>(ws, L.dkey[0]), at<K>(ws, L.dkey[1])};
   uint32_t* di[2] = {at<uint32_t>(ws, L.ditem[0]), at<uint32_t>(ws, L.ditem[1])};
-  int cur = radix_sort_pairs<K>(dk, di, nullptr, items, items, L.depth_bits, at<uint32_t>(ws, L.hist), st);
+  int cur;
+  {
+    StageScope sc(kStDepthSort, st);
+    cur = radix_sort_pairs<K>(dk, di, nullptr, items, items, L.depth_bits, at<uint32_t>(ws, L.hist), st);
+    g_launches += 3 * ((L.depth_bits + 7) / 8) - 1;
+  }
   GMR_LAUNCHED();
+  StageScope* emit_scope = new StageScope(kStEmit, st);
   const uint32_t* order = di[cur];
   const uint32_t* count = at<uint32_t>(ws, L.count);
   const int nb = (int)((items + kScanTile - 1) / kScanTile);
@@ -171,11 +212,16 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
                                                        nent, ek[0], ev[0]);
     GMR_LAUNCHED();
   }
+  delete emit_scope;
   const uint32_t ecap = (uint32_t)std::min<uint64_t>(L.ecap, 0xffffffffu);
-  int ecur = radix_sort_pairs<uint32_t>(ek, ev, nent, 0, ecap, L.entry_bits, at<uint32_t>(ws, L.hist), st);
-  GMR_LAUNCHED();
-  tile_ranges<<<grid_for((uint64_t)ecap + 1, 256), 256, 0, st>>>(ek[ecur], nent, 0, (uint32_t)L.bins,
-                                                                at<uint32_t>(ws, L.bounds));
+  int ecur;
+  {
+    StageScope sc(kStTileSort, st);
+    ecur = radix_sort_pairs<uint32_t>(ek, ev, nent, 0, ecap, L.entry_bits, at<uint32_t>(ws, L.hist), st);
+    g_launches += 3 * ((L.entry_bits + 7) / 8);
+    tile_ranges<<<grid_for((uint64_t)ecap + 1, 256), 256, 0, st>>>(ek[ecur], nent, 0, (uint32_t)L.bins,
+                                                                  at<uint32_t>(ws, L.bounds));
+  }
   GMR_LAUNCHED();
   BlendArgs<S> a{};
   a.bounds = at<uint32_t>(ws, L.bounds);
@@ -196,6 +242,7 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
   a.alpha = (S*)alpha;
   a.t_final = at<S>(ws, L.t_final);
   if (L.bins) {
+    StageScope sc(kStBlendFwd, st);
     blend_forward<S><<<(unsigned)L.bins, kBlendThreads, 0, st>>>(a);
     GMR_LAUNCHED();
   }
@@ -231,6 +278,7 @@ int render_forward_t(const GmrMesh* m, const GmrCamera* cams, int B, const GmrRa
     a.aux = (r->flags & GMR_FLAG_DEBUG_AUX) ? at<S>(ws, L.aux) : nullptr;
     a.st = at<DevStatus>(ws, L.status);
     if (F) {
+      StageScope sc(kStProject, st);
       mesh_to_splats<S><<<grid_for(F, 256), 256, 0, st>>>(a, make_cams<S>(cams, v0, nv));
       GMR_LAUNCHED();
     }
@@ -266,6 +314,7 @@ int blend_backward_launch(const Layout& L, void* ws, const GmrRaster* r, const v
   const size_t dyn = (size_t)8 * kBlendThreads * 8 * sizeof(S) + (kOpacity ? (size_t)8 * kBlendThreads * sizeof(S) : 0);
   GMR_CUDA(cudaFuncSetAttribute(blend_backward<S, kOpacity>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
   if (L.bins) {
+    StageScope sc(kStBlendBwd, st);
     blend_backward<S, kOpacity><<<(unsigned)L.bins, kBlendThreads, dyn, st>>>(a);
     GMR_LAUNCHED();
   }
@@ -294,11 +343,13 @@ int render_backward_t(const GmrMesh* m, const GmrCamera* cams, int B, const GmrR
     a.partial = at<S>(ws, L.partial);
     a.face_acc = at<S>(ws, L.face_acc);
     if (F) {
+      StageScope sc(kStFaceBwd, st);
       face_views_backward<S><<<grid_for(F, 128), 128, 0, st>>>(a, make_cams<S>(cams, v0, nv));
       GMR_LAUNCHED();
     }
   }
   if (F) {
+    StageScope sc(kStFaceBwd, st);
     face_convert_backward<S><<<grid_for(F, 128), 128, 0, st>>>((const S*)m->positions, m->faces, (int64_t)F,
                                                                r->rescale, at<S>(ws, L.face_acc),
                                                                at<S>(ws, L.corner));
@@ -307,6 +358,7 @@ int render_backward_t(const GmrMesh* m, const GmrCamera* cams, int B, const GmrR
   const uint32_t* vstart = (const uint32_t*)topo;
   const uint32_t* slots = vstart + align_up((V + 1) * 4) / 4;
   if (V) {
+    StageScope sc(kStVertex, st);
     vertex_gather<S><<<grid_for(V, 256), 256, 0, st>>>(vstart, slots, (int64_t)V, (int64_t)F,
                                                        at<S>(ws, L.corner), (S*)g_pos, (S*)g_col);
     GMR_LAUNCHED();
@@ -401,6 +453,32 @@ int convert_backward_t(const GmrMesh* m, int rescale, const void* gm, const void
 extern "C" {
 
 const char* gmr_last_error(void) { return g_err.c_str(); }
+
+void gmr_timing_enable(int32_t on) { g_timer.on = on != 0; }
+
+int64_t gmr_launch_count(void) { return g_launches; }
+
+int gmr_timing_read(double* ms, int64_t* launches, int32_t n, int32_t reset) {
+  for (int s = 0; s < kNumStages; ++s) {
+    for (auto& ev : g_timer.pending[s]) {
+      float t = 0.f;
+      GMR_CUDA(cudaEventSynchronize(ev.second));
+      GMR_CUDA(cudaEventElapsedTime(&t, ev.first, ev.second));
+      g_timer.ms[s] += t;
+      g_timer.calls[s] += 1;
+      cudaEventDestroy(ev.first);
+      cudaEventDestroy(ev.second);
+    }
+    g_timer.pending[s].clear();
+  }
+  for (int s = 0; s < n && s < kNumStages; ++s) {
+    if (ms) ms[s] = g_timer.ms[s];
+    if (launches) launches[s] = g_timer.calls[s];
+  }
+  if (reset)
+    for (int s = 0; s < kNumStages; ++s) g_timer.ms[s] = 0, g_timer.calls[s] = 0;
+  return kNumStages;
+}
 const char* gmr_version(void) { return "gmr-b200 0.1 (sm_100a)"; }
 
 int gmr_render_workspace_size(int64_t F, int32_t B, int32_t W, int32_t H, int64_t ecap, int32_t dtype,

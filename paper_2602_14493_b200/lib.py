@@ -23,6 +23,8 @@ GMR_ECAPACITY = -5
 GMR_F32 = 0
 GMR_F64 = 1
 FLAG_DEBUG_AUX = 1
+STAGES = ("convert_project", "depth_sort", "scan_emit", "tile_sort_ranges", "blend_forward",
+          "blend_backward", "face_backward", "vertex_gather")
 
 c_i32, c_i64, c_sz, c_vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t, ctypes.c_void_p
 
@@ -58,6 +60,9 @@ P = ctypes.POINTER
 _SIGNATURES = {
     "gmr_last_error": ([], ctypes.c_char_p),
     "gmr_version": ([], ctypes.c_char_p),
+    "gmr_timing_enable": ([c_i32], None),
+    "gmr_launch_count": ([], c_i64),
+    "gmr_timing_read": ([P(ctypes.c_double), P(c_i64), c_i32, c_i32], c_i32),
     "gmr_render_workspace_size": ([c_i64, c_i32, c_i32, c_i32, c_i64, c_i32, P(c_sz)], c_i32),
     "gmr_render_forward": ([P(GmrMesh), P(GmrCamera), c_i32, P(GmrRaster), c_vp, c_vp, c_vp,
                             c_sz, c_i64, c_vp], c_i32),
