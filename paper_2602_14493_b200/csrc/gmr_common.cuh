@@ -75,10 +75,8 @@ template <> struct alignas(16) V4<float> { float x, y, z, w; };
 template <> struct alignas(32) V4<double> { double x, y, z, w; };
 
 // Per-item screen-space record read by the blend kernels:
-//   a = (mean_x, mean_y, conic_a, conic_b), b = (conic_c, ext_x, ext_y, depth)
-// ext_* are the half-widths of the box that contains every pixel with
-// alpha >= 1/255 (padded; negative = never visible); used only to skip
-// (warp, splat) pairs, never to decide a pixel.
+//   a = (mean_x, mean_y, conic_a, conic_b), b = (conic_c, ext_x, ext_y, tau_cov)
+// (see screen_shape: the coverage bound, used only to skip pairs).
 template <typename S> struct Splat {
   V4<S> a, b;
 };
@@ -127,10 +125,16 @@ __device__ __forceinline__ void tile_rect(S mx, S my, S r, int tiles_x, int tile
 }
 
 // conic (render.py:76-81), 3-sigma radius (render.py:84-88,124) and the
-// alpha >= 1/255 extent box of a screen covariance (a, b, c) with opacity o.
+// coverage bound of a screen covariance (a, b, c) with opacity o:
+// alpha >= 1/255  <=>  o exp(-q/2) >= 1/255  <=>  q <= tau = 2 ln(255 o).
+// `tau_cov` is tau padded (relative and absolute) so that the per-row
+// coverage solve in the blend kernels is conservative; ext_* are the
+// half-widths of that ellipse's box (negative = never visible).  Neither
+// decides a pixel: they only let the kernels skip (pixel, splat) pairs
+// that cannot reach alpha >= 1/255.
 template <typename S>
 __device__ __forceinline__ void screen_shape(S a, S b, S c, S o, S& ca, S& cb, S& cc, S& radius,
-                                             S& ext_x, S& ext_y) {
+                                             S& ext_x, S& ext_y, S& tau_cov) {
   S det = sub_rn(mul_rn(a, c), mul_rn(b, b));
   ca = div_rn(c, det);
   cb = div_rn(-b, det);
@@ -138,14 +142,13 @@ __device__ __forceinline__ void screen_shape(S a, S b, S c, S o, S& ca, S& cb, S
   S half_sum = mul_rn(S(0.5), add_rn(a, c));
   S half_diff = mul_rn(S(0.5), sub_rn(a, c));
   radius = mul_rn(S(3), sqrt_s(add_rn(half_sum, hypot_s(half_diff, b))));
-  // o * exp(-q/2) >= 1/255  <=>  q <= 2 ln(255 o); box of that ellipse
   S tau = S(2) * log_s(S(255) * o);
-  if (!(tau > S(0))) {
-    ext_x = ext_y = S(-1);
+  if (!(tau > S(-1e-3))) {
+    ext_x = ext_y = tau_cov = S(-1);
   } else {
-    tau = tau * S(1.002) + S(1e-3);
-    ext_x = sqrt_s(tau * a) * S(1.001) + S(0.01);
-    ext_y = sqrt_s(tau * c) * S(1.001) + S(0.01);
+    tau_cov = fmax(tau, S(0)) * S(1.004) + S(2e-3);
+    ext_x = sqrt_s(tau_cov * a) * S(1.001) + S(0.02);
+    ext_y = sqrt_s(tau_cov * c) * S(1.001) + S(0.02);
   }
 }
 

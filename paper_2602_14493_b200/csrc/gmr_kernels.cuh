@@ -207,12 +207,12 @@ __global__ void __launch_bounds__(256) mesh_to_splats(MeshFwdArgs<S> p, const __
         c = add_rn(c, Const<S>::dilation());
         const S mx = add_rn(div_rn(mul_rn(cam.fx, t[0]), t[2]), cam.cx);
         const S my = add_rn(div_rn(mul_rn(cam.fy, t[1]), t[2]), cam.cy);
-        S ca, cb, cc, r, ex, ey;
-        screen_shape(a, b, c, S(1), ca, cb, cc, r, ex, ey);
+        S ca, cb, cc, r, ex, ey, tc;
+        screen_shape(a, b, c, S(1), ca, cb, cc, r, ex, ey, tc);
         const bool on = add_rn(mx, r) >= S(-0.5) && sub_rn(mx, r) <= S(p.W) - S(0.5) &&
                         add_rn(my, r) >= S(-0.5) && sub_rn(my, r) <= S(p.H) - S(0.5);
         rec.a.x = mx; rec.a.y = my; rec.a.z = ca; rec.a.w = cb;
-        rec.b.x = cc; rec.b.y = ex; rec.b.z = ey; rec.b.w = r;
+        rec.b.x = cc; rec.b.y = ex; rec.b.z = ey; rec.b.w = tc;
         if (p.aux) {
           p.aux[2 * item] = r;
           p.aux[2 * item + 1] = t[2];
@@ -279,11 +279,11 @@ __global__ void __launch_bounds__(256) pack_splats(PackArgs<S> p) {
   const S o = p.opacity[i], d = p.depth[i];
   V4<S> col;
   col.x = p.color[3 * i]; col.y = p.color[3 * i + 1]; col.z = p.color[3 * i + 2]; col.w = o;
-  S ca, cb, cc, r, ex, ey;
-  screen_shape(a, b, c, o, ca, cb, cc, r, ex, ey);
+  S ca, cb, cc, r, ex, ey, tc;
+  screen_shape(a, b, c, o, ca, cb, cc, r, ex, ey, tc);
   Splat<S> rec;
   rec.a.x = mx; rec.a.y = my; rec.a.z = ca; rec.a.w = cb;
-  rec.b.x = cc; rec.b.y = ex; rec.b.z = ey; rec.b.w = r;
+  rec.b.x = cc; rec.b.y = ex; rec.b.z = ey; rec.b.w = tc;
   const uint32_t item = (uint32_t)i;
   if (!(finite_s(mx) && finite_s(my))) flag_bad(p.st, 0, item);
   if (!(finite_s(a) && finite_s(b) && finite_s(c) && finite_s(p.cov2d[4 * i + 2]))) flag_bad(p.st, 1, item);
@@ -416,7 +416,16 @@ __global__ void __launch_bounds__(256) tile_ranges(const uint32_t* __restrict__ 
 }
 
 // ---------------------------------------------------------------------------
-// K3 / K4: per-tile blending
+// K3 / K4: per-tile blending over exact per-pixel coverage lists
+//
+// One CTA per (view, 16x16 tile); warp w owns tile rows 2w, 2w+1 and lane l
+// the pixel (x = l & 15, y = 2w + (l >> 4)), i.e. tile bit 32w + l.  Entries
+// are staged in shared memory in batches.  For each entry the loading
+// thread solves, row by row, the (padded) ellipse alpha >= 1/255 and writes a
+// 256-bit coverage mask of the tile.  A 32x32 bit transpose per warp turns
+// 32 entry masks into, per lane, the bits of the entries covering its pixel,
+// so every lane walks only its own pixel's candidates in front-to-back order
+// (the exact per-pixel decisions of render.py:251-267 then run unchanged).
 // ---------------------------------------------------------------------------
 
 template <typename S> struct BlendArgs {
@@ -442,79 +451,102 @@ template <typename S> struct BlendArgs {
   S* partial_op;     // [E] (splat path only) or null
 };
 
-template <typename S> struct BlendSmem {
-  V4<S> geo[kBlendThreads];   // mx, my, ca, cb
-  V4<S> geo2[kBlendThreads];  // cc, opacity, -, -
-  V4<S> col[kBlendThreads];   // r, g, b, -
-  uint16_t list[8][kBlendThreads];
-  uint8_t mask[kBlendThreads];
-};
+// lane r holds row r of a 32x32 bit matrix (bit c = M[r][c]); returns column
+// `lane` (bit r = M[r][lane]).  5 shuffle stages.
+__device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
+#pragma unroll
+  for (int j = 16; j > 0; j >>= 1) {
+    const uint32_t lo = j == 16 ? 0x0000FFFFu : j == 8 ? 0x00FF00FFu : j == 4 ? 0x0F0F0F0Fu
+                      : j == 2 ? 0x33333333u : 0x55555555u;
+    const uint32_t y = __shfl_xor_sync(0xffffffffu, x, j);
+    x = (lane & j) ? ((x & ~lo) | ((y & ~lo) >> j)) : ((x & lo) | ((y & lo) << j));
+  }
+  return x;
+}
 
-// Load one batch of entries into shared memory; per entry, the 8-bit mask
-// of warp sub-rectangles (8x4 px) its alpha >= 1/255 box touches.
+// Coverage of one splat in the tile with pixel origin (x0, y0): bit
+// (2r + (row & 1)) ... as tile bit index y*16 + x, packed in 8 words.
 template <typename S>
-__device__ __forceinline__ void blend_load(const BlendArgs<S>& p, BlendSmem<S>& sm, uint32_t base,
-                                           int n, uint32_t vbase_item, int tile_x0, int tile_y0,
-                                           uint32_t& my_item) {
-  const int i = threadIdx.x;
-  if (i < n) {
-    const uint32_t item = p.entry_item[base + i];
-    my_item = item;
-    const Splat<S> s = p.splat[item];
-    const V4<S> c = p.col4[item - vbase_item];
-    V4<S> g2;
-    g2.x = s.b.x; g2.y = c.w; g2.z = S(0); g2.w = S(0);
-    sm.geo[i] = s.a;
-    sm.geo2[i] = g2;
-    sm.col[i] = c;
-    uint32_t m = 0;
-    const S ex = s.b.y, ey = s.b.z;
-    if (ex >= S(0)) {
-      const S x0 = s.a.x - ex, x1 = s.a.x + ex, y0 = s.a.y - ey, y1 = s.a.y + ey;
-      uint32_t cols = 0, rows = 0;
+__device__ __forceinline__ void tile_coverage(const V4<S>& a, const V4<S>& b, int x0, int y0, uint32_t w[8]) {
 #pragma unroll
-      for (int cx = 0; cx < 2; ++cx) {
-        const S wx0 = S(tile_x0 + cx * 8), wx1 = wx0 + S(7);
-        if (x1 >= wx0 && x0 <= wx1) cols |= 1u << cx;
-      }
-#pragma unroll
-      for (int ry = 0; ry < 4; ++ry) {
-        const S wy0 = S(tile_y0 + ry * 4), wy1 = wy0 + S(3);
-        if (y1 >= wy0 && y0 <= wy1) rows |= 1u << ry;
-      }
-#pragma unroll
-      for (int w = 0; w < 8; ++w)
-        if (((cols >> (w & 1)) & 1u) && ((rows >> (w >> 1)) & 1u)) m |= 1u << w;
-    }
-    sm.mask[i] = (uint8_t)m;
+  for (int i = 0; i < 8; ++i) w[i] = 0;
+  const S mx = a.x, my = a.y, ca = a.z, cb = a.w, cc = b.x, ex = b.y, ey = b.z, tau = b.w;
+  if (!(ex >= S(0)) || !(ca > S(0))) return;
+  const S ylo = ceil(my - ey), yhi = floor(my + ey);
+  const int r0 = (int)fmax(S(0), ylo - S(y0)), r1 = (int)fmin(S(15), yhi - S(y0));
+  const S xlo_t = S(x0), xhi_t = S(x0 + 15);
+  const S neg_det = cb * cb - ca * cc;   // b^2 - ac < 0 for a positive definite conic
+  const S inv_a = S(1) / ca;
+  for (int r = r0; r <= r1; ++r) {
+    const S dy = S(y0 + r) - my;
+    const S disc = dy * dy * neg_det + ca * tau;
+    if (!(disc >= S(0))) continue;
+    const S hw = sqrt_s(disc) * inv_a * S(1.0005) + S(0.01);
+    const S xc = mx - cb * dy * inv_a;
+    const S lo = fmax(ceil(xc - hw), xlo_t), hi = fmin(floor(xc + hw), xhi_t);
+    if (lo > hi) continue;
+    const int ilo = (int)lo - x0, ihi = (int)hi - x0;
+    const uint32_t bits = ((0xffffu >> (15 - (ihi - ilo))) << ilo) & 0xffffu;
+    w[r >> 1] |= bits << ((r & 1) * 16);
   }
 }
 
-// compact the batch entries whose mask has this warp's bit, in order
+// alpha of a splat at a pixel (render.py:251-256); `ep` = exp(power)
 template <typename S>
-__device__ __forceinline__ int blend_warp_list(BlendSmem<S>& sm, int n, int warp, int lane) {
-  int cnt = 0;
+__device__ __forceinline__ S splat_alpha(S fpx, S fpy, const V4<S>& g, S cc, S o, S& dx, S& dy, S& ep, S& raw) {
+  dx = sub_rn(fpx, g.x);
+  dy = sub_rn(fpy, g.y);
+  const S q = add_rn(mul_rn(mul_rn(g.z, dx), dx), mul_rn(mul_rn(cc, dy), dy));
+  const S power = sub_rn(mul_rn(S(-0.5), q), mul_rn(mul_rn(g.w, dx), dy));
+  ep = exp_s(power);
+  raw = mul_rn(o, ep);
+  return raw < Const<S>::alpha_clamp() ? raw : Const<S>::alpha_clamp();
+}
+
+constexpr int kFwdBatch = 256;
+constexpr int kBwdBatch = 128;
+constexpr int kBwdSlots = 16;
+
+template <typename S, int NB> struct StageSmem {
+  V4<S> geo[NB];          // mx, my, ca, cb
+  V4<S> col[NB];          // r, g, b, opacity
+  S cc[NB];
+  uint32_t cov[NB][9];    // 8 coverage words (+1 pad: conflict-free transposes)
+};
+
+// Stage one batch: thread i < n loads entry base+i (i >= n: empty mask).
+template <typename S, int NB>
+__device__ __forceinline__ void stage_batch(const BlendArgs<S>& p, StageSmem<S, NB>& sm, uint32_t base, int n,
+                                            uint32_t vbase_item, int x0, int y0, uint32_t& my_item) {
+  for (int i = threadIdx.x; i < NB; i += kBlendThreads) {
+    uint32_t w[8];
+    if (i < n) {
+      const uint32_t item = p.entry_item[base + i];
+      if (i == (int)threadIdx.x) my_item = item;
+      const Splat<S> s = p.splat[item];
+      const V4<S> c = p.col4[item - vbase_item];
+      sm.geo[i] = s.a;
+      sm.col[i] = c;
+      sm.cc[i] = s.b.x;
+      tile_coverage(s.a, s.b, x0, y0, w);
+    } else {
 #pragma unroll
-  for (int c = 0; c < kBlendThreads / 32; ++c) {
-    const int j = c * 32 + lane;
-    const bool hit = j < n && ((sm.mask[j] >> warp) & 1u);
-    const unsigned b = __ballot_sync(0xffffffffu, hit);
-    if (hit) sm.list[warp][cnt + __popc(b & lanemask_lt())] = (uint16_t)j;
-    cnt += __popc(b);
+      for (int q = 0; q < 8; ++q) w[q] = 0;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) sm.cov[i][q] = w[q];
   }
-  __syncwarp();
-  return cnt;
 }
 
 template <typename S>
 __global__ void __launch_bounds__(kBlendThreads) blend_forward(BlendArgs<S> p) {
-  __shared__ BlendSmem<S> sm;
+  __shared__ StageSmem<S, kFwdBatch> sm;
   const uint32_t g = blockIdx.x;
   const uint32_t view = g / p.tiles_per_view, t = g % p.tiles_per_view;
   const int tx = (int)(t % (uint32_t)p.tiles_x), ty = (int)(t / (uint32_t)p.tiles_x);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int px = tx * kTile + (warp & 1) * 8 + (lane & 7);
-  const int py = ty * kTile + (warp >> 1) * 4 + (lane >> 3);
+  const int x0 = tx * kTile, y0 = ty * kTile;
+  const int px = x0 + (lane & 15), py = y0 + 2 * warp + (lane >> 4);
   const bool inside = px < p.W && py < p.H;
   const S fpx = S(px), fpy = S(py);
   const S one = S(1);
@@ -522,34 +554,33 @@ __global__ void __launch_bounds__(kBlendThreads) blend_forward(BlendArgs<S> p) {
   bool done = !inside;
   const uint32_t start = p.bounds[g], end = p.bounds[g + 1];
   const uint32_t vbase_item = view * p.items_per_view;
-  for (uint32_t base = start; base < end; base += kBlendThreads) {
+  for (uint32_t base = start; base < end; base += kFwdBatch) {
     if (__syncthreads_count(done) == kBlendThreads) break;
-    const int n = (int)min((uint32_t)kBlendThreads, end - base);
+    const int n = (int)min((uint32_t)kFwdBatch, end - base);
     uint32_t my_item;
-    blend_load(p, sm, base, n, vbase_item, tx * kTile, ty * kTile, my_item);
+    stage_batch<S, kFwdBatch>(p, sm, base, n, vbase_item, x0, y0, my_item);
     __syncthreads();
-    const int cnt = blend_warp_list(sm, n, warp, lane);
-    for (int k = 0; k < cnt; ++k) {
+    for (int c = 0; c < (n + 31) / 32; ++c) {
       if (__all_sync(0xffffffffu, done)) break;
-      const int j = sm.list[warp][k];
-      if (!done) {
+      uint32_t bits = transpose32(sm.cov[c * 32 + lane][warp], lane);
+      if (done) bits = 0;
+      while (bits) {
+        const int j = c * 32 + (__ffs(bits) - 1);
+        bits &= bits - 1;
         const V4<S> ge = sm.geo[j];
-        const V4<S> g2 = sm.geo2[j];
-        const S dx = sub_rn(fpx, ge.x), dy = sub_rn(fpy, ge.y);
-        const S q = add_rn(mul_rn(mul_rn(ge.z, dx), dx), mul_rn(mul_rn(g2.x, dy), dy));
-        const S power = sub_rn(mul_rn(S(-0.5), q), mul_rn(mul_rn(ge.w, dx), dy));
-        const S raw = mul_rn(g2.y, exp_s(power));
-        const S a = raw < Const<S>::alpha_clamp() ? raw : Const<S>::alpha_clamp();
+        const V4<S> co = sm.col[j];
+        S dx, dy, ep, raw;
+        const S a = splat_alpha(fpx, fpy, ge, sm.cc[j], co.w, dx, dy, ep, raw);
         if (a >= Const<S>::contrib_floor()) {
           const S test = mul_rn(T, sub_rn(one, a));
           if (test < Const<S>::t_stop()) {
             done = true;
+            bits = 0;
           } else {
-            const V4<S> c = sm.col[j];
             const S w = mul_rn(a, T);
-            ar += w * c.x;
-            ag += w * c.y;
-            ab += w * c.z;
+            ar += w * co.x;
+            ag += w * co.y;
+            ab += w * co.z;
             T = test;
           }
         }
@@ -567,164 +598,180 @@ __global__ void __launch_bounds__(kBlendThreads) blend_forward(BlendArgs<S> p) {
   }
 }
 
-// Butterfly-transpose reduction of 8 per-lane values over the warp:
-// 9 shuffles.  Returns, in every lane, the total of value index
-// ((lane>>4)&1)*4 + ((lane>>3)&1)*2 + ((lane>>2)&1).
-template <typename S>
-__device__ __forceinline__ S warp_reduce8(const S v[8], int lane) {
-  S a[4], c[2];
-  const bool h4 = lane & 16, h3 = lane & 8, h2 = lane & 4;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const S send = h4 ? v[i] : v[i + 4];
-    const S keep = h4 ? v[i + 4] : v[i];
-    a[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-  }
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const S send = h3 ? a[i] : a[i + 2];
-    const S keep = h3 ? a[i + 2] : a[i];
-    c[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-  }
-  const S send = h2 ? c[0] : c[1];
-  const S keep = h2 ? c[1] : c[0];
-  S d = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-  d += __shfl_xor_sync(0xffffffffu, d, 2);
-  d += __shfl_xor_sync(0xffffffffu, d, 1);
-  return d;
-}
+template <typename S> struct V2 { S x, y; };
 
-template <typename S>
-__device__ __forceinline__ S warp_sum(S v) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
+template <typename S> struct BwdSmem {
+  StageSmem<S, kBwdBatch> st;
+  uint32_t inc[kBwdBatch / 32][kBlendThreads];      // per pixel: included entries of this round
+  V4<S> pix[kBlendThreads];                          // per pixel: g_r, g_g, g_b, (g.bg - g_a) T_final
+  V2<S> slot[kBwdSlots][kBlendThreads];              // per pixel and included pair: (T_before, suffix)
+};
 
-// Front-to-back re-scan (same decisions as K3).  With C = g.(rgb - T_f bg)
-// = sum_j (g.c_j) w_j, the suffix S_k = C - sum_{j<=k} (g.c_j) w_j, so
-//   dL/dalpha_k = (g.c_k) T_k - (S_k + (g.bg - g_a) T_f) / (1 - alpha_k)
-// (render.py:327-334).  Per (warp, entry) the 8 sums
-//   [sum dp dx, dp dy, dp dx^2, dp dx dy, dp dy^2, w g_r, w g_g, w g_b]
-// are reduced in fixed order; warps are summed in warp order; each entry's
-// sums land in its pre-sort slot, so accumulation is deterministic.
+// Backward (render.py:294-361).  Per batch:
+//  pass 1 (lane = pixel): front-to-back re-scan with the forward's exact
+//    decisions; each included pair records (T_k, S_k) where
+//    S_k = C - sum_{j<=k} (g.c_j) w_j and C = g.(rgb - T_f bg) = sum_j (g.c_j) w_j;
+//  pass 2 (thread pair = entry, one half of the tile each): over the entry's
+//    covered pixels in row-major order,
+//      dL/dalpha = (g.c) T_k - (S_k + (g.bg - g_a) T_f) / (1 - alpha)
+//    -> sums [dp dx, dp dy, dp dx^2, dp dx dy, dp dy^2, w g_r, w g_g, w g_b]
+//    (dp = dL/dalpha * alpha where raw < 0.99, clamp gate :336-338).
+//  Fixed iteration orders and no atomics: the result is deterministic.
+//  If a pixel has more than kBwdSlots included pairs in a batch, the batch
+//  runs in several rounds.
 template <typename S, bool kOpacity>
 __global__ void __launch_bounds__(kBlendThreads) blend_backward(BlendArgs<S> p) {
-  __shared__ BlendSmem<S> sm;
-  extern __shared__ __align__(16) unsigned char dyn[];
-  S* part = reinterpret_cast<S*>(dyn);                       // [8 warps][256][8]
-  S* part_op = part + 8 * kBlendThreads * 8;                  // [8][256] (kOpacity)
+  extern __shared__ __align__(32) unsigned char dyn[];
+  BwdSmem<S>& sm = *reinterpret_cast<BwdSmem<S>*>(dyn);
   const uint32_t g = blockIdx.x;
   const uint32_t view = g / p.tiles_per_view, t = g % p.tiles_per_view;
   const int tx = (int)(t % (uint32_t)p.tiles_x), ty = (int)(t / (uint32_t)p.tiles_x);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int px = tx * kTile + (warp & 1) * 8 + (lane & 7);
-  const int py = ty * kTile + (warp >> 1) * 4 + (lane >> 3);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int x0 = tx * kTile, y0 = ty * kTile;
+  const int px = x0 + (lane & 15), py = y0 + 2 * warp + (lane >> 4);
   const bool inside = px < p.W && py < p.H;
   const S fpx = S(px), fpy = S(py);
   const S one = S(1);
-  S gr = 0, gg = 0, gb = 0, Ctot = 0, bterm = 0;
-  if (inside) {
-    const size_t pix = ((size_t)view * p.H + py) * p.W + px;
-    gr = p.g_rgb[3 * pix]; gg = p.g_rgb[3 * pix + 1]; gb = p.g_rgb[3 * pix + 2];
-    const S ga = p.g_alpha[pix];
-    const S tf = p.t_final[pix];
-    const S gbg = gr * p.bg0 + gg * p.bg1 + gb * p.bg2;
-    Ctot = gr * p.rgb[3 * pix] + gg * p.rgb[3 * pix + 1] + gb * p.rgb[3 * pix + 2] - gbg * tf;
-    bterm = (gbg - ga) * tf;
+  S Ctot = 0;
+  {
+    V4<S> pd;
+    pd.x = pd.y = pd.z = pd.w = S(0);
+    if (inside) {
+      const size_t pix = ((size_t)view * p.H + py) * p.W + px;
+      pd.x = p.g_rgb[3 * pix]; pd.y = p.g_rgb[3 * pix + 1]; pd.z = p.g_rgb[3 * pix + 2];
+      const S tf = p.t_final[pix];
+      const S gbg = pd.x * p.bg0 + pd.y * p.bg1 + pd.z * p.bg2;
+      Ctot = pd.x * p.rgb[3 * pix] + pd.y * p.rgb[3 * pix + 1] + pd.z * p.rgb[3 * pix + 2] - gbg * tf;
+      pd.w = (gbg - p.g_alpha[pix]) * tf;
+    }
+    sm.pix[tid] = pd;
   }
+  const V4<S> mypix = sm.pix[tid];
   S T = one, P = 0;
   bool done = !inside;
   const uint32_t start = p.bounds[g], end = p.bounds[g + 1];
   const uint32_t vbase_item = view * p.items_per_view;
-  const int holder = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+  // pass-2 role: entry je, rows [8h, 8h + 8) of the tile
+  const int je = tid >> 1, half = tid & 1;
   uint32_t base = start;
-  for (; base < end; base += kBlendThreads) {
-    const bool all_done = __syncthreads_count(done) == kBlendThreads;
-    const int n = (int)min((uint32_t)kBlendThreads, end - base);
+  for (; base < end; base += kBwdBatch) {
+    if (__syncthreads_count(done) == kBlendThreads) break;
+    const int n = (int)min((uint32_t)kBwdBatch, end - base);
     uint32_t my_item = 0;
-    if (all_done) break;
-    blend_load(p, sm, base, n, vbase_item, tx * kTile, ty * kTile, my_item);
+    stage_batch<S, kBwdBatch>(p, sm.st, base, n, vbase_item, x0, y0, my_item);
     __syncthreads();
-    const int cnt = blend_warp_list(sm, n, warp, lane);
-    int k = 0;
-    for (; k < cnt; ++k) {
-      if (__all_sync(0xffffffffu, done)) break;
-      const int j = sm.list[warp][k];
-      S v[8];
+    uint32_t cw[kBwdBatch / 32];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) v[q] = S(0);
-      S vop = S(0);
-      if (!done) {
-        const V4<S> ge = sm.geo[j];
-        const V4<S> g2 = sm.geo2[j];
-        const S dx = sub_rn(fpx, ge.x), dy = sub_rn(fpy, ge.y);
-        const S q = add_rn(mul_rn(mul_rn(ge.z, dx), dx), mul_rn(mul_rn(g2.x, dy), dy));
-        const S power = sub_rn(mul_rn(S(-0.5), q), mul_rn(mul_rn(ge.w, dx), dy));
-        const S ep = exp_s(power);
-        const S raw = mul_rn(g2.y, ep);
-        const S a = raw < Const<S>::alpha_clamp() ? raw : Const<S>::alpha_clamp();
-        if (a >= Const<S>::contrib_floor()) {
-          const S om = sub_rn(one, a);
-          const S test = mul_rn(T, om);
-          if (test < Const<S>::t_stop()) {
-            done = true;
-          } else {
-            const V4<S> c = sm.col[j];
-            const S w = mul_rn(a, T);
-            const S gdc = gr * c.x + gg * c.y + gb * c.z;
-            P += gdc * w;
-            const S suffix = Ctot - P;
-            const S d_alpha = gdc * T - (suffix + bterm) / om;
-            if (raw < Const<S>::alpha_clamp()) {
-              const S dp = d_alpha * a;
-              v[0] = dp * dx;
-              v[1] = dp * dy;
-              v[2] = v[0] * dx;
-              v[3] = v[0] * dy;
-              v[4] = v[1] * dy;
-              vop = d_alpha * ep;
+    for (int c = 0; c < kBwdBatch / 32; ++c) {
+      cw[c] = transpose32(sm.st.cov[c * 32 + lane][warp], lane);
+      if (done) cw[c] = 0;
+    }
+    // pass-2 entry parameters (registers across rounds)
+    V4<S> ge, co;
+    S ecc = S(0);
+    if (je < n) {
+      ge = sm.st.geo[je];
+      co = sm.st.col[je];
+      ecc = sm.st.cc[je];
+    }
+    S acc[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = S(0);
+    S aop = S(0);
+    for (;;) {
+      // ---- pass 1: my pixel ----
+      int cnt = 0;
+      uint32_t inc[kBwdBatch / 32];
+#pragma unroll
+      for (int c = 0; c < kBwdBatch / 32; ++c) {
+        inc[c] = 0;
+        while (cw[c] && cnt < kBwdSlots) {
+          const int k = __ffs(cw[c]) - 1;
+          cw[c] &= cw[c] - 1;
+          const int j = c * 32 + k;
+          const V4<S> g1 = sm.st.geo[j];
+          const V4<S> c1 = sm.st.col[j];
+          S dx, dy, ep, raw;
+          const S a = splat_alpha(fpx, fpy, g1, sm.st.cc[j], c1.w, dx, dy, ep, raw);
+          if (a >= Const<S>::contrib_floor()) {
+            const S om = sub_rn(one, a);
+            const S test = mul_rn(T, om);
+            if (test < Const<S>::t_stop()) {
+              done = true;
+#pragma unroll
+              for (int q = 0; q < kBwdBatch / 32; ++q) cw[q] = 0;
+            } else {
+              const S w = mul_rn(a, T);
+              P += (mypix.x * c1.x + mypix.y * c1.y + mypix.z * c1.z) * w;
+              V2<S> rec;
+              rec.x = T;
+              rec.y = Ctot - P;
+              sm.slot[cnt][tid] = rec;
+              inc[c] |= 1u << k;
+              ++cnt;
+              T = test;
             }
-            v[5] = w * gr;
-            v[6] = w * gg;
-            v[7] = w * gb;
-            T = test;
           }
         }
       }
-      const S r = warp_reduce8(v, lane);
-      if ((lane & 3) == 0) part[((size_t)warp * kBlendThreads + j) * 8 + holder] = r;
-      if (kOpacity) {
-        const S ro = warp_sum(vop);
-        if (lane == 0) part_op[warp * kBlendThreads + j] = ro;
+      bool left = false;
+#pragma unroll
+      for (int c = 0; c < kBwdBatch / 32; ++c) {
+        sm.inc[c][tid] = inc[c];
+        left |= cw[c] != 0;
       }
-    }
-    // entries this warp skipped after finishing contribute zero
-    for (int kk = k + lane; kk < cnt; kk += 32) {
-      const int j = sm.list[warp][kk];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) part[((size_t)warp * kBlendThreads + j) * 8 + q] = S(0);
-      if (kOpacity) part_op[warp * kBlendThreads + j] = S(0);
-    }
-    __syncthreads();
-    // per entry: sum over the warps in its mask, in warp order
-    if ((int)threadIdx.x < n) {
-      const int j = threadIdx.x;
-      const uint32_t m = sm.mask[j];
-      S acc[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) acc[q] = S(0);
-      S aop = S(0);
-      for (int w = 0; w < 8; ++w) {
-        if (!((m >> w) & 1u)) continue;
-        const S* src = part + ((size_t)w * kBlendThreads + j) * 8;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) acc[q] += src[q];
-        if (kOpacity) aop += part_op[w * kBlendThreads + j];
+      const bool more = __syncthreads_or(left);
+      // ---- pass 2: my entry over its covered pixels in my half ----
+      if (je < n) {
+        const int cj = je >> 5, kj = je & 31;
+        const uint32_t below = (1u << kj) - 1u;
+#pragma unroll 1
+        for (int wi = 4 * half; wi < 4 * half + 4; ++wi) {
+          uint32_t bits = sm.st.cov[je][wi];
+          while (bits) {
+            const int b = __ffs(bits) - 1;
+            bits &= bits - 1;
+            const int q = wi * 32 + b;   // tile pixel; its lane/thread index is q
+            const uint32_t iw = sm.inc[cj][q];
+            if (!((iw >> kj) & 1u)) continue;
+            int idx = __popc(iw & below);
+            for (int c = 0; c < cj; ++c) idx += __popc(sm.inc[c][q]);
+            const V2<S> rec = sm.slot[idx][q];
+            const V4<S> pd = sm.pix[q];
+            const S qx = S(x0 + (q & 15)), qy = S(y0 + (q >> 4));
+            S dx, dy, ep, raw;
+            const S a = splat_alpha(qx, qy, ge, ecc, co.w, dx, dy, ep, raw);
+            const S gdc = pd.x * co.x + pd.y * co.y + pd.z * co.z;
+            const S w = a * rec.x;
+            const S d_alpha = gdc * rec.x - (rec.y + pd.w) / sub_rn(one, a);
+            if (raw < Const<S>::alpha_clamp()) {
+              const S dp = d_alpha * a;
+              const S dpx = dp * dx, dpy = dp * dy;
+              acc[0] += dpx;
+              acc[1] += dpy;
+              acc[2] += dpx * dx;
+              acc[3] += dpx * dy;
+              acc[4] += dpy * dy;
+              if (kOpacity) aop += d_alpha * ep;
+            }
+            acc[5] += w * pd.x;
+            acc[6] += w * pd.y;
+            acc[7] += w * pd.z;
+          }
+        }
       }
-      const uint2 rc = p.rect[my_item];
+      __syncthreads();
+      if (!more) break;
+    }
+    // combine the two halves (fixed order) and store at the pre-sort slot
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], 1);
+    if (kOpacity) aop += __shfl_xor_sync(0xffffffffu, aop, 1);
+    const uint32_t item_j = (je < n) ? p.entry_item[base + je] : 0u;
+    if (half == 0 && je < n) {
+      const uint2 rc = p.rect[item_j];
       const int tx0 = rc.x & 0xffff, ty0 = rc.x >> 16, tx1 = rc.y & 0xffff;
-      const uint32_t slot = p.entry_off[my_item] + (uint32_t)((ty - ty0) * (tx1 - tx0 + 1) + (tx - tx0));
+      const uint32_t slot = p.entry_off[item_j] + (uint32_t)((ty - ty0) * (tx1 - tx0 + 1) + (tx - tx0));
       V4<S>* dst = reinterpret_cast<V4<S>*>(p.partial + (size_t)slot * 8);
       V4<S> lo, hi;
       lo.x = acc[0]; lo.y = acc[1]; lo.z = acc[2]; lo.w = acc[3];
@@ -733,7 +780,6 @@ __global__ void __launch_bounds__(kBlendThreads) blend_backward(BlendArgs<S> p) 
       dst[1] = hi;
       if (kOpacity) p.partial_op[slot] = aop;
     }
-    __syncthreads();
   }
   // the tile finished early: entries never loaded still own a partial slot,
   // which must hold zeros (every slot is written exactly once)
