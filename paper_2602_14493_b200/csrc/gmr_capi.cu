@@ -311,7 +311,7 @@ int blend_backward_launch(const Layout& L, void* ws, const GmrRaster* r, const v
   a.g_alpha = (const S*)g_alpha;
   a.partial = at<S>(ws, L.partial);
   a.partial_op = kOpacity ? at<S>(ws, L.partial_op) : nullptr;
-  const size_t dyn = sizeof(BwdSmem<S>);
+  const size_t dyn = sizeof(BwdSmem<S, kOpacity>);
   GMR_CUDA(cudaFuncSetAttribute(blend_backward<S, kOpacity>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
   if (L.bins) {
     StageScope sc(kStBlendBwd, st);

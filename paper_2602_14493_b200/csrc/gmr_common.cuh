@@ -71,6 +71,9 @@ template <> struct KeyOf<float> { typedef uint32_t type; };
 template <> struct KeyOf<double> { typedef unsigned long long type; };
 
 template <typename S> struct V4 { S x, y, z, w; };
+template <typename S> struct V2 { S x, y; };
+template <> struct alignas(8) V2<float> { float x, y; };
+template <> struct alignas(16) V2<double> { double x, y; };
 template <> struct alignas(16) V4<float> { float x, y, z, w; };
 template <> struct alignas(32) V4<double> { double x, y, z, w; };
 

@@ -464,8 +464,8 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
   return x;
 }
 
-// Coverage of one splat in the tile with pixel origin (x0, y0): bit
-// (2r + (row & 1)) ... as tile bit index y*16 + x, packed in 8 words.
+// Coverage of one splat in the tile with pixel origin (x0, y0): tile bit
+// y*16 + x, packed in 8 words (word w = rows 2w, 2w+1).
 template <typename S>
 __device__ __forceinline__ void tile_coverage(const V4<S>& a, const V4<S>& b, int x0, int y0, uint32_t w[8]) {
 #pragma unroll
@@ -491,43 +491,73 @@ __device__ __forceinline__ void tile_coverage(const V4<S>& a, const V4<S>& b, in
   }
 }
 
-// alpha of a splat at a pixel (render.py:251-256); `ep` = exp(power)
-template <typename S>
-__device__ __forceinline__ S splat_alpha(S fpx, S fpy, const V4<S>& g, S cc, S o, S& dx, S& dy, S& ep, S& raw) {
-  dx = sub_rn(fpx, g.x);
-  dy = sub_rn(fpy, g.y);
-  const S q = add_rn(mul_rn(mul_rn(g.z, dx), dx), mul_rn(mul_rn(cc, dy), dy));
-  const S power = sub_rn(mul_rn(S(-0.5), q), mul_rn(mul_rn(g.w, dx), dy));
-  ep = exp_s(power);
-  raw = mul_rn(o, ep);
-  return raw < Const<S>::alpha_clamp() ? raw : Const<S>::alpha_clamp();
-}
+// Per-pixel alpha of a staged splat (render.py:251-256).  `q` holds the
+// splat's conic in the form the evaluator wants (Eval<S>::prep).
+//  double (parity path): the reference's expression and exp(), with each
+//    operation rounded as numpy rounds it;
+//  float (fast path): power * log2(e) as dx (A dx + B dy) + C dy^2 with the
+//    coefficients folded at staging time, then ex2.approx.
+template <typename S> struct Eval;
+template <> struct Eval<double> {
+  static __device__ __forceinline__ V4<double> prep(double ca, double cb, double cc, double o) {
+    V4<double> q;
+    q.x = ca; q.y = cb; q.z = cc; q.w = o;
+    return q;
+  }
+  static __device__ __forceinline__ double alpha(double dx, double dy, const V4<double>& q, double& ep,
+                                                 double& raw) {
+    const double qq = add_rn(mul_rn(mul_rn(q.x, dx), dx), mul_rn(mul_rn(q.z, dy), dy));
+    const double power = sub_rn(mul_rn(-0.5, qq), mul_rn(mul_rn(q.y, dx), dy));
+    ep = exp(power);
+    raw = mul_rn(q.w, ep);
+    return raw < 0.99 ? raw : 0.99;
+  }
+};
+template <> struct Eval<float> {
+  static __device__ __forceinline__ V4<float> prep(float ca, float cb, float cc, float o) {
+    const float l2e = 1.4426950408889634f;
+    V4<float> q;
+    q.x = -0.5f * l2e * ca; q.y = -l2e * cb; q.z = -0.5f * l2e * cc; q.w = o;
+    return q;
+  }
+  static __device__ __forceinline__ float alpha(float dx, float dy, const V4<float>& q, float& ep, float& raw) {
+    const float p2 = __fmaf_rn(dx, __fmaf_rn(q.x, dx, __fmul_rn(q.y, dy)), __fmul_rn(__fmul_rn(q.z, dy), dy));
+    float e;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(p2));
+    ep = e;
+    raw = __fmul_rn(q.w, e);
+    return raw < 0.99f ? raw : 0.99f;
+  }
+};
 
 constexpr int kFwdBatch = 256;
 constexpr int kBwdBatch = 128;
 constexpr int kBwdSlots = 16;
 
 template <typename S, int NB> struct StageSmem {
-  V4<S> geo[NB];          // mx, my, ca, cb
-  V4<S> col[NB];          // r, g, b, opacity
-  S cc[NB];
+  V2<S> mean[NB];         // mx, my
+  V4<S> q[NB];            // evaluator coefficients + opacity
+  V4<S> col[NB];          // r, g, b, -
   uint32_t cov[NB][9];    // 8 coverage words (+1 pad: conflict-free transposes)
+  uint32_t tw[NB / 32][kBlendThreads];   // transposed: per pixel, covering entries per chunk
 };
 
-// Stage one batch: thread i < n loads entry base+i (i >= n: empty mask).
+// Stage one batch: thread i < n loads entry base+i (i >= n: empty mask),
+// then every warp transposes its coverage words into per-pixel bit lists.
 template <typename S, int NB>
 __device__ __forceinline__ void stage_batch(const BlendArgs<S>& p, StageSmem<S, NB>& sm, uint32_t base, int n,
-                                            uint32_t vbase_item, int x0, int y0, uint32_t& my_item) {
+                                            uint32_t vbase_item, int x0, int y0) {
   for (int i = threadIdx.x; i < NB; i += kBlendThreads) {
     uint32_t w[8];
     if (i < n) {
       const uint32_t item = p.entry_item[base + i];
-      if (i == (int)threadIdx.x) my_item = item;
       const Splat<S> s = p.splat[item];
       const V4<S> c = p.col4[item - vbase_item];
-      sm.geo[i] = s.a;
+      V2<S> m;
+      m.x = s.a.x; m.y = s.a.y;
+      sm.mean[i] = m;
+      sm.q[i] = Eval<S>::prep(s.a.z, s.a.w, s.b.x, c.w);
       sm.col[i] = c;
-      sm.cc[i] = s.b.x;
       tile_coverage(s.a, s.b, x0, y0, w);
     } else {
 #pragma unroll
@@ -536,7 +566,33 @@ __device__ __forceinline__ void stage_batch(const BlendArgs<S>& p, StageSmem<S, 
 #pragma unroll
     for (int q = 0; q < 8; ++q) sm.cov[i][q] = w[q];
   }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int c = 0; c < NB / 32; ++c)
+    if (c * 32 < n) sm.tw[c][threadIdx.x] = transpose32(sm.cov[c * 32 + lane][warp], lane);
 }
+
+// Iterator over a lane's covering entries of the staged batch, in order.
+struct BitWalk {
+  int c, nch;
+  uint32_t bits;
+  template <int NB>
+  __device__ __forceinline__ void start(const uint32_t (&tw)[NB / 32][kBlendThreads], int n, bool skip) {
+    nch = skip ? 0 : (n + 31) >> 5;
+    c = 0;
+    bits = nch ? tw[0][threadIdx.x] : 0u;
+  }
+  template <int NB>
+  __device__ __forceinline__ int next(const uint32_t (&tw)[NB / 32][kBlendThreads]) {
+    while (!bits && ++c < nch) bits = tw[c][threadIdx.x];
+    if (!bits) return -1;
+    const int k = __ffs(bits) - 1;
+    bits &= bits - 1;
+    return c * 32 + k;
+  }
+  __device__ __forceinline__ void stop() { bits = 0; nch = 0; }
+};
 
 template <typename S>
 __global__ void __launch_bounds__(kBlendThreads) blend_forward(BlendArgs<S> p) {
@@ -557,32 +613,26 @@ __global__ void __launch_bounds__(kBlendThreads) blend_forward(BlendArgs<S> p) {
   for (uint32_t base = start; base < end; base += kFwdBatch) {
     if (__syncthreads_count(done) == kBlendThreads) break;
     const int n = (int)min((uint32_t)kFwdBatch, end - base);
-    uint32_t my_item;
-    stage_batch<S, kFwdBatch>(p, sm, base, n, vbase_item, x0, y0, my_item);
+    stage_batch<S, kFwdBatch>(p, sm, base, n, vbase_item, x0, y0);
     __syncthreads();
-    for (int c = 0; c < (n + 31) / 32; ++c) {
-      if (__all_sync(0xffffffffu, done)) break;
-      uint32_t bits = transpose32(sm.cov[c * 32 + lane][warp], lane);
-      if (done) bits = 0;
-      while (bits) {
-        const int j = c * 32 + (__ffs(bits) - 1);
-        bits &= bits - 1;
-        const V4<S> ge = sm.geo[j];
-        const V4<S> co = sm.col[j];
-        S dx, dy, ep, raw;
-        const S a = splat_alpha(fpx, fpy, ge, sm.cc[j], co.w, dx, dy, ep, raw);
-        if (a >= Const<S>::contrib_floor()) {
-          const S test = mul_rn(T, sub_rn(one, a));
-          if (test < Const<S>::t_stop()) {
-            done = true;
-            bits = 0;
-          } else {
-            const S w = mul_rn(a, T);
-            ar += w * co.x;
-            ag += w * co.y;
-            ab += w * co.z;
-            T = test;
-          }
+    BitWalk it;
+    it.start<kFwdBatch>(sm.tw, n, done);
+    for (int j; (j = it.next<kFwdBatch>(sm.tw)) >= 0;) {
+      const V2<S> m = sm.mean[j];
+      S ep, raw;
+      const S a = Eval<S>::alpha(sub_rn(fpx, m.x), sub_rn(fpy, m.y), sm.q[j], ep, raw);
+      if (a >= Const<S>::contrib_floor()) {
+        const S test = mul_rn(T, sub_rn(one, a));
+        if (test < Const<S>::t_stop()) {
+          done = true;
+          it.stop();
+        } else {
+          const V4<S> co = sm.col[j];
+          const S w = mul_rn(a, T);
+          ar += w * co.x;
+          ag += w * co.y;
+          ab += w * co.z;
+          T = test;
         }
       }
     }
@@ -598,31 +648,35 @@ __global__ void __launch_bounds__(kBlendThreads) blend_forward(BlendArgs<S> p) {
   }
 }
 
-template <typename S> struct V2 { S x, y; };
+template <typename S, bool kOpacity> struct SlotOf { typedef V2<S> type; };
+template <typename S> struct SlotOf<S, true> { typedef V4<S> type; };
 
-template <typename S> struct BwdSmem {
+template <typename S, bool kOpacity> struct BwdSmem {
   StageSmem<S, kBwdBatch> st;
-  uint32_t inc[kBwdBatch / 32][kBlendThreads];      // per pixel: included entries of this round
-  V4<S> pix[kBlendThreads];                          // per pixel: g_r, g_g, g_b, (g.bg - g_a) T_final
-  V2<S> slot[kBwdSlots][kBlendThreads];              // per pixel and included pair: (T_before, suffix)
+  uint32_t inc[kBwdBatch / 32][kBlendThreads];   // per pixel: included entries of this round
+  uint32_t incpre[kBlendThreads];                 // per pixel: bytes = included count before chunk c
+  V4<S> pix[kBlendThreads];                       // per pixel: g_r, g_g, g_b
+  typename SlotOf<S, kOpacity>::type slot[kBwdSlots][kBlendThreads];   // (dp, w[, d_alpha * ep])
 };
 
 // Backward (render.py:294-361).  Per batch:
 //  pass 1 (lane = pixel): front-to-back re-scan with the forward's exact
-//    decisions; each included pair records (T_k, S_k) where
-//    S_k = C - sum_{j<=k} (g.c_j) w_j and C = g.(rgb - T_f bg) = sum_j (g.c_j) w_j;
-//  pass 2 (thread pair = entry, one half of the tile each): over the entry's
-//    covered pixels in row-major order,
-//      dL/dalpha = (g.c) T_k - (S_k + (g.bg - g_a) T_f) / (1 - alpha)
-//    -> sums [dp dx, dp dy, dp dx^2, dp dx dy, dp dy^2, w g_r, w g_g, w g_b]
-//    (dp = dL/dalpha * alpha where raw < 0.99, clamp gate :336-338).
-//  Fixed iteration orders and no atomics: the result is deterministic.
-//  If a pixel has more than kBwdSlots included pairs in a batch, the batch
-//  runs in several rounds.
+//    decisions.  With C = g.(rgb - T_f bg) = sum_j (g.c_j) w_j the suffix is
+//    S_k = C - sum_{j<=k} (g.c_j) w_j, and for each included pair
+//      dL/dalpha_k = (g.c_k) T_k - (S_k + (g.bg - g_a) T_f) / (1 - alpha_k)
+//    (render.py:327-334); it records dp = dL/dalpha * alpha (0 where the
+//    0.99 clamp is active, :336-338) and w = alpha T in a per-pixel slot;
+//  pass 2 (two threads per entry, one tile half each): over the entry's
+//    covered pixels in row-major order, the sums
+//      [dp dx, dp dy, dp dx^2, dp dx dy, dp dy^2, w g_r, w g_g, w g_b].
+//  Fixed iteration orders and no atomics: the result is deterministic.  A
+//  pixel with more than kBwdSlots included pairs in a batch makes the batch
+//  run in several rounds.
 template <typename S, bool kOpacity>
 __global__ void __launch_bounds__(kBlendThreads) blend_backward(BlendArgs<S> p) {
   extern __shared__ __align__(32) unsigned char dyn[];
-  BwdSmem<S>& sm = *reinterpret_cast<BwdSmem<S>*>(dyn);
+  BwdSmem<S, kOpacity>& sm = *reinterpret_cast<BwdSmem<S, kOpacity>*>(dyn);
+  typedef typename SlotOf<S, kOpacity>::type Slot;
   const uint32_t g = blockIdx.x;
   const uint32_t view = g / p.tiles_per_view, t = g % p.tiles_per_view;
   const int tx = (int)(t % (uint32_t)p.tiles_x), ty = (int)(t / (uint32_t)p.tiles_x);
@@ -632,48 +686,35 @@ __global__ void __launch_bounds__(kBlendThreads) blend_backward(BlendArgs<S> p) 
   const bool inside = px < p.W && py < p.H;
   const S fpx = S(px), fpy = S(py);
   const S one = S(1);
-  S Ctot = 0;
-  {
-    V4<S> pd;
-    pd.x = pd.y = pd.z = pd.w = S(0);
-    if (inside) {
-      const size_t pix = ((size_t)view * p.H + py) * p.W + px;
-      pd.x = p.g_rgb[3 * pix]; pd.y = p.g_rgb[3 * pix + 1]; pd.z = p.g_rgb[3 * pix + 2];
-      const S tf = p.t_final[pix];
-      const S gbg = pd.x * p.bg0 + pd.y * p.bg1 + pd.z * p.bg2;
-      Ctot = pd.x * p.rgb[3 * pix] + pd.y * p.rgb[3 * pix + 1] + pd.z * p.rgb[3 * pix + 2] - gbg * tf;
-      pd.w = (gbg - p.g_alpha[pix]) * tf;
-    }
-    sm.pix[tid] = pd;
+  S Ctot = 0, bterm = 0;
+  V4<S> mypix;
+  mypix.x = mypix.y = mypix.z = mypix.w = S(0);
+  if (inside) {
+    const size_t pix = ((size_t)view * p.H + py) * p.W + px;
+    mypix.x = p.g_rgb[3 * pix]; mypix.y = p.g_rgb[3 * pix + 1]; mypix.z = p.g_rgb[3 * pix + 2];
+    const S tf = p.t_final[pix];
+    const S gbg = mypix.x * p.bg0 + mypix.y * p.bg1 + mypix.z * p.bg2;
+    Ctot = mypix.x * p.rgb[3 * pix] + mypix.y * p.rgb[3 * pix + 1] + mypix.z * p.rgb[3 * pix + 2] - gbg * tf;
+    bterm = (gbg - p.g_alpha[pix]) * tf;
   }
-  const V4<S> mypix = sm.pix[tid];
+  sm.pix[tid] = mypix;
   S T = one, P = 0;
   bool done = !inside;
   const uint32_t start = p.bounds[g], end = p.bounds[g + 1];
   const uint32_t vbase_item = view * p.items_per_view;
-  // pass-2 role: entry je, rows [8h, 8h + 8) of the tile
+  // pass-2 role: entry je, tile rows [8 half, 8 half + 8)
   const int je = tid >> 1, half = tid & 1;
   uint32_t base = start;
   for (; base < end; base += kBwdBatch) {
     if (__syncthreads_count(done) == kBlendThreads) break;
     const int n = (int)min((uint32_t)kBwdBatch, end - base);
-    uint32_t my_item = 0;
-    stage_batch<S, kBwdBatch>(p, sm.st, base, n, vbase_item, x0, y0, my_item);
+    stage_batch<S, kBwdBatch>(p, sm.st, base, n, vbase_item, x0, y0);
     __syncthreads();
-    uint32_t cw[kBwdBatch / 32];
-#pragma unroll
-    for (int c = 0; c < kBwdBatch / 32; ++c) {
-      cw[c] = transpose32(sm.st.cov[c * 32 + lane][warp], lane);
-      if (done) cw[c] = 0;
-    }
-    // pass-2 entry parameters (registers across rounds)
-    V4<S> ge, co;
-    S ecc = S(0);
-    if (je < n) {
-      ge = sm.st.geo[je];
-      co = sm.st.col[je];
-      ecc = sm.st.cc[je];
-    }
+    BitWalk it;
+    it.start<kBwdBatch>(sm.st.tw, n, done);
+    V2<S> em;
+    em.x = em.y = S(0);
+    if (je < n) em = sm.st.mean[je];
     S acc[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) acc[q] = S(0);
@@ -683,43 +724,50 @@ __global__ void __launch_bounds__(kBlendThreads) blend_backward(BlendArgs<S> p) 
       int cnt = 0;
       uint32_t inc[kBwdBatch / 32];
 #pragma unroll
-      for (int c = 0; c < kBwdBatch / 32; ++c) {
-        inc[c] = 0;
-        while (cw[c] && cnt < kBwdSlots) {
-          const int k = __ffs(cw[c]) - 1;
-          cw[c] &= cw[c] - 1;
-          const int j = c * 32 + k;
-          const V4<S> g1 = sm.st.geo[j];
-          const V4<S> c1 = sm.st.col[j];
-          S dx, dy, ep, raw;
-          const S a = splat_alpha(fpx, fpy, g1, sm.st.cc[j], c1.w, dx, dy, ep, raw);
-          if (a >= Const<S>::contrib_floor()) {
-            const S om = sub_rn(one, a);
-            const S test = mul_rn(T, om);
-            if (test < Const<S>::t_stop()) {
-              done = true;
-#pragma unroll
-              for (int q = 0; q < kBwdBatch / 32; ++q) cw[q] = 0;
-            } else {
-              const S w = mul_rn(a, T);
-              P += (mypix.x * c1.x + mypix.y * c1.y + mypix.z * c1.z) * w;
-              V2<S> rec;
-              rec.x = T;
-              rec.y = Ctot - P;
-              sm.slot[cnt][tid] = rec;
-              inc[c] |= 1u << k;
-              ++cnt;
-              T = test;
+      for (int c = 0; c < kBwdBatch / 32; ++c) inc[c] = 0;
+      int j;
+      while (cnt < kBwdSlots && (j = it.next<kBwdBatch>(sm.st.tw)) >= 0) {
+        const V2<S> m = sm.st.mean[j];
+        S ep, raw;
+        const S a = Eval<S>::alpha(sub_rn(fpx, m.x), sub_rn(fpy, m.y), sm.st.q[j], ep, raw);
+        if (a >= Const<S>::contrib_floor()) {
+          const S om = sub_rn(one, a);
+          const S test = mul_rn(T, om);
+          if (test < Const<S>::t_stop()) {
+            done = true;
+            it.stop();
+          } else {
+            const V4<S> co = sm.st.col[j];
+            const S w = mul_rn(a, T);
+            const S gdc = mypix.x * co.x + mypix.y * co.y + mypix.z * co.z;
+            P += gdc * w;
+            const S d_alpha = gdc * T - ((Ctot - P) + bterm) / om;
+            Slot s;
+            s.x = raw < Const<S>::alpha_clamp() ? d_alpha * a : S(0);
+            s.y = w;
+            if constexpr (kOpacity) {
+              s.z = raw < Const<S>::alpha_clamp() ? d_alpha * ep : S(0);
+              s.w = S(0);
             }
+            sm.slot[cnt][tid] = s;
+            // inc[] is a register array: select the word with constant indices
+#pragma unroll
+            for (int c = 0; c < kBwdBatch / 32; ++c)
+              if ((j >> 5) == c) inc[c] |= 1u << (j & 31);
+            ++cnt;
+            T = test;
           }
         }
       }
-      bool left = false;
+      uint32_t pre = 0, run = 0;
 #pragma unroll
       for (int c = 0; c < kBwdBatch / 32; ++c) {
         sm.inc[c][tid] = inc[c];
-        left |= cw[c] != 0;
+        pre |= run << (8 * c);
+        run += __popc(inc[c]);
       }
+      sm.incpre[tid] = pre;
+      const bool left = it.bits != 0 || (it.c + 1 < it.nch);
       const bool more = __syncthreads_or(left);
       // ---- pass 2: my entry over its covered pixels in my half ----
       if (je < n) {
@@ -731,32 +779,23 @@ __global__ void __launch_bounds__(kBlendThreads) blend_backward(BlendArgs<S> p) 
           while (bits) {
             const int b = __ffs(bits) - 1;
             bits &= bits - 1;
-            const int q = wi * 32 + b;   // tile pixel; its lane/thread index is q
+            const int q = wi * 32 + b;   // tile pixel (= its thread index)
             const uint32_t iw = sm.inc[cj][q];
             if (!((iw >> kj) & 1u)) continue;
-            int idx = __popc(iw & below);
-            for (int c = 0; c < cj; ++c) idx += __popc(sm.inc[c][q]);
-            const V2<S> rec = sm.slot[idx][q];
+            const int idx = __popc(iw & below) + ((sm.incpre[q] >> (8 * cj)) & 255u);
+            const Slot s = sm.slot[idx][q];
             const V4<S> pd = sm.pix[q];
-            const S qx = S(x0 + (q & 15)), qy = S(y0 + (q >> 4));
-            S dx, dy, ep, raw;
-            const S a = splat_alpha(qx, qy, ge, ecc, co.w, dx, dy, ep, raw);
-            const S gdc = pd.x * co.x + pd.y * co.y + pd.z * co.z;
-            const S w = a * rec.x;
-            const S d_alpha = gdc * rec.x - (rec.y + pd.w) / sub_rn(one, a);
-            if (raw < Const<S>::alpha_clamp()) {
-              const S dp = d_alpha * a;
-              const S dpx = dp * dx, dpy = dp * dy;
-              acc[0] += dpx;
-              acc[1] += dpy;
-              acc[2] += dpx * dx;
-              acc[3] += dpx * dy;
-              acc[4] += dpy * dy;
-              if (kOpacity) aop += d_alpha * ep;
-            }
-            acc[5] += w * pd.x;
-            acc[6] += w * pd.y;
-            acc[7] += w * pd.z;
+            const S dx = sub_rn(S(x0 + (q & 15)), em.x), dy = sub_rn(S(y0 + (q >> 4)), em.y);
+            const S dpx = s.x * dx, dpy = s.x * dy;
+            acc[0] += dpx;
+            acc[1] += dpy;
+            acc[2] += dpx * dx;
+            acc[3] += dpx * dy;
+            acc[4] += dpy * dy;
+            acc[5] += s.y * pd.x;
+            acc[6] += s.y * pd.y;
+            acc[7] += s.y * pd.z;
+            if constexpr (kOpacity) aop += s.z;
           }
         }
       }
@@ -767,8 +806,8 @@ __global__ void __launch_bounds__(kBlendThreads) blend_backward(BlendArgs<S> p) 
 #pragma unroll
     for (int q = 0; q < 8; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], 1);
     if (kOpacity) aop += __shfl_xor_sync(0xffffffffu, aop, 1);
-    const uint32_t item_j = (je < n) ? p.entry_item[base + je] : 0u;
     if (half == 0 && je < n) {
+      const uint32_t item_j = p.entry_item[base + je];
       const uint2 rc = p.rect[item_j];
       const int tx0 = rc.x & 0xffff, ty0 = rc.x >> 16, tx1 = rc.y & 0xffff;
       const uint32_t slot = p.entry_off[item_j] + (uint32_t)((ty - ty0) * (tx1 - tx0 + 1) + (tx - tx0));
