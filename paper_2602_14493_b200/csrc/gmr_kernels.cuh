@@ -465,31 +465,35 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
 }
 
 // Coverage of one splat in the tile with pixel origin (x0, y0): tile bit
-// y*16 + x, packed in 8 words (word w = rows 2w, 2w+1).
+// y*16 + x, OR-ed row by row into 8 zeroed words `w` (word i = rows 2i,
+// 2i+1; shared memory, so the row index may be dynamic).
 template <typename S>
-__device__ __forceinline__ void tile_coverage(const V4<S>& a, const V4<S>& b, int x0, int y0, uint32_t w[8]) {
-#pragma unroll
-  for (int i = 0; i < 8; ++i) w[i] = 0;
+__device__ __forceinline__ void tile_coverage(const V4<S>& a, const V4<S>& b, int x0, int y0, uint32_t* w) {
   const S mx = a.x, my = a.y, ca = a.z, cb = a.w, cc = b.x, ex = b.y, ey = b.z, tau = b.w;
   if (!(ex >= S(0)) || !(ca > S(0))) return;
-  const S ylo = ceil(my - ey), yhi = floor(my + ey);
-  const int r0 = (int)fmax(S(0), ylo - S(y0)), r1 = (int)fmin(S(15), yhi - S(y0));
-  const S xlo_t = S(x0), xhi_t = S(x0 + 15);
+  const int r0 = (int)fmax(S(0), ceil(my - ey) - S(y0));
+  const int r1 = (int)fmin(S(15), floor(my + ey) - S(y0));
+  const S mxr = mx - S(x0);
   const S neg_det = cb * cb - ca * cc;   // b^2 - ac < 0 for a positive definite conic
   const S inv_a = S(1) / ca;
+#pragma unroll 1
   for (int r = r0; r <= r1; ++r) {
     const S dy = S(y0 + r) - my;
     const S disc = dy * dy * neg_det + ca * tau;
     if (!(disc >= S(0))) continue;
     const S hw = sqrt_s(disc) * inv_a * S(1.0005) + S(0.01);
-    const S xc = mx - cb * dy * inv_a;
-    const S lo = fmax(ceil(xc - hw), xlo_t), hi = fmin(floor(xc + hw), xhi_t);
+    const S xc = mxr - cb * dy * inv_a;
+    const S lo = fmax(ceil(xc - hw), S(0)), hi = fmin(floor(xc + hw), S(15));
     if (lo > hi) continue;
-    const int ilo = (int)lo - x0, ihi = (int)hi - x0;
-    const uint32_t bits = ((0xffffu >> (15 - (ihi - ilo))) << ilo) & 0xffffu;
+    const int ilo = (int)lo, ihi = (int)hi;
+    const uint32_t bits = (0xffffu >> (15 - (ihi - ilo))) << ilo;
     w[r >> 1] |= bits << ((r & 1) * 16);
   }
 }
+
+// 1 / (1 - alpha) with 1 - alpha >= 0.01 (alpha clamp)
+__device__ __forceinline__ float inv_om(float om) { return __fdividef(1.0f, om); }
+__device__ __forceinline__ double inv_om(double om) { return 1.0 / om; }
 
 // Per-pixel alpha of a staged splat (render.py:251-256).  `q` holds the
 // splat's conic in the form the evaluator wants (Eval<S>::prep).
@@ -548,7 +552,9 @@ template <typename S, int NB>
 __device__ __forceinline__ void stage_batch(const BlendArgs<S>& p, StageSmem<S, NB>& sm, uint32_t base, int n,
                                             uint32_t vbase_item, int x0, int y0) {
   for (int i = threadIdx.x; i < NB; i += kBlendThreads) {
-    uint32_t w[8];
+    uint32_t* w = sm.cov[i];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) w[q] = 0;
     if (i < n) {
       const uint32_t item = p.entry_item[base + i];
       const Splat<S> s = p.splat[item];
@@ -559,12 +565,7 @@ __device__ __forceinline__ void stage_batch(const BlendArgs<S>& p, StageSmem<S, 
       sm.q[i] = Eval<S>::prep(s.a.z, s.a.w, s.b.x, c.w);
       sm.col[i] = c;
       tile_coverage(s.a, s.b, x0, y0, w);
-    } else {
-#pragma unroll
-      for (int q = 0; q < 8; ++q) w[q] = 0;
     }
-#pragma unroll
-    for (int q = 0; q < 8; ++q) sm.cov[i][q] = w[q];
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -653,8 +654,7 @@ template <typename S> struct SlotOf<S, true> { typedef V4<S> type; };
 
 template <typename S, bool kOpacity> struct BwdSmem {
   StageSmem<S, kBwdBatch> st;
-  uint32_t inc[kBwdBatch / 32][kBlendThreads];   // per pixel: included entries of this round
-  uint32_t incpre[kBlendThreads];                 // per pixel: bytes = included count before chunk c
+  uint2 incp[kBwdBatch / 32][kBlendThreads];     // per pixel and chunk: (included bits, count before chunk)
   V4<S> pix[kBlendThreads];                       // per pixel: g_r, g_g, g_b
   typename SlotOf<S, kOpacity>::type slot[kBwdSlots][kBlendThreads];   // (dp, w[, d_alpha * ep])
 };
@@ -710,8 +710,9 @@ __global__ void __launch_bounds__(kBlendThreads) blend_backward(BlendArgs<S> p) 
     const int n = (int)min((uint32_t)kBwdBatch, end - base);
     stage_batch<S, kBwdBatch>(p, sm.st, base, n, vbase_item, x0, y0);
     __syncthreads();
-    BitWalk it;
-    it.start<kBwdBatch>(sm.st.tw, n, done);
+    uint32_t cw[kBwdBatch / 32];
+#pragma unroll
+    for (int c = 0; c < kBwdBatch / 32; ++c) cw[c] = (done || c * 32 >= n) ? 0u : sm.st.tw[c][tid];
     V2<S> em;
     em.x = em.y = S(0);
     if (je < n) em = sm.st.mean[je];
@@ -724,65 +725,69 @@ __global__ void __launch_bounds__(kBlendThreads) blend_backward(BlendArgs<S> p) 
       int cnt = 0;
       uint32_t inc[kBwdBatch / 32];
 #pragma unroll
-      for (int c = 0; c < kBwdBatch / 32; ++c) inc[c] = 0;
-      int j;
-      while (cnt < kBwdSlots && (j = it.next<kBwdBatch>(sm.st.tw)) >= 0) {
-        const V2<S> m = sm.st.mean[j];
-        S ep, raw;
-        const S a = Eval<S>::alpha(sub_rn(fpx, m.x), sub_rn(fpy, m.y), sm.st.q[j], ep, raw);
-        if (a >= Const<S>::contrib_floor()) {
-          const S om = sub_rn(one, a);
-          const S test = mul_rn(T, om);
-          if (test < Const<S>::t_stop()) {
-            done = true;
-            it.stop();
-          } else {
-            const V4<S> co = sm.st.col[j];
-            const S w = mul_rn(a, T);
-            const S gdc = mypix.x * co.x + mypix.y * co.y + mypix.z * co.z;
-            P += gdc * w;
-            const S d_alpha = gdc * T - ((Ctot - P) + bterm) / om;
-            Slot s;
-            s.x = raw < Const<S>::alpha_clamp() ? d_alpha * a : S(0);
-            s.y = w;
-            if constexpr (kOpacity) {
-              s.z = raw < Const<S>::alpha_clamp() ? d_alpha * ep : S(0);
-              s.w = S(0);
-            }
-            sm.slot[cnt][tid] = s;
-            // inc[] is a register array: select the word with constant indices
+      for (int c = 0; c < kBwdBatch / 32; ++c) {
+        inc[c] = 0;
+        while (cw[c] && cnt < kBwdSlots) {
+          const int kk = __ffs(cw[c]) - 1;
+          cw[c] &= cw[c] - 1;
+          const int j = c * 32 + kk;
+          const V2<S> m = sm.st.mean[j];
+          S ep, raw;
+          const S a = Eval<S>::alpha(sub_rn(fpx, m.x), sub_rn(fpy, m.y), sm.st.q[j], ep, raw);
+          if (a >= Const<S>::contrib_floor()) {
+            const S om = sub_rn(one, a);
+            const S test = mul_rn(T, om);
+            if (test < Const<S>::t_stop()) {
+              done = true;
 #pragma unroll
-            for (int c = 0; c < kBwdBatch / 32; ++c)
-              if ((j >> 5) == c) inc[c] |= 1u << (j & 31);
-            ++cnt;
-            T = test;
+              for (int q2 = 0; q2 < kBwdBatch / 32; ++q2) cw[q2] = 0;
+            } else {
+              const V4<S> co = sm.st.col[j];
+              const S w = mul_rn(a, T);
+              const S gdc = mypix.x * co.x + mypix.y * co.y + mypix.z * co.z;
+              P += gdc * w;
+              const S d_alpha = gdc * T - ((Ctot - P) + bterm) * inv_om(om);
+              Slot s;
+              s.x = raw < Const<S>::alpha_clamp() ? d_alpha * a : S(0);
+              s.y = w;
+              if constexpr (kOpacity) {
+                s.z = raw < Const<S>::alpha_clamp() ? d_alpha * ep : S(0);
+                s.w = S(0);
+              }
+              sm.slot[cnt][tid] = s;
+              inc[c] |= 1u << kk;
+              ++cnt;
+              T = test;
+            }
           }
         }
       }
-      uint32_t pre = 0, run = 0;
+      {
+        uint32_t run = 0;
 #pragma unroll
-      for (int c = 0; c < kBwdBatch / 32; ++c) {
-        sm.inc[c][tid] = inc[c];
-        pre |= run << (8 * c);
-        run += __popc(inc[c]);
+        for (int c = 0; c < kBwdBatch / 32; ++c) {
+          sm.incp[c][tid] = make_uint2(inc[c], run);
+          run += __popc(inc[c]);
+        }
       }
-      sm.incpre[tid] = pre;
-      const bool left = it.bits != 0 || (it.c + 1 < it.nch);
+      bool left = false;
+#pragma unroll
+      for (int c = 0; c < kBwdBatch / 32; ++c) left |= cw[c] != 0;
       const bool more = __syncthreads_or(left);
-      // ---- pass 2: my entry over its covered pixels in my half ----
+      // ---- pass 2: my entry over its covered pixels (row pairs 2i + half) ----
       if (je < n) {
         const int cj = je >> 5, kj = je & 31;
         const uint32_t below = (1u << kj) - 1u;
 #pragma unroll 1
-        for (int wi = 4 * half; wi < 4 * half + 4; ++wi) {
+        for (int wi = half; wi < 8; wi += 2) {
           uint32_t bits = sm.st.cov[je][wi];
           while (bits) {
             const int b = __ffs(bits) - 1;
             bits &= bits - 1;
             const int q = wi * 32 + b;   // tile pixel (= its thread index)
-            const uint32_t iw = sm.inc[cj][q];
-            if (!((iw >> kj) & 1u)) continue;
-            const int idx = __popc(iw & below) + ((sm.incpre[q] >> (8 * cj)) & 255u);
+            const uint2 ip = sm.incp[cj][q];
+            if (!((ip.x >> kj) & 1u)) continue;
+            const int idx = __popc(ip.x & below) + (int)ip.y;
             const Slot s = sm.slot[idx][q];
             const V4<S> pd = sm.pix[q];
             const S dx = sub_rn(S(x0 + (q & 15)), em.x), dy = sub_rn(S(y0 + (q >> 4)), em.y);
