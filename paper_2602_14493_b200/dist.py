@@ -1,0 +1,112 @@
+"""Multi-GPU view sharding.
+
+The reference sums per-view vertex gradients in a serial Python loop
+(`losses.py:151-162`: grad_v += gv, grad_c += gc, each view scaled by w/n).
+Views are independent given the mesh, so every rank renders a contiguous
+shard of the batch on its own GPU, and the only exchange is one SUM
+all-reduce of the packed [grad_pos | grad_col] (V x 6) buffer plus the
+loss partial sums.  One process per GPU, `torch.distributed` with NCCL
+over NVLink/NVSwitch (gloo works for CPU tests of this logic).
+
+Single-rank vs R-rank results differ only by the fp32 summation order of
+the all-reduce (rank order is fixed, so a given world size is
+deterministic).
+"""
+
+from __future__ import annotations
+
+from typing import Callable, Sequence
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+
+def shard_range(n: int, rank: int, world: int):
+    """Contiguous split of n views: rank r gets [r*n/R, (r+1)*n/R)."""
+    return (rank * n) // world, ((rank + 1) * n) // world
+
+
+def allreduce_vertex_grads(g_pos: torch.Tensor, g_col: torch.Tensor, extra: torch.Tensor | None = None,
+                           group=None):
+    """One packed SUM all-reduce of [grad_pos | grad_col (| extra scalars)]."""
+    parts = [g_pos.reshape(-1), g_col.reshape(-1)]
+    if extra is not None:
+        parts.append(extra.reshape(-1).to(g_pos.dtype))
+    buf = torch.cat(parts)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+    n = g_pos.numel()
+    out_pos = buf[:n].view_as(g_pos)
+    out_col = buf[n:2 * n].view_as(g_col)
+    out_extra = buf[2 * n:] if extra is not None else None
+    return out_pos, out_col, out_extra
+
+
+def sharded_image_loss(local_fn: Callable, cameras: Sequence, target_rgb: Sequence, target_mask: Sequence,
+                       num_vertices: int, w_color: float = 1.0, w_sil: float = 1.0, group=None,
+                       device=None):
+    """Image part of `total_loss` (losses.py:146-164) over views sharded
+    across the process group.
+
+    `local_fn(cams, rgbs, masks, scale_rgb, scale_alpha)` evaluates this
+    rank's views and returns (sum of per-view colour losses, sum of per-view
+    silhouette losses, grad_pos [V,3], grad_col [V,3]) with image grads
+    pre-scaled by w/n (n = the GLOBAL view count) -- on the GPU that is
+    `gpu_local_image_loss` below.  Returns
+    (color, silhouette, grad_pos, grad_col) identical on every rank.
+    """
+    world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+    rank = dist.get_rank(group) if world > 1 else 0
+    n = len(cameras)
+    lo, hi = shard_range(n, rank, world)
+    if hi > lo:
+        cval, sval, gp, gc = local_fn(cameras[lo:hi], target_rgb[lo:hi], target_mask[lo:hi],
+                                      w_color / n, w_sil / n)
+        gp = torch.as_tensor(gp, dtype=torch.float64, device=device)
+        gc = torch.as_tensor(gc, dtype=torch.float64, device=device)
+    else:
+        cval = sval = 0.0
+        gp = torch.zeros((num_vertices, 3), dtype=torch.float64, device=device)
+        gc = torch.zeros((num_vertices, 3), dtype=torch.float64, device=device)
+    extra = torch.tensor([cval, sval], dtype=torch.float64, device=gp.device)
+    gp, gc, extra = allreduce_vertex_grads(gp, gc, extra, group)
+    return float(extra[0]) / n, float(extra[1]) / n, gp, gc
+
+
+def gpu_local_image_loss(mesh, background=(0.0, 0.0, 0.0), rescale=True, dtype=np.float32):
+    """The GPU `local_fn` for `sharded_image_loss`: this rank's views in one
+    libgmr call per resolution (paper_2602_14493_b200.api.total_loss math)."""
+    from . import api, engine
+
+    pos, col, faces = api._device_mesh(mesh, dtype)
+    tdt = api._torch_dtype(dtype)
+    dev = pos.device
+
+    def local_fn(cams, rgbs, masks, scale_rgb, scale_alpha):
+        gp_all = torch.zeros((pos.shape[0], 3), dtype=torch.float64, device=dev)
+        gc_all = torch.zeros_like(gp_all)
+        cv = sv = 0.0
+        groups = {}
+        for i, c in enumerate(cams):
+            groups.setdefault((c.width, c.height), []).append(i)
+        for (w, h), idx in groups.items():
+            rgb, alpha, st = engine.render_forward(pos, col, faces, [cams[i] for i in idx], w, h,
+                                                   np.asarray(background, np.float64), rescale)
+            t_rgb = torch.as_tensor(np.stack([np.asarray(rgbs[i], np.float64) for i in idx])).to(dev)
+            t_m = torch.as_tensor(np.stack([np.asarray(masks[i], np.float64) for i in idx])).to(dev)
+            r64, a64 = rgb.double(), alpha.double()
+            diff = r64 - t_rgb
+            cv += float((diff * diff).mean(dim=(1, 2, 3)).sum())
+            g_rgb = (2.0 / diff[0].numel()) * diff * scale_rgb
+            p = a64.clamp(api.BCE_CLAMP, 1.0 - api.BCE_CLAMP)
+            sv += float((-(t_m * torch.log(p) + (1.0 - t_m) * torch.log1p(-p))).mean(dim=(1, 2)).sum())
+            inside = (a64 > api.BCE_CLAMP) & (a64 < 1.0 - api.BCE_CLAMP)
+            g_a = torch.where(inside, (-t_m / p + (1.0 - t_m) / (1.0 - p)) / a64[0].numel(),
+                              torch.zeros_like(a64)) * scale_alpha
+            gp, gc = engine.render_backward(st, pos, col, faces, rgb, g_rgb.to(tdt), g_a.to(tdt))
+            gp_all += gp.double()
+            gc_all += gc.double()
+        return cv, sv, gp_all, gc_all
+
+    return local_fn
