@@ -649,34 +649,44 @@ __global__ void __launch_bounds__(kBlendThreads) blend_forward(BlendArgs<S> p) {
   }
 }
 
-template <typename S, bool kOpacity> struct SlotOf { typedef V2<S> type; };
-template <typename S> struct SlotOf<S, true> { typedef V4<S> type; };
+template <typename S, bool kOpacity> struct RecOf { typedef V2<S> type; };
+template <typename S> struct RecOf<S, true> { typedef V4<S> type; };
+
+constexpr int kBwdPairBytes = 32 * 1024;
 
 template <typename S, bool kOpacity> struct BwdSmem {
+  typedef typename RecOf<S, kOpacity>::type Rec;
+  static constexpr int kCap = kBwdPairBytes / (int)(sizeof(Rec) + 1);
   StageSmem<S, kBwdBatch> st;
-  uint2 incp[kBwdBatch / 32][kBlendThreads];     // per pixel and chunk: (included bits, count before chunk)
-  V4<S> pix[kBlendThreads];                       // per pixel: g_r, g_g, g_b
-  typename SlotOf<S, kOpacity>::type slot[kBwdSlots][kBlendThreads];   // (dp, w[, d_alpha * ep])
+  uint32_t pre[kBwdBatch][2];       // per entry: covered-pixel count before each row pair (bytes)
+  uint32_t off[kBwdBatch + 1];      // per entry: first record (exclusive scan of covered counts)
+  uint32_t scan_tmp[8];
+  V4<S> pix[kBlendThreads];         // per pixel: g_r, g_g, g_b
+  Rec rec[kCap];                    // per (entry, covered pixel in row-major order): (dp, w[, dL/dalpha * ep])
+  uint8_t rq[kCap];                 // tile pixel of each record
 };
 
-// Backward (render.py:294-361).  Per batch:
-//  pass 1 (lane = pixel): front-to-back re-scan with the forward's exact
+// Backward (render.py:294-361).  Per batch of staged entries:
+//  - every entry's covered pixels get a contiguous record range (block scan
+//    of the coverage popcounts; the batch is cut where the ranges would
+//    overflow shared memory) and the records are zeroed;
+//  - pass 1 (lane = pixel) re-scans front to back with the forward's exact
 //    decisions.  With C = g.(rgb - T_f bg) = sum_j (g.c_j) w_j the suffix is
-//    S_k = C - sum_{j<=k} (g.c_j) w_j, and for each included pair
+//    S_k = C - sum_{j<=k} (g.c_j) w_j, so (render.py:327-334)
 //      dL/dalpha_k = (g.c_k) T_k - (S_k + (g.bg - g_a) T_f) / (1 - alpha_k)
-//    (render.py:327-334); it records dp = dL/dalpha * alpha (0 where the
-//    0.99 clamp is active, :336-338) and w = alpha T in a per-pixel slot;
-//  pass 2 (two threads per entry, one tile half each): over the entry's
-//    covered pixels in row-major order, the sums
-//      [dp dx, dp dy, dp dx^2, dp dx dy, dp dy^2, w g_r, w g_g, w g_b].
-//  Fixed iteration orders and no atomics: the result is deterministic.  A
-//  pixel with more than kBwdSlots included pairs in a batch makes the batch
-//  run in several rounds.
+//    and each included pair writes (dp = dL/dalpha * alpha, 0 where the 0.99
+//    clamp is active (:336-338), w = alpha T) to record
+//    off[j] + (rank of this pixel among j's covered pixels);
+//  - pass 2 (two threads per entry, halves of its records) sums
+//      [dp dx, dp dy, dp dx^2, dp dx dy, dp dy^2, w g_r, w g_g, w g_b]
+//    in pixel order; the halves are combined in a fixed order.
+//  No atomics, fixed orders: the result is deterministic.
 template <typename S, bool kOpacity>
 __global__ void __launch_bounds__(kBlendThreads) blend_backward(BlendArgs<S> p) {
   extern __shared__ __align__(32) unsigned char dyn[];
-  BwdSmem<S, kOpacity>& sm = *reinterpret_cast<BwdSmem<S, kOpacity>*>(dyn);
-  typedef typename SlotOf<S, kOpacity>::type Slot;
+  typedef BwdSmem<S, kOpacity> Sm;
+  typedef typename Sm::Rec Rec;
+  Sm& sm = *reinterpret_cast<Sm*>(dyn);
   const uint32_t g = blockIdx.x;
   const uint32_t view = g / p.tiles_per_view, t = g % p.tiles_per_view;
   const int tx = (int)(t % (uint32_t)p.tiles_x), ty = (int)(t / (uint32_t)p.tiles_x);
@@ -686,6 +696,7 @@ __global__ void __launch_bounds__(kBlendThreads) blend_backward(BlendArgs<S> p) 
   const bool inside = px < p.W && py < p.H;
   const S fpx = S(px), fpy = S(py);
   const S one = S(1);
+  const unsigned lt = lanemask_lt();
   S Ctot = 0, bterm = 0;
   V4<S> mypix;
   mypix.x = mypix.y = mypix.z = mypix.w = S(0);
@@ -702,110 +713,130 @@ __global__ void __launch_bounds__(kBlendThreads) blend_backward(BlendArgs<S> p) 
   bool done = !inside;
   const uint32_t start = p.bounds[g], end = p.bounds[g + 1];
   const uint32_t vbase_item = view * p.items_per_view;
-  // pass-2 role: entry je, tile rows [8 half, 8 half + 8)
   const int je = tid >> 1, half = tid & 1;
   uint32_t base = start;
-  for (; base < end; base += kBwdBatch) {
+  while (base < end) {
     if (__syncthreads_count(done) == kBlendThreads) break;
-    const int n = (int)min((uint32_t)kBwdBatch, end - base);
-    stage_batch<S, kBwdBatch>(p, sm.st, base, n, vbase_item, x0, y0);
-    __syncthreads();
-    uint32_t cw[kBwdBatch / 32];
+    const int n_st = (int)min((uint32_t)kBwdBatch, end - base);
+    // ---- stage records + coverage ----
+    for (int i = tid; i < kBwdBatch; i += kBlendThreads) {
+      uint32_t* w = sm.st.cov[i];
 #pragma unroll
-    for (int c = 0; c < kBwdBatch / 32; ++c) cw[c] = (done || c * 32 >= n) ? 0u : sm.st.tw[c][tid];
-    V2<S> em;
-    em.x = em.y = S(0);
-    if (je < n) em = sm.st.mean[je];
+      for (int q = 0; q < 8; ++q) w[q] = 0;
+      if (i < n_st) {
+        const uint32_t item = p.entry_item[base + i];
+        const Splat<S> s = p.splat[item];
+        const V4<S> c = p.col4[item - vbase_item];
+        V2<S> m;
+        m.x = s.a.x; m.y = s.a.y;
+        sm.st.mean[i] = m;
+        sm.st.q[i] = Eval<S>::prep(s.a.z, s.a.w, s.b.x, c.w);
+        sm.st.col[i] = c;
+        tile_coverage(s.a, s.b, x0, y0, w);
+      }
+    }
+    __syncthreads();
+    // ---- per entry: covered count, row-pair prefixes; block scan -> offsets ----
+    uint32_t ncov = 0;
+    if (tid < kBwdBatch) {
+      uint32_t pre0 = 0, pre1 = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (q < 4) pre0 |= ncov << (8 * q); else pre1 |= ncov << (8 * (q - 4));
+        ncov += __popc(sm.st.cov[tid][q]);
+      }
+      sm.pre[tid][0] = pre0;
+      sm.pre[tid][1] = pre1;
+    }
+    uint32_t total;
+    const uint32_t excl = block_exclusive_scan_256(ncov, sm.scan_tmp, &total);
+    const bool fits = tid < n_st && excl + ncov <= (uint32_t)Sm::kCap;
+    if (tid < kBwdBatch) sm.off[tid] = excl;
+    const int n = __syncthreads_count(fits);          // entries taken this batch (prefix property)
+    // entries not taken are re-staged next batch: clear their coverage
+    for (int i = n + tid; i < kBwdBatch; i += kBlendThreads) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) sm.st.cov[i][q] = 0;
+    }
+    __syncthreads();
+    const uint32_t rec_end = (n == kBwdBatch) ? total : sm.off[n];
+    for (uint32_t r = tid; r < rec_end; r += kBlendThreads) {
+      Rec z;
+      z.x = z.y = S(0);
+      if constexpr (kOpacity) { z.z = z.w = S(0); }
+      sm.rec[r] = z;
+    }
+    const int warp_ = warp;
+#pragma unroll
+    for (int c = 0; c < kBwdBatch / 32; ++c)
+      if (c * 32 < n) sm.st.tw[c][tid] = transpose32(sm.st.cov[c * 32 + lane][warp_], lane);
+    __syncthreads();
+    // ---- pass 1: my pixel ----
+    {
+      BitWalk it;
+      it.start<kBwdBatch>(sm.st.tw, n, done);
+      for (int j; (j = it.next<kBwdBatch>(sm.st.tw)) >= 0;) {
+        const V2<S> m = sm.st.mean[j];
+        S ep, raw;
+        const S a = Eval<S>::alpha(sub_rn(fpx, m.x), sub_rn(fpy, m.y), sm.st.q[j], ep, raw);
+        if (a >= Const<S>::contrib_floor()) {
+          const S om = sub_rn(one, a);
+          const S test = mul_rn(T, om);
+          if (test < Const<S>::t_stop()) {
+            done = true;
+            it.stop();
+          } else {
+            const V4<S> co = sm.st.col[j];
+            const S w = mul_rn(a, T);
+            const S gdc = mypix.x * co.x + mypix.y * co.y + mypix.z * co.z;
+            P += gdc * w;
+            const S d_alpha = gdc * T - ((Ctot - P) + bterm) * inv_om(om);
+            Rec s;
+            s.x = raw < Const<S>::alpha_clamp() ? d_alpha * a : S(0);
+            s.y = w;
+            if constexpr (kOpacity) {
+              s.z = raw < Const<S>::alpha_clamp() ? d_alpha * ep : S(0);
+              s.w = S(0);
+            }
+            const uint32_t pw = sm.pre[j][warp >> 2];
+            const uint32_t r = sm.off[j] + ((pw >> (8 * (warp & 3))) & 255u) +
+                               (uint32_t)__popc(sm.st.cov[j][warp] & lt);
+            sm.rec[r] = s;
+            sm.rq[r] = (uint8_t)tid;
+            T = test;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // ---- pass 2: my entry, my half of its records (pixel order) ----
     S acc[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) acc[q] = S(0);
     S aop = S(0);
-    for (;;) {
-      // ---- pass 1: my pixel ----
-      int cnt = 0;
-      uint32_t inc[kBwdBatch / 32];
-#pragma unroll
-      for (int c = 0; c < kBwdBatch / 32; ++c) {
-        inc[c] = 0;
-        while (cw[c] && cnt < kBwdSlots) {
-          const int kk = __ffs(cw[c]) - 1;
-          cw[c] &= cw[c] - 1;
-          const int j = c * 32 + kk;
-          const V2<S> m = sm.st.mean[j];
-          S ep, raw;
-          const S a = Eval<S>::alpha(sub_rn(fpx, m.x), sub_rn(fpy, m.y), sm.st.q[j], ep, raw);
-          if (a >= Const<S>::contrib_floor()) {
-            const S om = sub_rn(one, a);
-            const S test = mul_rn(T, om);
-            if (test < Const<S>::t_stop()) {
-              done = true;
-#pragma unroll
-              for (int q2 = 0; q2 < kBwdBatch / 32; ++q2) cw[q2] = 0;
-            } else {
-              const V4<S> co = sm.st.col[j];
-              const S w = mul_rn(a, T);
-              const S gdc = mypix.x * co.x + mypix.y * co.y + mypix.z * co.z;
-              P += gdc * w;
-              const S d_alpha = gdc * T - ((Ctot - P) + bterm) * inv_om(om);
-              Slot s;
-              s.x = raw < Const<S>::alpha_clamp() ? d_alpha * a : S(0);
-              s.y = w;
-              if constexpr (kOpacity) {
-                s.z = raw < Const<S>::alpha_clamp() ? d_alpha * ep : S(0);
-                s.w = S(0);
-              }
-              sm.slot[cnt][tid] = s;
-              inc[c] |= 1u << kk;
-              ++cnt;
-              T = test;
-            }
-          }
-        }
+    if (je < n) {
+      const uint32_t r0 = sm.off[je];
+      const uint32_t r1 = (je + 1 < n) ? sm.off[je + 1] : rec_end;
+      const uint32_t mid = r0 + ((r1 - r0 + 1) >> 1);
+      const uint32_t lo = half ? mid : r0, hi = half ? r1 : mid;
+      const V2<S> em = sm.st.mean[je];
+      const S ex0 = S(x0) - em.x, ey0 = S(y0) - em.y;
+      for (uint32_t r = lo; r < hi; ++r) {
+        const Rec s = sm.rec[r];
+        const int q = sm.rq[r];
+        const V4<S> pd = sm.pix[q];
+        const S dx = ex0 + S(q & 15), dy = ey0 + S(q >> 4);
+        const S dpx = s.x * dx, dpy = s.x * dy;
+        acc[0] += dpx;
+        acc[1] += dpy;
+        acc[2] += dpx * dx;
+        acc[3] += dpx * dy;
+        acc[4] += dpy * dy;
+        acc[5] += s.y * pd.x;
+        acc[6] += s.y * pd.y;
+        acc[7] += s.y * pd.z;
+        if constexpr (kOpacity) aop += s.z;
       }
-      {
-        uint32_t run = 0;
-#pragma unroll
-        for (int c = 0; c < kBwdBatch / 32; ++c) {
-          sm.incp[c][tid] = make_uint2(inc[c], run);
-          run += __popc(inc[c]);
-        }
-      }
-      bool left = false;
-#pragma unroll
-      for (int c = 0; c < kBwdBatch / 32; ++c) left |= cw[c] != 0;
-      const bool more = __syncthreads_or(left);
-      // ---- pass 2: my entry over its covered pixels (row pairs 2i + half) ----
-      if (je < n) {
-        const int cj = je >> 5, kj = je & 31;
-        const uint32_t below = (1u << kj) - 1u;
-#pragma unroll 1
-        for (int wi = half; wi < 8; wi += 2) {
-          uint32_t bits = sm.st.cov[je][wi];
-          while (bits) {
-            const int b = __ffs(bits) - 1;
-            bits &= bits - 1;
-            const int q = wi * 32 + b;   // tile pixel (= its thread index)
-            const uint2 ip = sm.incp[cj][q];
-            if (!((ip.x >> kj) & 1u)) continue;
-            const int idx = __popc(ip.x & below) + (int)ip.y;
-            const Slot s = sm.slot[idx][q];
-            const V4<S> pd = sm.pix[q];
-            const S dx = sub_rn(S(x0 + (q & 15)), em.x), dy = sub_rn(S(y0 + (q >> 4)), em.y);
-            const S dpx = s.x * dx, dpy = s.x * dy;
-            acc[0] += dpx;
-            acc[1] += dpy;
-            acc[2] += dpx * dx;
-            acc[3] += dpx * dy;
-            acc[4] += dpy * dy;
-            acc[5] += s.y * pd.x;
-            acc[6] += s.y * pd.y;
-            acc[7] += s.y * pd.z;
-            if constexpr (kOpacity) aop += s.z;
-          }
-        }
-      }
-      __syncthreads();
-      if (!more) break;
     }
     // combine the two halves (fixed order) and store at the pre-sort slot
 #pragma unroll
@@ -824,6 +855,7 @@ __global__ void __launch_bounds__(kBlendThreads) blend_backward(BlendArgs<S> p) 
       dst[1] = hi;
       if (kOpacity) p.partial_op[slot] = aop;
     }
+    base += (uint32_t)n;
   }
   // the tile finished early: entries never loaded still own a partial slot,
   // which must hold zeros (every slot is written exactly once)
