@@ -618,23 +618,45 @@ __global__ void __launch_bounds__(kBlendThreads) blend_forward(BlendArgs<S> p) {
     __syncthreads();
     BitWalk it;
     it.start<kFwdBatch>(sm.tw, n, done);
-    for (int j; (j = it.next<kFwdBatch>(sm.tw)) >= 0;) {
-      const V2<S> m = sm.mean[j];
+    // two candidates per trip: their alphas are independent, only the
+    // transmittance update is sequential (front-to-back order kept)
+    for (int j1; (j1 = it.next<kFwdBatch>(sm.tw)) >= 0;) {
+      const int j2 = it.next<kFwdBatch>(sm.tw);
+      const V2<S> m1 = sm.mean[j1];
       S ep, raw;
-      const S a = Eval<S>::alpha(sub_rn(fpx, m.x), sub_rn(fpy, m.y), sm.q[j], ep, raw);
-      if (a >= Const<S>::contrib_floor()) {
-        const S test = mul_rn(T, sub_rn(one, a));
+      const S a1 = Eval<S>::alpha(sub_rn(fpx, m1.x), sub_rn(fpy, m1.y), sm.q[j1], ep, raw);
+      S a2 = S(0);
+      if (j2 >= 0) {
+        const V2<S> m2 = sm.mean[j2];
+        a2 = Eval<S>::alpha(sub_rn(fpx, m2.x), sub_rn(fpy, m2.y), sm.q[j2], ep, raw);
+      }
+      if (a1 >= Const<S>::contrib_floor()) {
+        const S test = mul_rn(T, sub_rn(one, a1));
         if (test < Const<S>::t_stop()) {
           done = true;
           it.stop();
-        } else {
-          const V4<S> co = sm.col[j];
-          const S w = mul_rn(a, T);
-          ar += w * co.x;
-          ag += w * co.y;
-          ab += w * co.z;
-          T = test;
+          break;
         }
+        const V4<S> co = sm.col[j1];
+        const S w = mul_rn(a1, T);
+        ar += w * co.x;
+        ag += w * co.y;
+        ab += w * co.z;
+        T = test;
+      }
+      if (a2 >= Const<S>::contrib_floor()) {
+        const S test = mul_rn(T, sub_rn(one, a2));
+        if (test < Const<S>::t_stop()) {
+          done = true;
+          it.stop();
+          break;
+        }
+        const V4<S> co = sm.col[j2];
+        const S w = mul_rn(a2, T);
+        ar += w * co.x;
+        ag += w * co.y;
+        ab += w * co.z;
+        T = test;
       }
     }
     __syncthreads();
@@ -771,40 +793,59 @@ __global__ void __launch_bounds__(kBlendThreads) blend_backward(BlendArgs<S> p) 
     for (int c = 0; c < kBwdBatch / 32; ++c)
       if (c * 32 < n) sm.st.tw[c][tid] = transpose32(sm.st.cov[c * 32 + lane][warp_], lane);
     __syncthreads();
-    // ---- pass 1: my pixel ----
+    // ---- pass 1: my pixel (two candidates per trip, sequential T) ----
     {
       BitWalk it;
       it.start<kBwdBatch>(sm.st.tw, n, done);
-      for (int j; (j = it.next<kBwdBatch>(sm.st.tw)) >= 0;) {
-        const V2<S> m = sm.st.mean[j];
-        S ep, raw;
-        const S a = Eval<S>::alpha(sub_rn(fpx, m.x), sub_rn(fpy, m.y), sm.st.q[j], ep, raw);
-        if (a >= Const<S>::contrib_floor()) {
+      const uint32_t my_word_shift = 8 * (warp & 3);
+      for (int j1; (j1 = it.next<kBwdBatch>(sm.st.tw)) >= 0;) {
+        const int j2 = it.next<kBwdBatch>(sm.st.tw);
+        int js[2] = {j1, j2};
+        S as[2], eps[2], raws[2];
+        {
+          const V2<S> m = sm.st.mean[j1];
+          as[0] = Eval<S>::alpha(sub_rn(fpx, m.x), sub_rn(fpy, m.y), sm.st.q[j1], eps[0], raws[0]);
+        }
+        as[1] = S(0);
+        if (j2 >= 0) {
+          const V2<S> m = sm.st.mean[j2];
+          as[1] = Eval<S>::alpha(sub_rn(fpx, m.x), sub_rn(fpy, m.y), sm.st.q[j2], eps[1], raws[1]);
+        }
+        bool stop = false;
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int j = js[u];
+          const S a = as[u];
+          if (stop || !(a >= Const<S>::contrib_floor())) continue;
           const S om = sub_rn(one, a);
           const S test = mul_rn(T, om);
           if (test < Const<S>::t_stop()) {
-            done = true;
-            it.stop();
-          } else {
-            const V4<S> co = sm.st.col[j];
-            const S w = mul_rn(a, T);
-            const S gdc = mypix.x * co.x + mypix.y * co.y + mypix.z * co.z;
-            P += gdc * w;
-            const S d_alpha = gdc * T - ((Ctot - P) + bterm) * inv_om(om);
-            Rec s;
-            s.x = raw < Const<S>::alpha_clamp() ? d_alpha * a : S(0);
-            s.y = w;
-            if constexpr (kOpacity) {
-              s.z = raw < Const<S>::alpha_clamp() ? d_alpha * ep : S(0);
-              s.w = S(0);
-            }
-            const uint32_t pw = sm.pre[j][warp >> 2];
-            const uint32_t r = sm.off[j] + ((pw >> (8 * (warp & 3))) & 255u) +
-                               (uint32_t)__popc(sm.st.cov[j][warp] & lt);
-            sm.rec[r] = s;
-            sm.rq[r] = (uint8_t)tid;
-            T = test;
+            stop = true;
+            continue;
           }
+          const V4<S> co = sm.st.col[j];
+          const S w = mul_rn(a, T);
+          const S gdc = mypix.x * co.x + mypix.y * co.y + mypix.z * co.z;
+          P += gdc * w;
+          const S d_alpha = gdc * T - ((Ctot - P) + bterm) * inv_om(om);
+          Rec s;
+          s.x = raws[u] < Const<S>::alpha_clamp() ? d_alpha * a : S(0);
+          s.y = w;
+          if constexpr (kOpacity) {
+            s.z = raws[u] < Const<S>::alpha_clamp() ? d_alpha * eps[u] : S(0);
+            s.w = S(0);
+          }
+          const uint32_t pw = sm.pre[j][warp >> 2];
+          const uint32_t r = sm.off[j] + ((pw >> my_word_shift) & 255u) +
+                             (uint32_t)__popc(sm.st.cov[j][warp] & lt);
+          sm.rec[r] = s;
+          sm.rq[r] = (uint8_t)tid;
+          T = test;
+        }
+        if (stop) {
+          done = true;
+          it.stop();
+          break;
         }
       }
     }

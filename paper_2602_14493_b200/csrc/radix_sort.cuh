@@ -129,6 +129,7 @@ __global__ void __launch_bounds__(kSortThreads) radix_downsweep(
   const uint32_t base = blockIdx.x * (uint32_t)kSortTile;
   if (base >= n) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool trivial = __syncthreads_or(totals[tid] == n);
   for (int i = tid; i < kSortWarps * 256; i += kSortThreads) (&wc[0][0])[i] = 0;
   uint32_t ex = block_exclusive_scan_256(totals[tid], sw, nullptr);
   dbase[tid] = ex + hist[(size_t)tid * nblocks + blockIdx.x];
@@ -138,13 +139,30 @@ __global__ void __launch_bounds__(kSortThreads) radix_downsweep(
   K key[kSortPerThread];
   uint32_t val[kSortPerThread];
   uint32_t rank[kSortPerThread];
+  // all loads first (independent, in flight together), then the rounds
+#pragma unroll
+  for (int r = 0; r < kSortPerThread; ++r) {
+    const uint32_t idx = seg + r * 32 + lane;
+    key[r] = idx < n ? kin[idx] : K(0);
+    val[r] = idx < n ? vin[idx] : 0u;
+  }
+  // a pass whose digit is the same for every key is the identity permutation
+  if (trivial) {
+#pragma unroll
+    for (int r = 0; r < kSortPerThread; ++r) {
+      const uint32_t idx = seg + r * 32 + lane;
+      if (idx < n) {
+        kout[idx] = key[r];
+        vout[idx] = val[r];
+      }
+    }
+    return;
+  }
   const unsigned lt = lanemask_lt_sort();
 #pragma unroll
   for (int r = 0; r < kSortPerThread; ++r) {
     const uint32_t idx = seg + r * 32 + lane;
     const bool valid = idx < n;
-    key[r] = valid ? kin[idx] : K(0);
-    val[r] = valid ? vin[idx] : 0u;
     const uint32_t d = valid ? ((uint32_t)(key[r] >> shift) & 255u) : 256u;
     const unsigned peers = __match_any_sync(0xffffffffu, d);
     const uint32_t cnt = valid ? wc[warp][d] : 0u;

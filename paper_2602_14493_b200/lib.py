@@ -12,7 +12,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgmr.so")
+LIB_PATH = os.environ.get("GMR_LIB_PATH") or os.path.join(_HERE, "libgmr.so")
 
 GMR_OK = 0
 GMR_EINVAL = -1
