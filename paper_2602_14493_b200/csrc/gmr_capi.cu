@@ -198,18 +198,12 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
   }
   scan_top<<<1, 256, 0, st>>>(bsum, nb, dst, (unsigned long long)L.ecap, nent);
   GMR_LAUNCHED();
-  if (items) {
-    scan_apply<<<nb, 256, 0, st>>>(order, count, items, bsum, at<uint32_t>(ws, L.offs),
-                                   at<uint32_t>(ws, L.entry_off));
-    GMR_LAUNCHED();
-  }
   uint32_t* ek[2] = {at<uint32_t>(ws, L.ekey[0]), at<uint32_t>(ws, L.ekey[1])};
   uint32_t* ev[2] = {at<uint32_t>(ws, L.eval[0]), at<uint32_t>(ws, L.eval[1])};
   if (items) {
-    emit_entries<<<grid_for(items, 256), 256, 0, st>>>(order, count, at<uint32_t>(ws, L.offs),
-                                                       at<uint2>(ws, L.rect), items,
-                                                       (uint32_t)L.faces, L.tiles_x, (uint32_t)L.tiles,
-                                                       nent, ek[0], ev[0]);
+    scan_emit<<<nb, 256, 0, st>>>(order, count, at<uint2>(ws, L.rect), items, bsum, (uint32_t)L.faces,
+                                  L.tiles_x, (uint32_t)L.tiles, nent, at<uint32_t>(ws, L.entry_off), ek[0],
+                                  ev[0]);
     GMR_LAUNCHED();
   }
   delete emit_scope;

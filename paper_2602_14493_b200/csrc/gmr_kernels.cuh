@@ -2,7 +2,7 @@
 //
 //   K1 mesh_to_splats      convert.py:239-276,321-326 + render.py:103-145
 //   K1' pack_splats        render.py:168-188 (rasterize() stage input)
-//   K2 depth sort -> count scan -> emit_entries -> tile sort -> tile_ranges
+//   K2 depth sort -> count scan + entry emission -> tile sort -> tile_ranges
 //                          render.py:200-229 (_RasterPlan)
 //   K3 blend_forward       render.py:244-291
 //   K4 blend_backward      render.py:294-361
@@ -308,15 +308,14 @@ __global__ void __launch_bounds__(256) pack_splats(PackArgs<S> p) {
 // K2: counts in depth order -> offsets -> entries -> (view, tile) sort -> ranges
 // ---------------------------------------------------------------------------
 
-constexpr int kScanTile = 4096;
+constexpr int kScanTile = 256;   // one depth-sorted splat per thread
 
 __global__ void __launch_bounds__(256) scan_reduce(const uint32_t* __restrict__ order,
                                                   const uint32_t* __restrict__ count, uint32_t n,
                                                   uint32_t* __restrict__ bsum) {
   __shared__ uint32_t sw[8];
-  const uint32_t base = blockIdx.x * (uint32_t)kScanTile;
-  uint32_t s = 0;
-  for (uint32_t i = base + threadIdx.x; i < min(n, base + kScanTile); i += 256) s += count[order[i]];
+  const uint32_t i = blockIdx.x * (uint32_t)kScanTile + threadIdx.x;
+  const uint32_t s = i < n ? count[order[i]] : 0u;
   uint32_t tot;
   block_exclusive_scan_256(s, sw, &tot);
   if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
@@ -342,64 +341,35 @@ __global__ void __launch_bounds__(256) scan_top(uint32_t* __restrict__ bsum, int
   }
 }
 
-__global__ void __launch_bounds__(256) scan_apply(const uint32_t* __restrict__ order,
-                                                 const uint32_t* __restrict__ count, uint32_t n,
-                                                 const uint32_t* __restrict__ bsum,
-                                                 uint32_t* __restrict__ offs_sorted,
-                                                 uint32_t* __restrict__ entry_off) {
+// Fused offsets + emission: per depth-sorted splat (4 per thread, block
+// scan + the block's carry), record its first entry slot `entry_off[item]`
+// and write its tile entries row-major over its rectangle (render.py:218-226):
+// key = view * T + tile, value = item.  Skipped when the entries overflow.
+__global__ void __launch_bounds__(256) scan_emit(const uint32_t* __restrict__ order,
+                                                const uint32_t* __restrict__ count,
+                                                const uint2* __restrict__ rect, uint32_t n,
+                                                const uint32_t* __restrict__ bsum,
+                                                uint32_t items_per_view, int tiles_x,
+                                                uint32_t tiles_per_view,
+                                                const uint32_t* __restrict__ n_entries,
+                                                uint32_t* __restrict__ entry_off,
+                                                uint32_t* __restrict__ key, uint32_t* __restrict__ val) {
   __shared__ uint32_t sw[8];
-  const uint32_t base = blockIdx.x * (uint32_t)kScanTile;
-  uint32_t carry = bsum[blockIdx.x];
-  for (uint32_t b0 = base; b0 < min(n, base + kScanTile); b0 += 256 * 4) {
-    uint32_t it[4], c[4], s = 0;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      uint32_t i = b0 + threadIdx.x * 4 + k;
-      bool ok = i < n && i < base + kScanTile;
-      it[k] = ok ? order[i] : 0u;
-      c[k] = ok ? count[it[k]] : 0u;
-      s += c[k];
-    }
-    uint32_t tot;
-    uint32_t run = carry + block_exclusive_scan_256(s, sw, &tot);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      uint32_t i = b0 + threadIdx.x * 4 + k;
-      if (i < n && i < base + kScanTile) {
-        offs_sorted[i] = run;
-        entry_off[it[k]] = run;
-      }
-      run += c[k];
-    }
-    carry += tot;
-  }
-}
-
-// one thread per depth-sorted splat: write its tile entries row-major over
-// its rectangle (render.py:218-226); key = view * T + tile, value = item
-__global__ void __launch_bounds__(256) emit_entries(const uint32_t* __restrict__ order,
-                                                   const uint32_t* __restrict__ count,
-                                                   const uint32_t* __restrict__ offs_sorted,
-                                                   const uint2* __restrict__ rect, uint32_t n,
-                                                   uint32_t items_per_view, int tiles_x,
-                                                   uint32_t tiles_per_view,
-                                                   const uint32_t* __restrict__ n_entries,
-                                                   uint32_t* __restrict__ key,
-                                                   uint32_t* __restrict__ val) {
-  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= n || *n_entries == 0) return;
-  const uint32_t item = order[r];
-  const uint32_t cnt = count[item];
-  if (!cnt) return;
-  const uint32_t off = offs_sorted[r];
+  const uint32_t i = blockIdx.x * (uint32_t)kScanTile + threadIdx.x;
+  const uint32_t item = i < n ? order[i] : 0u;
+  const uint32_t c = i < n ? count[item] : 0u;
+  const uint32_t run = bsum[blockIdx.x] + block_exclusive_scan_256(c, sw, nullptr);
+  if (i >= n) return;
+  entry_off[item] = run;
+  if (!c || *n_entries == 0) return;
   const uint2 rc = rect[item];
   const int tx0 = rc.x & 0xffff, ty0 = rc.x >> 16, tx1 = rc.y & 0xffff;
-  const int nx = tx1 - tx0 + 1;
   const uint32_t vbase = (item / items_per_view) * tiles_per_view;
-  for (uint32_t k = 0; k < cnt; ++k) {
-    const int ty = ty0 + (int)k / nx, tx = tx0 + (int)k % nx;
-    key[off + k] = vbase + (uint32_t)(ty * tiles_x + tx);
-    val[off + k] = item;
+  int tx = tx0, ty = ty0;
+  for (uint32_t e = 0; e < c; ++e) {
+    key[run + e] = vbase + (uint32_t)(ty * tiles_x + tx);
+    val[run + e] = item;
+    if (++tx > tx1) { tx = tx0; ++ty; }
   }
 }
 

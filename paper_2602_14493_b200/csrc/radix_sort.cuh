@@ -118,46 +118,52 @@ __global__ void __launch_bounds__(kSortThreads) radix_scan(uint32_t* __restrict_
 }
 
 template <typename K>
-__global__ void __launch_bounds__(kSortThreads) radix_downsweep(
+struct DownSmem {
+  uint32_t wc[kSortWarps][256];   // per-warp digit counts -> exclusive prefixes
+  uint32_t boff[257];             // block-local start of each digit
+  uint32_t gbase[256];            // global start of each digit for this block
+  uint32_t sw[kSortWarps];
+  K keys[kSortTile];              // the block's items in sorted (stable) order
+  uint32_t vals[kSortTile];
+};
+
+// Stable in-block ranking (warp match_any, warps in order), the block's
+// items staged in smem in sorted order, then written out in coalesced runs
+// per digit.
+template <typename K>
+__global__ void __launch_bounds__(kSortThreads, 3) radix_downsweep(
     const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __restrict__ kout,
     uint32_t* __restrict__ vout, const uint32_t* n_dev, uint32_t n_host, int shift,
     const uint32_t* __restrict__ hist, const uint32_t* __restrict__ totals, int nblocks) {
-  __shared__ uint32_t wc[kSortWarps][256];
-  __shared__ uint32_t dbase[256];
-  __shared__ uint32_t sw[kSortWarps];
+  extern __shared__ __align__(16) unsigned char dsm_raw[];
+  DownSmem<K>& sm = *reinterpret_cast<DownSmem<K>*>(dsm_raw);
   const uint32_t n = sort_count(n_dev, n_host);
   const uint32_t base = blockIdx.x * (uint32_t)kSortTile;
   if (base >= n) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const bool trivial = __syncthreads_or(totals[tid] == n);
-  for (int i = tid; i < kSortWarps * 256; i += kSortThreads) (&wc[0][0])[i] = 0;
-  uint32_t ex = block_exclusive_scan_256(totals[tid], sw, nullptr);
-  dbase[tid] = ex + hist[(size_t)tid * nblocks + blockIdx.x];
-  __syncthreads();
-
+  const uint32_t cnt_blk = min((uint32_t)kSortTile, n - base);
+  const uint32_t tot_d = totals[tid];
+  const bool trivial = __syncthreads_or(tot_d == n);
   const uint32_t seg = base + (uint32_t)warp * (kSortPerThread * 32);
+  // a pass whose digit is the same for every key is the identity permutation
+  if (trivial) {
+    for (uint32_t i = base + tid; i < base + cnt_blk; i += kSortThreads) {
+      kout[i] = kin[i];
+      vout[i] = vin[i];
+    }
+    return;
+  }
   K key[kSortPerThread];
-  uint32_t val[kSortPerThread];
-  uint32_t rank[kSortPerThread];
-  // all loads first (independent, in flight together), then the rounds
 #pragma unroll
   for (int r = 0; r < kSortPerThread; ++r) {
     const uint32_t idx = seg + r * 32 + lane;
     key[r] = idx < n ? kin[idx] : K(0);
-    val[r] = idx < n ? vin[idx] : 0u;
   }
-  // a pass whose digit is the same for every key is the identity permutation
-  if (trivial) {
-#pragma unroll
-    for (int r = 0; r < kSortPerThread; ++r) {
-      const uint32_t idx = seg + r * 32 + lane;
-      if (idx < n) {
-        kout[idx] = key[r];
-        vout[idx] = val[r];
-      }
-    }
-    return;
-  }
+  for (int i = tid; i < kSortWarps * 256; i += kSortThreads) (&sm.wc[0][0])[i] = 0;
+  const uint32_t ex = block_exclusive_scan_256(tot_d, sm.sw, nullptr);
+  sm.gbase[tid] = ex + hist[(size_t)tid * nblocks + blockIdx.x];
+  __syncthreads();
+  uint16_t rank[kSortPerThread];
   const unsigned lt = lanemask_lt_sort();
 #pragma unroll
   for (int r = 0; r < kSortPerThread; ++r) {
@@ -165,21 +171,26 @@ __global__ void __launch_bounds__(kSortThreads) radix_downsweep(
     const bool valid = idx < n;
     const uint32_t d = valid ? ((uint32_t)(key[r] >> shift) & 255u) : 256u;
     const unsigned peers = __match_any_sync(0xffffffffu, d);
-    const uint32_t cnt = valid ? wc[warp][d] : 0u;
-    rank[r] = cnt + __popc(peers & lt);
+    const uint32_t c = valid ? sm.wc[warp][d] : 0u;
+    rank[r] = (uint16_t)(c + __popc(peers & lt));
     __syncwarp();
-    if (valid && (lt & peers) == 0) wc[warp][d] = cnt + __popc(peers);
+    if (valid && (lt & peers) == 0) sm.wc[warp][d] = c + __popc(peers);
     __syncwarp();
   }
   __syncthreads();
   {
+    // digit tid: per-warp exclusive prefixes and the block-local digit start
     uint32_t run = 0;
 #pragma unroll
     for (int w = 0; w < kSortWarps; ++w) {
-      uint32_t c = wc[w][tid];
-      wc[w][tid] = run;
+      const uint32_t c = sm.wc[w][tid];
+      sm.wc[w][tid] = run;
       run += c;
     }
+    uint32_t tot;
+    const uint32_t off = block_exclusive_scan_256(run, sm.sw, &tot);
+    sm.boff[tid] = off;
+    if (tid == 0) sm.boff[256] = tot;
   }
   __syncthreads();
 #pragma unroll
@@ -187,10 +198,19 @@ __global__ void __launch_bounds__(kSortThreads) radix_downsweep(
     const uint32_t idx = seg + r * 32 + lane;
     if (idx < n) {
       const uint32_t d = (uint32_t)(key[r] >> shift) & 255u;
-      const uint32_t pos = dbase[d] + wc[warp][d] + rank[r];
-      kout[pos] = key[r];
-      vout[pos] = val[r];
+      const uint32_t lp = sm.boff[d] + sm.wc[warp][d] + rank[r];
+      sm.keys[lp] = key[r];
+      sm.vals[lp] = vin[idx];
     }
+  }
+  __syncthreads();
+  // coalesced write-out: local position i -> digit run -> global slot
+  for (uint32_t i = tid; i < cnt_blk; i += kSortThreads) {
+    const K k = sm.keys[i];
+    const uint32_t d = (uint32_t)(k >> shift) & 255u;
+    const uint32_t pos = sm.gbase[d] + (i - sm.boff[d]);
+    kout[pos] = k;
+    vout[pos] = sm.vals[i];
   }
 }
 
@@ -205,14 +225,19 @@ inline int radix_sort_pairs(K* keys[2], uint32_t* vals[2], const uint32_t* n_dev
   const int nblocks = (int)((capacity + kSortTile - 1) / kSortTile);
   if (nblocks == 0 || bits <= 0) return 0;
   uint32_t* totals = hist + (size_t)256 * nblocks;
+  static bool attr_set = false;   // per K instantiation
+  if (!attr_set) {
+    cudaFuncSetAttribute(radix_downsweep<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(DownSmem<K>));
+    attr_set = true;
+  }
   int cur = 0;
   for (int shift = 0; shift < bits; shift += 8) {
     radix_upsweep<K><<<nblocks, kSortThreads, 0, stream>>>(keys[cur], n_dev, n_host, shift, hist,
                                                            nblocks);
     radix_scan<<<256, kSortThreads, 0, stream>>>(hist, totals, nblocks);
-    radix_downsweep<K><<<nblocks, kSortThreads, 0, stream>>>(keys[cur], vals[cur], keys[cur ^ 1],
-                                                             vals[cur ^ 1], n_dev, n_host, shift,
-                                                             hist, totals, nblocks);
+    radix_downsweep<K><<<nblocks, kSortThreads, sizeof(DownSmem<K>), stream>>>(
+        keys[cur], vals[cur], keys[cur ^ 1], vals[cur ^ 1], n_dev, n_host, shift, hist, totals, nblocks);
     cur ^= 1;
   }
   return cur;

@@ -60,8 +60,10 @@ class _Capacity:
         self._cap[key] = int(needed * 1.25) + 4096
         return self._cap[key]
 
-    def note(self, key, cap):
-        self._cap[key] = cap
+    def note(self, key, cap, used):
+        # keep ~25% headroom over what the last call needed
+        want = int(used * 1.25) + 4096
+        self._cap[key] = want if (cap > 2 * want or cap < want) else cap
 
 
 _capacity = _Capacity()
@@ -135,7 +137,7 @@ def render_forward(pos, col, faces, cams, width, height, background, rescale=Tru
                                        _ptr(alpha), _ptr(ws), nb.value, cap, _stream()))
         st, code = _status_or_raise(ws, "mesh", item_to_index)
         if code == L.GMR_OK:
-            _capacity.note(key, cap)
+            _capacity.note(key, cap, st.entries)
             return rgb, alpha, ForwardState(ws, cap, raster, cam_arr, B, st.entries, st.kept)
         cap = _capacity.grow(key, st.entries)
     raise RuntimeError("tile-entry capacity did not converge")
@@ -217,7 +219,7 @@ def rasterize_forward(mean2d, cov2d, depth, color, opacity, width, height, backg
                                           _ptr(ws), nb.value, cap, _stream()))
         st, code = _status_or_raise(ws, "splats")
         if code == L.GMR_OK:
-            _capacity.note(key, cap)
+            _capacity.note(key, cap, st.entries)
             return rgb, alpha, ForwardState(ws, cap, raster, None, 1, st.entries, st.kept)
         cap = _capacity.grow(key, st.entries)
     raise RuntimeError("tile-entry capacity did not converge")
