@@ -1,0 +1,127 @@
+"""Stress the blend kernels' control paths against the oracle (float64):
+dynamic batch cuts (huge splats covering whole tiles), early termination
+inside a batch (stacks of opaque splats), partial tiles, multi-view batches
+(one device call == sum of single-view reference calls) and determinism."""
+
+import numpy as np
+import pytest
+
+import golden_cases as gc
+from oracle import gmr_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return float(np.abs(a - b).max() / max(1.0, np.abs(b).max()))
+
+
+def _splat_scene(rng, k, lo, hi, cov_scale, opacity, W, H):
+    mean2d = rng.uniform(lo, hi, size=(k, 2))
+    cov = []
+    for _ in range(k):
+        a = rng.normal(size=(2, 2))
+        cov.append(a @ a.T * cov_scale + np.eye(2) * 0.5)
+    return dict(mean2d=mean2d, cov2d=np.array(cov), depth=rng.uniform(1, 5, size=k),
+                color=rng.random((k, 3)), opacity=np.full(k, opacity) if np.isscalar(opacity) else opacity,
+                source=np.arange(k), g_rgb=rng.normal(size=(H, W, 3)), g_alpha=rng.normal(size=(H, W)))
+
+
+def _check_splats(gmr, case, W, H, bg=(0.2, 0.1, 0.3)):
+    from paper_2602_14493_b200.camera import Camera
+    cam = Camera(rotation=np.eye(3), translation=np.zeros(3), fx=40, fy=40, cx=W / 2, cy=H / 2, width=W, height=H)
+    s = orc.splats_from_arrays(case["mean2d"], case["cov2d"], case["depth"], case["color"], case["opacity"])
+    rgb, alpha = orc.composite(s, W, H, bg)
+    gm, gcv, gcol, gop = orc.composite_backward(s, W, H, bg, case["g_rgb"], case["g_alpha"])
+    sp = [gmr.Splat2D(m, c, float(d), col, float(o), int(i)) for m, c, d, col, o, i in
+          zip(case["mean2d"], case["cov2d"], case["depth"], case["color"], case["opacity"], case["source"])]
+    out = gmr.rasterize(sp, cam, bg)
+    assert np.abs(out.rgb - rgb).max() <= 1e-10
+    assert np.abs(out.alpha - alpha).max() <= 1e-10
+    g = gmr.rasterize_backward(sp, cam, out, case["g_rgb"], case["g_alpha"])
+    for a, b in zip(g, (gm, gcv, gcol, gop)):
+        assert rel(a, b) <= 1e-8
+
+
+def test_huge_splats_force_batch_cuts(gmr):
+    """Splats covering whole tiles: a staged batch's coverage records exceed
+    shared memory, so the backward takes fewer entries per batch."""
+    rng = np.random.default_rng(1)
+    case = _splat_scene(rng, 40, 4, 44, 60.0, rng.uniform(0.02, 0.2, 40), 48, 40)
+    _check_splats(gmr, case, 48, 40)
+
+
+def test_opaque_stacks_terminate_inside_batches(gmr):
+    """60 nearly opaque splats stacked on a few pixels: transmittance drops
+    below 1e-4 mid-list, later entries are skipped and the tail of the tile
+    list never loads (zero partials)."""
+    rng = np.random.default_rng(2)
+    k = 300
+    case = _splat_scene(rng, k, 10, 22, 1.0, 0.97, 32, 32)
+    case["mean2d"][:60] = 16.0 + rng.normal(scale=0.3, size=(60, 2))
+    _check_splats(gmr, case, 32, 32)
+
+
+def test_many_low_opacity_layers(gmr):
+    rng = np.random.default_rng(3)
+    case = _splat_scene(rng, 500, 2, 30, 3.0, 0.05, 32, 32)
+    _check_splats(gmr, case, 32, 32)
+
+
+def test_batched_views_equal_sum_of_single_views(gmr):
+    """One device call over 5 views == the reference's serial view loop."""
+    from paper_2602_14493_b200 import engine
+    import torch
+    case = gc.c1_case()
+    mesh = gmr.TriangleMesh(case["vertices"], case["facets"], case["colors"])
+    cams = gmr.hemisphere_cameras(5, 2.6, (64, 48))
+    rng = np.random.default_rng(4)
+    g_rgb = rng.normal(size=(5, 48, 64, 3))
+    g_a = rng.normal(size=(5, 48, 64))
+    pos, col, faces = gmr.api._device_mesh(mesh, np.float64)
+    rgb, alpha, st = engine.render_forward(pos, col, faces, cams, 64, 48, (0.1, 0.2, 0.3))
+    gp, gcol = engine.render_backward(st, pos, col, faces, rgb, torch.as_tensor(g_rgb).cuda(),
+                                      torch.as_tensor(g_a).cuda())
+    ogv = np.zeros_like(mesh.vertices)
+    ogc = np.zeros_like(mesh.vertices)
+    for v, cam in enumerate(cams):
+        r, a, ctx = orc.render(mesh.vertices, mesh.facets, mesh.colors, cam, (0.1, 0.2, 0.3))
+        assert np.abs(rgb[v].cpu().numpy() - r).max() <= 1e-10
+        x, y = orc.render_grad(ctx, g_rgb[v], g_a[v])
+        ogv += x
+        ogc += y
+    assert rel(gp.cpu().numpy(), ogv) <= 1e-8
+    assert rel(gcol.cpu().numpy(), ogc) <= 1e-8
+
+
+def test_backward_is_bit_deterministic_f32(gmr):
+    from paper_2602_14493_b200 import engine, make_geodesic_sphere, hemisphere_cameras
+    import torch
+    m = make_geodesic_sphere(20, seed=2)
+    cams = hemisphere_cameras(3, 3.0, (160, 120))
+    pos, col, faces = gmr.api._device_mesh(m, np.float32)
+    g = torch.randn((3, 120, 160, 3), device="cuda")
+    ga = torch.randn((3, 120, 160), device="cuda")
+    outs = []
+    for _ in range(3):
+        rgb, alpha, st = engine.render_forward(pos, col, faces, cams, 160, 120, (0.1, 0.1, 0.1))
+        outs.append([x.cpu().numpy() for x in (rgb, alpha) + engine.render_backward(st, pos, col, faces, rgb, g, ga)])
+    for o in outs[1:]:
+        for a, b in zip(o, outs[0]):
+            np.testing.assert_array_equal(a, b)
+
+
+def test_sharded_image_loss_gpu_local_fn(gmr):
+    """dist.sharded_image_loss with the GPU local_fn (world size 1) == the
+    reference's total_loss image terms (golden)."""
+    from paper_2602_14493_b200 import dist
+    case, g = gc.loss_case(), gc.load("loss_octa_3views_16")
+    mesh = gmr.TriangleMesh(case["vertices"], case["facets"], case["colors"])
+    fn = dist.gpu_local_image_loss(mesh, background=case["background"], dtype=np.float64)
+    c, s, gp, gcol = dist.sharded_image_loss(fn, case["cameras"], case["target_rgb"], case["target_mask"],
+                                            len(case["vertices"]), device="cuda")
+    assert c == pytest.approx(float(g["color"]), rel=1e-10)
+    assert s == pytest.approx(float(g["silhouette"]), rel=1e-10)
+    assert rel(gp.cpu().numpy(), g["grad_v"]) <= 1e-8
+    assert rel(gcol.cpu().numpy(), g["grad_c"]) <= 1e-8
