@@ -202,8 +202,16 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
   uint32_t* ev[2] = {at<uint32_t>(ws, L.eval[0]), at<uint32_t>(ws, L.eval[1])};
   if (items) {
     scan_emit<<<nb, 256, 0, st>>>(order, count, at<uint2>(ws, L.rect), items, bsum, (uint32_t)L.faces,
-                                  L.tiles_x, (uint32_t)L.tiles, nent, at<uint32_t>(ws, L.entry_off), ek[0],
-                                  ev[0]);
+                                  L.tiles_x, (uint32_t)L.tiles, nent, ek[0], ev[0]);
+    GMR_LAUNCHED();
+    // face-major partial offsets (bsum and offs are free again here)
+    const int fb = (int)((L.faces + 255) / 256);
+    face_counts<<<fb, 256, 0, st>>>(count, (uint32_t)L.faces, L.views, at<uint32_t>(ws, L.offs), bsum);
+    GMR_LAUNCHED();
+    scan_inplace<<<1, 256, 0, st>>>(bsum, fb);
+    GMR_LAUNCHED();
+    item_offsets<<<fb, 256, 0, st>>>(count, (uint32_t)L.faces, L.views, at<uint32_t>(ws, L.offs), bsum,
+                                     at<uint32_t>(ws, L.entry_off));
     GMR_LAUNCHED();
   }
   delete emit_scope;

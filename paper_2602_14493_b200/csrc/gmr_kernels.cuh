@@ -341,10 +341,10 @@ __global__ void __launch_bounds__(256) scan_top(uint32_t* __restrict__ bsum, int
   }
 }
 
-// Fused offsets + emission: per depth-sorted splat (4 per thread, block
-// scan + the block's carry), record its first entry slot `entry_off[item]`
-// and write its tile entries row-major over its rectangle (render.py:218-226):
-// key = view * T + tile, value = item.  Skipped when the entries overflow.
+// Entry emission: per depth-sorted splat (one per thread; block scan + the
+// block's carry from scan_top), write its tile entries row-major over its
+// rectangle (render.py:218-226): key = view * T + tile, value = item.
+// Skipped when the entries overflow.
 __global__ void __launch_bounds__(256) scan_emit(const uint32_t* __restrict__ order,
                                                 const uint32_t* __restrict__ count,
                                                 const uint2* __restrict__ rect, uint32_t n,
@@ -352,16 +352,13 @@ __global__ void __launch_bounds__(256) scan_emit(const uint32_t* __restrict__ or
                                                 uint32_t items_per_view, int tiles_x,
                                                 uint32_t tiles_per_view,
                                                 const uint32_t* __restrict__ n_entries,
-                                                uint32_t* __restrict__ entry_off,
                                                 uint32_t* __restrict__ key, uint32_t* __restrict__ val) {
   __shared__ uint32_t sw[8];
   const uint32_t i = blockIdx.x * (uint32_t)kScanTile + threadIdx.x;
   const uint32_t item = i < n ? order[i] : 0u;
   const uint32_t c = i < n ? count[item] : 0u;
   const uint32_t run = bsum[blockIdx.x] + block_exclusive_scan_256(c, sw, nullptr);
-  if (i >= n) return;
-  entry_off[item] = run;
-  if (!c || *n_entries == 0) return;
+  if (i >= n || !c || *n_entries == 0) return;
   const uint2 rc = rect[item];
   const int tx0 = rc.x & 0xffff, ty0 = rc.x >> 16, tx1 = rc.y & 0xffff;
   const uint32_t vbase = (item / items_per_view) * tiles_per_view;
@@ -370,6 +367,51 @@ __global__ void __launch_bounds__(256) scan_emit(const uint32_t* __restrict__ or
     key[run + e] = vbase + (uint32_t)(ty * tiles_x + tx);
     val[run + e] = item;
     if (++tx > tx1) { tx = tx0; ++ty; }
+  }
+}
+
+// Face-major layout of the per-entry gradient partials: all entries of face
+// f (views 0..B-1, each row-major over its rectangle) are contiguous at
+// entry_off[v * F + f], so K5 streams one range per face.
+__global__ void __launch_bounds__(256) face_counts(const uint32_t* __restrict__ count, uint32_t F, int B,
+                                                  uint32_t* __restrict__ face_local,
+                                                  uint32_t* __restrict__ bsum) {
+  __shared__ uint32_t sw[8];
+  const uint32_t f = blockIdx.x * 256u + threadIdx.x;
+  uint32_t s = 0;
+  if (f < F)
+    for (int v = 0; v < B; ++v) s += count[(size_t)v * F + f];
+  uint32_t tot;
+  const uint32_t ex = block_exclusive_scan_256(s, sw, &tot);
+  if (f < F) face_local[f] = ex;
+  if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
+}
+
+// single-block exclusive scan in place
+__global__ void __launch_bounds__(256) scan_inplace(uint32_t* __restrict__ a, int n) {
+  __shared__ uint32_t sw[8];
+  uint32_t carry = 0;
+  for (int base = 0; base < n; base += 256) {
+    const int i = base + threadIdx.x;
+    const uint32_t v = i < n ? a[i] : 0u;
+    uint32_t tot;
+    const uint32_t ex = block_exclusive_scan_256(v, sw, &tot);
+    if (i < n) a[i] = carry + ex;
+    carry += tot;
+  }
+}
+
+__global__ void __launch_bounds__(256) item_offsets(const uint32_t* __restrict__ count, uint32_t F, int B,
+                                                   const uint32_t* __restrict__ face_local,
+                                                   const uint32_t* __restrict__ bsum,
+                                                   uint32_t* __restrict__ entry_off) {
+  const uint32_t f = blockIdx.x * 256u + threadIdx.x;
+  if (f >= F) return;
+  uint32_t run = bsum[blockIdx.x] + face_local[f];
+  for (int v = 0; v < B; ++v) {
+    const size_t item = (size_t)v * F + f;
+    entry_off[item] = run;
+    run += count[item];
   }
 }
 
