@@ -44,6 +44,26 @@ def _device():
 
 
 _mesh_cache: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+_topo_cache: dict = {}   # id(facets array) -> (weakref to it, int32 faces on device, edges, CSR)
+
+
+def _facets_entry(facets):
+    """Per-topology device/host data, keyed by the facets array object (a
+    TriangleMesh rebuilt with new vertices, as in the fit loop, shares it)."""
+    key = id(facets)
+    hit = _topo_cache.get(key)
+    if hit is not None and hit[0]() is facets:
+        return hit[1]
+    dev = _device()
+    entry = {"faces": torch.as_tensor(np.array(facets, dtype=np.int32)).to(dev)}
+    try:
+        ref = weakref.ref(facets)
+    except TypeError:
+        return entry
+    if len(_topo_cache) > 64:
+        _topo_cache.clear()
+    _topo_cache[key] = (ref, entry)
+    return entry
 
 
 def _device_mesh(mesh, dtype):
@@ -58,10 +78,7 @@ def _device_mesh(mesh, dtype):
     if hit is None:
         pos = torch.as_tensor(np.array(mesh.vertices, dtype=np.float64), dtype=tdt).to(dev)
         col = torch.as_tensor(np.array(mesh.colors, dtype=np.float64), dtype=tdt).to(dev)
-        faces = per.get("faces")
-        if faces is None:
-            faces = torch.as_tensor(np.array(mesh.facets, dtype=np.int32)).to(dev)
-            per["faces"] = faces
+        faces = _facets_entry(mesh.facets)["faces"]
         hit = per[tdt] = (pos, col, faces)
     return hit
 
@@ -302,7 +319,16 @@ def silhouette_loss(alpha, mask):
 
 
 def _edges(facets):
-    return np.unique(np.sort(np.asarray(facets)[:, [0, 1, 1, 2, 2, 0]].reshape(-1, 2), axis=1), axis=0)
+    ent = _facets_entry(facets) if _cuda_ok() else {}
+    e = ent.get("edges")
+    if e is None:
+        e = np.unique(np.sort(np.asarray(facets)[:, [0, 1, 1, 2, 2, 0]].reshape(-1, 2), axis=1), axis=0)
+        ent["edges"] = e
+    return e
+
+
+def _cuda_ok():
+    return torch.cuda.is_available()
 
 
 def edge_length_loss(mesh, vertices=None):
@@ -325,9 +351,13 @@ def laplacian_loss(mesh, vertices=None):
     """losses.py:100-123 (uniform Laplacian regulariser)."""
     verts = np.asarray(mesh.vertices if vertices is None else vertices, dtype=np.float64)
     nv = len(verts)
-    e = _edges(mesh.facets) if len(mesh.facets) else np.zeros((0, 2), np.int64)
-    both = np.concatenate([e, e[:, ::-1]]) if len(e) else np.zeros((0, 2), np.int64)
-    both = both[np.lexsort((both[:, 1], both[:, 0]))]
+    ent = _facets_entry(mesh.facets) if _cuda_ok() else {}
+    both = ent.get("adjacency")
+    if both is None:
+        e = _edges(mesh.facets) if len(mesh.facets) else np.zeros((0, 2), np.int64)
+        both = np.concatenate([e, e[:, ::-1]]) if len(e) else np.zeros((0, 2), np.int64)
+        both = both[np.lexsort((both[:, 1], both[:, 0]))]
+        ent["adjacency"] = both
     deg = np.bincount(both[:, 0], minlength=nv).astype(np.float64)
     owner = both[:, 0]
     has = deg > 0
@@ -358,10 +388,10 @@ def total_loss(mesh, cameras: Sequence[Camera], target_rgb, target_mask, weights
     groups = {}
     for i, c in enumerate(cameras):
         groups.setdefault((c.width, c.height), []).append(i)
-    grad_v = np.zeros((len(mesh.vertices), 3))
-    grad_c = np.zeros((len(mesh.vertices), 3))
-    cval = np.zeros(n)
-    sval = np.zeros(n)
+    gp_acc = torch.zeros((len(mesh.vertices), 3), dtype=torch.float64, device=dev)
+    gc_acc = torch.zeros_like(gp_acc)
+    cv_acc = torch.zeros((), dtype=torch.float64, device=dev)
+    sv_acc = torch.zeros((), dtype=torch.float64, device=dev)
     bg = np.asarray(background, dtype=np.float64)
     for (w, h), idx in groups.items():
         cams = [cameras[i] for i in idx]
@@ -372,18 +402,24 @@ def total_loss(mesh, cameras: Sequence[Camera], target_rgb, target_mask, weights
             raise ValueError("shape mismatch between renders and targets")
         r64, a64 = rgb.double(), alpha.double()
         diff = r64 - t_rgb
-        cval[idx] = (diff * diff).mean(dim=(1, 2, 3)).cpu().numpy()
+        cv_acc += (diff * diff).mean(dim=(1, 2, 3)).sum()
         g_rgb = (2.0 / diff[0].numel()) * diff * (weights.color / n)
         p = a64.clamp(BCE_CLAMP, 1.0 - BCE_CLAMP)
-        sval[idx] = (-(t_m * torch.log(p) + (1.0 - t_m) * torch.log1p(-p))).mean(dim=(1, 2)).cpu().numpy()
+        sv_acc += (-(t_m * torch.log(p) + (1.0 - t_m) * torch.log1p(-p))).mean(dim=(1, 2)).sum()
         inside = (a64 > BCE_CLAMP) & (a64 < 1.0 - BCE_CLAMP)
         g_a = torch.where(inside, (-t_m / p + (1.0 - t_m) / (1.0 - p)) / a64[0].numel(),
                           torch.zeros_like(a64)) * (weights.silhouette / n)
         gp, gc = engine.render_backward(state, pos, col, faces, rgb, g_rgb.to(tdt), g_a.to(tdt))
-        grad_v += gp.double().cpu().numpy()
-        grad_c += gc.double().cpu().numpy()
-    color_val = float(cval.sum() / n)
-    sil_val = float(sval.sum() / n)
+        gp_acc += gp.double()
+        gc_acc += gc.double()
+    # one transfer for everything
+    flat = torch.cat([cv_acc.view(1), sv_acc.view(1), gp_acc.view(-1), gc_acc.view(-1)]).cpu().numpy()
+    cval_sum, sval_sum = flat[0], flat[1]
+    nv = len(mesh.vertices)
+    grad_v = flat[2:2 + 3 * nv].reshape(nv, 3).copy()
+    grad_c = flat[2 + 3 * nv:].reshape(nv, 3).copy()
+    color_val = float(cval_sum / n)
+    sil_val = float(sval_sum / n)
     edge_val, g_edge = edge_length_loss(mesh)
     lap_val, g_lap = laplacian_loss(mesh)
     grad_v += weights.edge * g_edge + weights.laplacian * g_lap

@@ -546,6 +546,16 @@ template <> struct Eval<float> {
   }
 };
 
+// Warm L2 with the records of the next batch while the current one is
+// processed: the gathers entry -> item -> record are otherwise exposed at
+// every batch start.
+template <typename S>
+__device__ __forceinline__ void prefetch_records(const BlendArgs<S>& p, uint32_t item, uint32_t vbase_item) {
+  if (item == 0xffffffffu) return;
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p.splat + item));
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p.col4 + (item - vbase_item)));
+}
+
 constexpr int kFwdBatch = 256;
 constexpr int kBwdBatch = 128;
 constexpr int kBwdSlots = 16;
@@ -628,6 +638,8 @@ __global__ void __launch_bounds__(kBlendThreads) blend_forward(BlendArgs<S> p) {
     const int n = (int)min((uint32_t)kFwdBatch, end - base);
     stage_batch<S, kFwdBatch>(p, sm, base, n, vbase_item, x0, y0);
     __syncthreads();
+    const uint32_t nxt_e = base + kFwdBatch + threadIdx.x;
+    const uint32_t nxt = nxt_e < end ? p.entry_item[nxt_e] : 0xffffffffu;
     BitWalk it;
     it.start<kFwdBatch>(sm.tw, n, done);
     // two candidates per trip: their alphas are independent, only the
@@ -671,6 +683,7 @@ __global__ void __launch_bounds__(kBlendThreads) blend_forward(BlendArgs<S> p) {
         T = test;
       }
     }
+    prefetch_records(p, nxt, vbase_item);
     __syncthreads();
   }
   if (inside) {
@@ -805,6 +818,8 @@ __global__ void __launch_bounds__(kBlendThreads) blend_backward(BlendArgs<S> p) 
     for (int c = 0; c < kBwdBatch / 32; ++c)
       if (c * 32 < n) sm.st.tw[c][tid] = transpose32(sm.st.cov[c * 32 + lane][warp_], lane);
     __syncthreads();
+    const uint32_t nxt_e = base + (uint32_t)n + threadIdx.x;
+    const uint32_t nxt = (threadIdx.x < kBwdBatch && nxt_e < end) ? p.entry_item[nxt_e] : 0xffffffffu;
     // ---- pass 1: my pixel (two candidates per trip, sequential T) ----
     {
       BitWalk it;
@@ -861,6 +876,7 @@ __global__ void __launch_bounds__(kBlendThreads) blend_backward(BlendArgs<S> p) 
         }
       }
     }
+    prefetch_records(p, nxt, vbase_item);
     __syncthreads();
     // ---- pass 2: my entry, my half of its records (pixel order) ----
     S acc[8];

@@ -186,3 +186,76 @@ def make_geodesic_sphere(frequency: int, amplitude: float = 0.05, seed: int = 0,
 def seeded_colors(num_vertices: int, seed: int = 0) -> np.ndarray:
     """Vertex colours U[0.1, 0.9] (SURVEY §8d shared settings)."""
     return np.random.default_rng(seed).uniform(0.1, 0.9, size=(num_vertices, 3))
+
+
+def make_grid_cube(divisions: int = 8, half_extent: float = 1.0, position_colors: bool = False) -> TriangleMesh:
+    """Axis-aligned cube, each face a divisions x divisions grid of quads
+    (two triangles each), outward winding; same vertex/facet order as the
+    reference (mesh.py:508-550)."""
+    if divisions < 1:
+        raise MeshError("divisions must be >= 1")
+    pts, tris, index = [], [], {}
+
+    def vid(p):
+        key = tuple(np.round(p, 12))
+        if key not in index:
+            index[key] = len(pts)
+            pts.append(np.asarray(p, dtype=np.float64))
+        return index[key]
+
+    h = half_extent
+    lin = np.linspace(-h, h, divisions + 1)
+    for axis in range(3):
+        for sign in (-1.0, 1.0):
+            ua, va = [a for a in range(3) if a != axis]
+            for i in range(divisions):
+                for j in range(divisions):
+                    quad = []
+                    for du, dv in ((0, 0), (1, 0), (1, 1), (0, 1)):
+                        p = np.zeros(3)
+                        p[axis] = sign * h
+                        p[ua] = lin[i + du]
+                        p[va] = lin[j + dv]
+                        quad.append(vid(p))
+                    a, b, c, d = quad
+                    if (sign > 0) ^ (axis == 1):
+                        tris += [(a, b, c), (a, c, d)]
+                    else:
+                        tris += [(a, c, b), (a, d, c)]
+    verts = np.asarray(pts)
+    col = np.clip((verts / h + 1.0) / 2.0, 0.0, 1.0) if position_colors else None
+    return TriangleMesh(verts, tris, col)
+
+
+def _diameter(points) -> float:
+    pts = np.asarray(points, dtype=np.float64)
+    if len(pts) > 1024:
+        try:
+            from scipy.spatial import ConvexHull
+            pts = pts[ConvexHull(pts).vertices]
+        except Exception:
+            pass
+    best = 0.0
+    block = max(1, int(2 ** 22 // max(len(pts), 1)))
+    for s in range(0, len(pts), block):
+        d2 = ((pts[s:s + block, None, :] - pts[None, :, :]) ** 2).sum(axis=2)
+        best = max(best, float(d2.max()))
+    return float(np.sqrt(best))
+
+
+def normalize_mesh(mesh: TriangleMesh):
+    """Centre on the bounding-box centre, scale the diameter to 2
+    (reference mesh.py:428-456).  Returns (mesh, (center, scale))."""
+    if mesh.num_vertices < 2:
+        raise MeshError("need at least 2 vertices to normalize")
+    d = _diameter(mesh.vertices)
+    if d < 1e-12:
+        raise MeshError("all vertices coincide; cannot normalize")
+    center = 0.5 * (mesh.vertices.min(axis=0) + mesh.vertices.max(axis=0))
+    scale = 2.0 / d
+    return mesh.with_vertices(scale * (mesh.vertices - center)), (center, scale)
+
+
+def make_grid_cube_normalized(divisions: int = 4) -> TriangleMesh:
+    """Config 5 target: normalize_mesh(make_grid_cube(divisions, position_colors=True))."""
+    return normalize_mesh(make_grid_cube(divisions, position_colors=True))[0]

@@ -130,3 +130,16 @@ def convert_case():
     col = rng.random((150, 3))
     return dict(vertices=v, facets=f, colors=col, g_means=rng.normal(size=(50, 3)),
                 g_cov3d=rng.normal(size=(50, 3, 3)), g_colors=rng.normal(size=(50, 3)))
+
+
+def _mesh_dict(m):
+    return dict(vertices=np.asarray(m.vertices), facets=np.asarray(m.facets), colors=np.asarray(m.colors))
+
+
+def fit_case():
+    """Config 5 inputs (reference tests/test_acceptance.py:57-93)."""
+    from paper_2602_14493_b200.camera import sphere_views
+    from paper_2602_14493_b200.mesh import TriangleMesh, make_grid_cube_normalized
+    target = make_grid_cube_normalized(4)
+    init = make_icosphere(1280)
+    return dict(target=_mesh_dict(target), init=_mesh_dict(init), cameras=sphere_views(20, 3.0, 64))

@@ -93,6 +93,31 @@ def convert_case(name, case):
     print(name, {k: v.shape for k, v in out.items()})
 
 
+def fit_case(name, iterations=200):
+    """Config 5: icosphere(1280) -> normalised 4x4 grid cube, 20 views 64^2,
+    FitConfig(iterations=200, batch_size=1, lr_positions=1e-2, seed=0)
+    (reference tests/test_acceptance.py:57-93)."""
+    from meshsplat.optim import FitConfig, fit
+    case = gc.fit_case()
+    target = ref_mesh(case["target"])
+    cams = [ref_cam(c) for c in case["cameras"]]
+    views = [ms.render_mesh(target, c, dtype=np.float64) for c in cams]
+    init = ref_mesh(case["init"])
+    cfg = FitConfig(iterations=iterations, batch_size=1, seed=0, log_every=0, lr_positions=1e-2)
+    res = fit(init, cams, [v.rgb for v in views], [v.alpha for v in views], cfg)
+    hist = np.array([[h["total"], h["color"], h["silhouette"], h["edge"], h["laplacian"]] for h in res.history])
+    # the same loop rendered in float64: the reference's own precision spread
+    cfg64 = FitConfig(iterations=iterations, batch_size=1, seed=0, log_every=0, lr_positions=1e-2,
+                      dtype="float64")
+    res64 = fit(init, cams, [v.rgb for v in views], [v.alpha for v in views], cfg64)
+    hist64 = np.array([h["total"] for h in res64.history])
+    out = dict(history=hist, history_f64=hist64, final_vertices=res.mesh.vertices, final_colors=res.mesh.colors,
+               target_rgb=np.array([v.rgb for v in views]), target_mask=np.array([v.alpha for v in views]),
+               wall_time=res.wall_time)
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+    print(name, hist[0], hist[-1], res.wall_time)
+
+
 if __name__ == "__main__":
     render_case("c1_icosphere1280_128", gc.c1_case())
     render_case("octahedron_32", gc.octahedron_case())
@@ -101,3 +126,5 @@ if __name__ == "__main__":
     splat_case("splats_closed_form_32", gc.closed_form_splat_case())
     loss_case("loss_octa_3views_16", gc.loss_case())
     convert_case("convert_random50", gc.convert_case())
+    if "--fit" in sys.argv:
+        fit_case("fit_c5_200")

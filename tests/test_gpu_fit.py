@@ -1,0 +1,33 @@
+"""Config 5: the 200-iteration inverse-rendering loop on the device render
+path vs the real reference's trajectory (tests/golden/fit_c5_200.npz, made by
+make_golden.py --fit; iteration-0 total 1.405564 as recorded in
+pkg/test_output.txt:265)."""
+
+import numpy as np
+import pytest
+
+import golden_cases as gc
+
+pytestmark = pytest.mark.gpu
+
+
+def test_fit_config5_loss_parity(gmr):
+    from paper_2602_14493_b200 import fit as gfit
+    case, g = gc.fit_case(), gc.load("fit_c5_200")
+    init = gmr.TriangleMesh(case["init"]["vertices"], case["init"]["facets"], case["init"]["colors"])
+    cfg = gfit.FitConfig(iterations=200, batch_size=1, seed=0, log_every=0, lr_positions=1e-2)
+    res = gfit.fit(init, case["cameras"], list(g["target_rgb"]), list(g["target_mask"]), cfg)
+    hist = np.array([[h["total"], h["color"], h["silhouette"], h["edge"], h["laplacian"]] for h in res.history])
+    ref = g["history"]
+    # same seeded view order, same fp32 render dtype: the first iterations agree
+    # to fp32 rounding; later ones drift apart only through optimiser feedback.
+    # Tolerance: the reference's OWN fp32-vs-fp64 spread on this loop (up to
+    # ~2.4 % along the trajectory), plus margin.
+    spread = np.max(np.abs(g["history_f64"] - ref[:, 0]) / ref[:, 0])
+    assert spread < 0.03
+    assert hist[0, 0] == pytest.approx(1.405564, abs=5e-6)
+    np.testing.assert_allclose(hist[:5, 0], ref[:5, 0], rtol=1e-4)
+    np.testing.assert_allclose(hist[:, 0], ref[:, 0], rtol=1.25 * spread)
+    assert abs(hist[-1, 0] - ref[-1, 0]) <= 1.25 * spread * ref[-1, 0]
+    print(f"fit: final total {hist[-1, 0]:.6f} (reference {ref[-1, 0]:.6f}), {res.wall_time:.2f}s "
+          f"vs reference {float(g['wall_time']):.1f}s")
