@@ -4,6 +4,7 @@
 // never allocates: every buffer lives in the caller's workspace, carved by
 // `plan()` identically for the size query, the forward and the backward.
 #include <math.h>
+#include <stdlib.h>
 #include <stdarg.h>
 #include <stdio.h>
 #include <string.h>

@@ -699,7 +699,7 @@ __global__ void __launch_bounds__(kBlendThreads) blend_forward(BlendArgs<S> p) {
 template <typename S, bool kOpacity> struct RecOf { typedef V2<S> type; };
 template <typename S> struct RecOf<S, true> { typedef V4<S> type; };
 
-constexpr int kBwdPairBytes = 32 * 1024;
+constexpr int kBwdPairBytes = 24 * 1024;
 
 template <typename S, bool kOpacity> struct BwdSmem {
   typedef typename RecOf<S, kOpacity>::type Rec;
@@ -729,7 +729,7 @@ template <typename S, bool kOpacity> struct BwdSmem {
 //    in pixel order; the halves are combined in a fixed order.
 //  No atomics, fixed orders: the result is deterministic.
 template <typename S, bool kOpacity>
-__global__ void __launch_bounds__(kBlendThreads) blend_backward(BlendArgs<S> p) {
+__global__ void __launch_bounds__(kBlendThreads, 5) blend_backward(BlendArgs<S> p) {
   extern __shared__ __align__(32) unsigned char dyn[];
   typedef BwdSmem<S, kOpacity> Sm;
   typedef typename Sm::Rec Rec;
