@@ -170,17 +170,25 @@ def run_gmr(args, cfg):
 
     state = {}
 
-    def step():
-        rgb, alpha, st = engine.render_forward(pos, col, faces, cams, W, H, BG)
+    pending = []
+
+    def step(final=False):
+        # forward and backward enqueued back to back; the forward's status
+        # (entry capacity, non-finite splats) is validated one step behind,
+        # so the device never drains between steps
+        rgb, alpha, st = engine.render_forward(pos, col, faces, cams, W, H, BG, check=False)
         gp, gc = engine.render_backward(st, pos, col, faces, rgb, g_rgb, g_a)
         if world > 1:
             buf = torch.cat([gp, gc], dim=1)
             dist.all_reduce(buf)
+        pending.append(st)
+        while len(pending) > (0 if final else 1):
+            engine.check_status(pending.pop(0))   # raises on overflow / non-finite
         state["st"] = st
         return gp
 
-    for _ in range(args.warmup):
-        step()
+    for i in range(args.warmup):
+        step(final=(i == args.warmup - 1))
     torch.cuda.synchronize()
     sampler = ClockSampler(local) if rank == 0 else None
     time.sleep(0.3 if sampler else 0)
@@ -193,8 +201,8 @@ def run_gmr(args, cfg):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     wall0 = time.time()
     e0.record()
-    for _ in range(args.steps):
-        step()
+    for i in range(args.steps):
+        step(final=(i == args.steps - 1))
     e1.record()
     torch.cuda.synchronize()
     wall1 = time.time()

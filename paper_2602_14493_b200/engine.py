@@ -116,9 +116,13 @@ def _status_or_raise(ws, kind, item_to_index=None):
 
 
 def render_forward(pos, col, faces, cams, width, height, background, rescale=True, flags=0,
-                   item_to_index=None):
+                   item_to_index=None, check=True):
     """B-view forward.  pos/col [V,3] (f32|f64, cuda), faces [F,3] int32.
-    Returns (rgb [B,H,W,3], alpha [B,H,W], ForwardState)."""
+    Returns (rgb [B,H,W,3], alpha [B,H,W], ForwardState).
+
+    check=False enqueues without waiting for the status (no host sync); the
+    caller must then call `check_status(state)` before using any result --
+    a capacity overflow or a non-finite splat is reported there."""
     lib = L.load()
     dtype = pos.dtype
     B, F = len(cams), int(faces.shape[0])
@@ -129,6 +133,20 @@ def render_forward(pos, col, faces, cams, width, height, background, rescale=Tru
     cap = _capacity.get(key, F * B)
     rgb = torch.empty((B, height, width, 3), dtype=dtype, device=pos.device)
     alpha = torch.empty((B, height, width), dtype=dtype, device=pos.device)
+    if not check:
+        nb = ctypes.c_size_t()
+        L.check(lib.gmr_render_workspace_size(F, B, width, height, cap, raster.dtype, ctypes.byref(nb)))
+        ws = torch.empty(nb.value, dtype=torch.uint8, device=pos.device)
+        L.check(lib.gmr_render_forward(ctypes.byref(mesh), cam_arr, B, ctypes.byref(raster), _ptr(rgb),
+                                       _ptr(alpha), _ptr(ws), nb.value, cap, _stream()))
+        st = ForwardState(ws, cap, raster, cam_arr, B, -1, -1)
+        # the 64-byte device status, copied behind the forward (no sync)
+        st.status_host = torch.empty(64, dtype=torch.uint8, pin_memory=True)
+        st.status_host.copy_(ws[:64], non_blocking=True)
+        st.status_event = torch.cuda.Event()
+        st.status_event.record()
+        st.key = key
+        return rgb, alpha, st
     for _ in range(3):
         nb = ctypes.c_size_t()
         L.check(lib.gmr_render_workspace_size(F, B, width, height, cap, raster.dtype, ctypes.byref(nb)))
@@ -141,6 +159,31 @@ def render_forward(pos, col, faces, cams, width, height, background, rescale=Tru
             return rgb, alpha, ForwardState(ws, cap, raster, cam_arr, B, st.entries, st.kept)
         cap = _capacity.grow(key, st.entries)
     raise RuntimeError("tile-entry capacity did not converge")
+
+
+class CapacityExceeded(RuntimeError):
+    """A deferred-check forward needed more tile entries than it was planned
+    for; its outputs are invalid.  The capacity has been raised: re-run."""
+
+
+def check_status(state: ForwardState, key=None):
+    """Validate a forward launched with check=False.  Waits only for that
+    forward (its status copy event), not for work enqueued after it."""
+    key = getattr(state, "key", key)
+    state.status_event.synchronize()
+    raw = state.status_host.numpy()
+    entries, kept = (int(x) for x in raw[:16].view(np.uint64))
+    words = raw[16:48].view(np.uint32)
+    bad, overflow = words[:6], int(words[6])
+    state.entries, state.kept = entries, kept
+    for field in range(6):
+        if bad[field] != 0xFFFFFFFF:
+            raise ValueError(f"non-finite splat parameter {_FIELDS[field]!r} at splat {int(bad[field])}")
+    if overflow:
+        _capacity.grow(key, entries)
+        raise CapacityExceeded(f"{entries} tile entries > capacity {state.capacity}")
+    _capacity.note(key, state.capacity, entries)
+    return state
 
 
 def render_backward(state: ForwardState, pos, col, faces, rgb, g_rgb, g_alpha):
