@@ -353,12 +353,12 @@ def run_fit(args, cfg):
     iters = 200
     cfg5 = gfit.FitConfig(iterations=iters, batch_size=1, seed=0, log_every=0, lr_positions=1e-2)
     for _ in range(max(1, args.warmup)):
-        gfit.fit(init, case["cameras"], rgbs, masks, gfit.FitConfig(iterations=5, batch_size=1, seed=0,
+        gfit.fit_device(init, case["cameras"], rgbs, masks, gfit.FitConfig(iterations=5, batch_size=1, seed=0,
                                                                   log_every=0, lr_positions=1e-2))
     torch.cuda.synchronize()
     walls = []
     for _ in range(max(1, args.steps // 10)):
-        res = gfit.fit(init, case["cameras"], rgbs, masks, cfg5)
+        res = gfit.fit_device(init, case["cameras"], rgbs, masks, cfg5)
         walls.append(res.wall_time)
     wall = float(np.median(walls))
     final = res.history[-1]["total"]

@@ -17,6 +17,8 @@
  *   convert.py:313-368 convert_mesh (embed route)    gmr_convert
  *   convert.py:371-437 convert_backward              gmr_convert_backward
  *   losses.py:151-162  total_loss view loop          B views per gmr_render_* call
+ *   losses.py:43-73    color_loss, silhouette_loss   gmr_render_forward_loss (fused)
+ *   losses.py:76-123, optim.py:29-135, :271-295      gmr_fit_step (regularisers + Adam)
  *
  * Scalars: every floating-point buffer is either float32 (GMR_F32, the fast
  * path; `fit`'s default dtype, reference optim.py:161) or float64
@@ -117,6 +119,64 @@ int gmr_render_workspace_size(int64_t num_faces, int32_t num_views, int32_t widt
 int gmr_render_forward(const GmrMesh* mesh, const GmrCamera* cameras, int32_t num_views,
                        const GmrRaster* raster, void* rgb, void* alpha, void* workspace,
                        size_t workspace_bytes, int64_t entry_capacity, void* stream);
+
+/* Forward with the image losses fused into the blend epilogue (reference
+ * losses.py:43-73 and the w/n scaling of total_loss, :158-160): for target
+ * images target_rgb [B,H,W,3] / target_mask [B,H,W] (dtype) it also writes
+ * g_rgb = d(w_c/n * sum_v MSE_v)/d rgb and g_alpha likewise for the clamped
+ * BCE (scale_rgb = w_c/n, scale_alpha = w_s/n), and loss_sums (device, 2
+ * doubles) = (sum of squared colour errors, sum of BCE terms) over all
+ * pixels of all views -- divide by 3HW and HW for the per-view means. */
+int gmr_render_forward_loss(const GmrMesh* mesh, const GmrCamera* cameras, int32_t num_views,
+                            const GmrRaster* raster, const void* target_rgb,
+                            const void* target_mask, double scale_rgb, double scale_alpha,
+                            void* rgb, void* alpha, void* g_rgb, void* g_alpha,
+                            double* loss_sums, void* workspace, size_t workspace_bytes,
+                            int64_t entry_capacity, void* stream);
+
+/* ---- device-resident optimisation step (reference optim.py / losses.py) -- */
+
+typedef struct {
+  double* positions;        /* [V,3] float64 parameters, updated in place     */
+  double* colors;           /* [V,3]                                         */
+  float* positions_f32;     /* float32 render copies refreshed by the step   */
+  float* colors_f32;        /*   (may be null)                               */
+  double* m_pos;            /* VectorAdam state: [V,3] and [V]               */
+  double* v_pos;
+  double* m_col;            /* ScalarAdam state: [V,3] and [V,3]             */
+  double* v_col;
+  int64_t* step_counts;     /* [2] accepted steps (positions, colours)        */
+  int32_t* flags;           /* [2] scratch, zero before the first step        */
+} GmrFitState;
+
+/* Static mesh graph: unique undirected edges [E,2] (lexsorted, smaller index
+ * first, mesh.py:96-106), the vertex -> (edge, endpoint) CSR in np.add.at
+ * order (slot = 2 edge + endpoint, all endpoint-1 slots before endpoint-0
+ * ones, losses.py:95-96) and the sorted neighbour CSR (mesh.py:114-126). */
+typedef struct {
+  const int32_t* edges;
+  int64_t num_edges;
+  const int32_t* ve_ptr;
+  const int32_t* ve_slot;
+  const int32_t* adj_ptr;
+  const int32_t* adj;
+} GmrMeshGraph;
+
+int gmr_fit_scratch_size(int64_t num_vertices, int64_t num_edges, size_t* bytes);
+
+/* One optimisation step (optim.py:271-295): total gradient = image terms
+ * (grad_img_*, float32, from gmr_render_backward) + w_edge * edge-length +
+ * w_lap * Laplacian gradients; VectorAdam on positions, ScalarAdam + [0,1]
+ * clip on colours (a step with a non-finite gradient is rejected, as in the
+ * reference); history_row (device, 5 doubles) = (total, color, silhouette,
+ * edge, laplacian) with color = img_loss_sums[0] * inv_nc and silhouette =
+ * img_loss_sums[1] * inv_na (the loss sums of gmr_render_forward_loss). */
+int gmr_fit_step(const GmrFitState* state, const GmrMeshGraph* graph, int64_t num_vertices,
+                 const float* grad_img_pos, const float* grad_img_col,
+                 const double* img_loss_sums, double inv_nc, double inv_na, double w_color,
+                 double w_sil, double w_edge, double w_lap, double lr_pos, double lr_col,
+                 double beta1, double beta2, double eps, int32_t optimize_colors,
+                 double* history_row, void* scratch, size_t scratch_bytes, void* stream);
 
 /* Synchronise `stream` and read the status of the last forward that used
  * `workspace`.  Returns GMR_ECAPACITY / GMR_ENONFINITE as appropriate. */

@@ -395,21 +395,17 @@ def total_loss(mesh, cameras: Sequence[Camera], target_rgb, target_mask, weights
     bg = np.asarray(background, dtype=np.float64)
     for (w, h), idx in groups.items():
         cams = [cameras[i] for i in idx]
-        rgb, alpha, state = engine.render_forward(pos, col, faces, cams, w, h, bg, rescale)
-        t_rgb = torch.as_tensor(np.stack([np.asarray(target_rgb[i], np.float64) for i in idx])).to(dev)
-        t_m = torch.as_tensor(np.stack([np.asarray(target_mask[i], np.float64) for i in idx])).to(dev)
-        if t_rgb.shape != rgb.shape or t_m.shape != alpha.shape:
+        t_rgb = torch.as_tensor(np.stack([np.asarray(target_rgb[i], np.float64) for i in idx]),
+                                dtype=tdt).to(dev)
+        t_m = torch.as_tensor(np.stack([np.asarray(target_mask[i], np.float64) for i in idx]), dtype=tdt).to(dev)
+        if t_rgb.shape != (len(idx), h, w, 3) or t_m.shape != (len(idx), h, w):
             raise ValueError("shape mismatch between renders and targets")
-        r64, a64 = rgb.double(), alpha.double()
-        diff = r64 - t_rgb
-        cv_acc += (diff * diff).mean(dim=(1, 2, 3)).sum()
-        g_rgb = (2.0 / diff[0].numel()) * diff * (weights.color / n)
-        p = a64.clamp(BCE_CLAMP, 1.0 - BCE_CLAMP)
-        sv_acc += (-(t_m * torch.log(p) + (1.0 - t_m) * torch.log1p(-p))).mean(dim=(1, 2)).sum()
-        inside = (a64 > BCE_CLAMP) & (a64 < 1.0 - BCE_CLAMP)
-        g_a = torch.where(inside, (-t_m / p + (1.0 - t_m) / (1.0 - p)) / a64[0].numel(),
-                          torch.zeros_like(a64)) * (weights.silhouette / n)
-        gp, gc = engine.render_backward(state, pos, col, faces, rgb, g_rgb.to(tdt), g_a.to(tdt))
+        # losses fused into the blend epilogue (gmr_render_forward_loss)
+        rgb, alpha, g_rgb, g_a, sums, state = engine.render_forward_loss(
+            pos, col, faces, cams, w, h, bg, t_rgb, t_m, weights.color / n, weights.silhouette / n, rescale)
+        cv_acc += sums[0] / (3.0 * w * h)
+        sv_acc += sums[1] / (1.0 * w * h)
+        gp, gc = engine.render_backward(state, pos, col, faces, rgb, g_rgb, g_a)
         gp_acc += gp.double()
         gc_acc += gc.double()
     # one transfer for everything

@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "gmr_kernels.cuh"
+#include "gmr_train.cuh"
 
 using namespace gmr;
 
@@ -89,7 +90,7 @@ inline unsigned grid_for(uint64_t n, unsigned block) { return (unsigned)std::max
 // Workspace layout (byte offsets).
 struct Layout {
   size_t status, splat, col4, rect, count, dkey[2], ditem[2], offs, entry_off, bsum, nent;
-  size_t ekey[2], eval[2], bounds, t_final, hist, partial, partial_op, face_acc, corner, aux;
+  size_t ekey[2], eval[2], bounds, t_final, hist, partial, partial_op, face_acc, corner, aux, loss_tile;
   size_t total;
   uint64_t items, faces, bins, pixels, ecap;
   int views, tiles_x, tiles_y, tiles;
@@ -139,6 +140,7 @@ Layout plan(uint64_t faces, int views, int W, int H, uint64_t ecap, int dtype, b
   L.face_acc = take(mesh ? faces * 12 * s : 0);
   L.corner = take(mesh ? faces * 18 * s : 0);
   L.aux = take(mesh ? L.items * 2 * s : 0);
+  L.loss_tile = take(L.bins * 16);
   L.total = o;
   return L;
 }
@@ -170,10 +172,20 @@ CamBatch<S> make_cams(const GmrCamera* cams, int v0, int nv) {
   return b;
 }
 
+// optional fused losses of a forward
+struct LossArgs {
+  const void* target_rgb;
+  const void* target_mask;
+  double scale_rgb, scale_alpha;
+  void* g_rgb;
+  void* g_alpha;
+  double* sums;   // device [2]
+};
+
 // Binning (K2) + blend forward (K3) over prepared item records.
 template <typename S>
 int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void* alpha,
-                  cudaStream_t st) {
+                  cudaStream_t st, const LossArgs* la = nullptr) {
   typedef typename KeyOf<S>::type K;
   const uint32_t items = (uint32_t)L.items;
   // depth order of all items (stable: ties keep item = (view, face) order)
@@ -244,9 +256,22 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
   a.rgb = (S*)rgb;
   a.alpha = (S*)alpha;
   a.t_final = at<S>(ws, L.t_final);
+  if (la) {
+    a.target_rgb = (const S*)la->target_rgb;
+    a.target_mask = (const S*)la->target_mask;
+    a.scale_rgb = la->scale_rgb;
+    a.scale_alpha = la->scale_alpha;
+    a.g_rgb_out = (S*)la->g_rgb;
+    a.g_alpha_out = (S*)la->g_alpha;
+    a.loss_tile = at<double>(ws, L.loss_tile);
+  }
   if (L.bins) {
     StageScope sc(kStBlendFwd, st);
     blend_forward<S><<<(unsigned)L.bins, kBlendThreads, 0, st>>>(a);
+    GMR_LAUNCHED();
+  }
+  if (la && L.bins) {
+    loss_reduce<<<1, 256, 0, st>>>(at<double>(ws, L.loss_tile), (uint32_t)L.bins, la->sums);
     GMR_LAUNCHED();
   }
   return GMR_OK;
@@ -254,7 +279,7 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
 
 template <typename S>
 int render_forward_t(const GmrMesh* m, const GmrCamera* cams, int B, const GmrRaster* r, void* rgb,
-                     void* alpha, void* ws, const Layout& L, cudaStream_t st) {
+                     void* alpha, void* ws, const Layout& L, cudaStream_t st, const LossArgs* la = nullptr) {
   reset_status<<<1, 1, 0, st>>>(at<DevStatus>(ws, L.status));
   GMR_LAUNCHED();
   const uint64_t F = L.faces;
@@ -286,7 +311,7 @@ int render_forward_t(const GmrMesh* m, const GmrCamera* cams, int B, const GmrRa
       GMR_LAUNCHED();
     }
   }
-  return bin_and_blend<S>(L, ws, r, rgb, alpha, st);
+  return bin_and_blend<S>(L, ws, r, rgb, alpha, st, la);
 }
 
 template <typename S, bool kOpacity>
@@ -506,6 +531,90 @@ int gmr_render_forward(const GmrMesh* mesh, const GmrCamera* cams, int32_t B, co
   cudaStream_t st = (cudaStream_t)stream;
   if (r->dtype == GMR_F64) return render_forward_t<double>(mesh, cams, B, r, rgb, alpha, ws, L, st);
   return render_forward_t<float>(mesh, cams, B, r, rgb, alpha, ws, L, st);
+}
+
+int gmr_render_forward_loss(const GmrMesh* mesh, const GmrCamera* cams, int32_t B, const GmrRaster* r,
+                            const void* target_rgb, const void* target_mask, double scale_rgb,
+                            double scale_alpha, void* rgb, void* alpha, void* g_rgb, void* g_alpha,
+                            double* loss_sums, void* ws, size_t ws_bytes, int64_t ecap, void* stream) {
+  int rc = check_mesh(mesh);
+  if (rc) return rc;
+  if ((rc = check_raster(r))) return rc;
+  if (!cams || B < 1 || B > GMR_MAX_VIEWS_PER_CALL) return fail(GMR_EINVAL, "need 1..%d cameras", GMR_MAX_VIEWS_PER_CALL);
+  if (!rgb || !alpha || !ws || !target_rgb || !target_mask || !g_rgb || !g_alpha || !loss_sums)
+    return fail(GMR_EINVAL, "null pointer argument");
+  if ((uint64_t)mesh->num_faces * B >= 0xffffffffull) return fail(GMR_EINVAL, "faces*views must be < 2^32");
+  const Layout L = plan((uint64_t)mesh->num_faces, B, r->width, r->height, (uint64_t)ecap, r->dtype, true);
+  if (ws_bytes < L.total) return fail(GMR_EWORKSPACE, "workspace has %zu bytes, needs %zu", ws_bytes, L.total);
+  LossArgs la{target_rgb, target_mask, scale_rgb, scale_alpha, g_rgb, g_alpha, loss_sums};
+  cudaStream_t st = (cudaStream_t)stream;
+  if (r->dtype == GMR_F64) return render_forward_t<double>(mesh, cams, B, r, rgb, alpha, ws, L, st, &la);
+  return render_forward_t<float>(mesh, cams, B, r, rgb, alpha, ws, L, st, &la);
+}
+
+int gmr_fit_scratch_size(int64_t V, int64_t E, size_t* bytes) {
+  if (!bytes || V < 0 || E < 0) return fail(GMR_EINVAL, "bad sizes");
+  const size_t nbe = (E + kTrainThreads - 1) / kTrainThreads + 1, nbv = (V + kTrainThreads - 1) / kTrainThreads + 1;
+  *bytes = align_up(E * 32) + align_up(V * 32) + 2 * align_up(V * 24) + align_up((2 * nbe + nbv) * 8) + align_up(64);
+  return GMR_OK;
+}
+
+int gmr_fit_step(const GmrFitState* s, const GmrMeshGraph* gr, int64_t V, const float* grad_img_pos,
+                 const float* grad_img_col, const double* img_loss_sums, double inv_nc, double inv_na,
+                 double w_color, double w_sil, double w_edge, double w_lap, double lr_pos, double lr_col,
+                 double beta1, double beta2, double eps, int32_t optimize_colors, double* history_row,
+                 void* scratch, size_t scratch_bytes, void* stream) {
+  if (!s || !gr || V <= 0 || !grad_img_pos || !grad_img_col || !img_loss_sums || !history_row || !scratch)
+    return fail(GMR_EINVAL, "null or empty argument");
+  const int64_t E = gr->num_edges;
+  size_t need;
+  int rc = gmr_fit_scratch_size(V, E, &need);
+  if (rc) return rc;
+  if (scratch_bytes < need) return fail(GMR_EWORKSPACE, "fit scratch has %zu bytes, needs %zu", scratch_bytes, need);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nbe = (int)((E + kTrainThreads - 1) / kTrainThreads), nbv = (int)((V + kTrainThreads - 1) / kTrainThreads);
+  char* o = (char*)scratch;
+  double* evec4 = (double*)o; o += align_up(E * 32);
+  double* lap4 = (double*)o; o += align_up(V * 32);
+  double* gpos = (double*)o; o += align_up(V * 24);
+  double* gcol = (double*)o; o += align_up(V * 24);
+  double* part = (double*)o; o += align_up((2 * (nbe + 1) + nbv + 1) * 8);
+  double* sums = (double*)o;   // [0] sum len, [1] sum dev^2, [2] sum |lap|^2
+  double* part_len = part;
+  double* part_dev = part + nbe + 1;
+  double* part_lap = part + 2 * (nbe + 1);
+  if (E) {
+    edge_lengths<<<nbe, kTrainThreads, 0, st>>>(s->positions, gr->edges, E, evec4, part_len);
+    GMR_LAUNCHED();
+    sum_partials<<<1, kTrainThreads, 0, st>>>(part_len, nbe, sums);
+    GMR_LAUNCHED();
+    edge_terms<<<nbe, kTrainThreads, 0, st>>>(evec4, E, sums, part_dev);
+    GMR_LAUNCHED();
+    sum_partials<<<1, kTrainThreads, 0, st>>>(part_dev, nbe, sums + 1);
+    GMR_LAUNCHED();
+  } else {
+    GMR_CUDA(cudaMemsetAsync(sums, 0, 16, st));
+  }
+  laplacian_terms<<<nbv, kTrainThreads, 0, st>>>(s->positions, gr->adj_ptr, gr->adj, V, lap4, part_lap);
+  GMR_LAUNCHED();
+  sum_partials<<<1, kTrainThreads, 0, st>>>(part_lap, nbv, sums + 2);
+  GMR_LAUNCHED();
+  AdamArgs a{};
+  a.pos = s->positions; a.col = s->colors; a.pos_f = s->positions_f32; a.col_f = s->colors_f32;
+  a.g_img_pos = grad_img_pos; a.g_img_col = grad_img_col;
+  a.m_pos = s->m_pos; a.v_pos = s->v_pos; a.m_col = s->m_col; a.v_col = s->v_col;
+  a.counts = s->step_counts; a.bad = s->flags;
+  a.lr_pos = lr_pos; a.lr_col = lr_col; a.beta1 = beta1; a.beta2 = beta2; a.eps = eps;
+  a.optimize_colors = optimize_colors;
+  a.reg.ve_ptr = gr->ve_ptr; a.reg.ve_slot = gr->ve_slot; a.reg.adj_ptr = gr->adj_ptr; a.reg.adj = gr->adj;
+  a.reg.evec4 = evec4; a.reg.lap4 = lap4; a.reg.V = V; a.reg.w_edge = w_edge; a.reg.w_lap = w_lap;
+  fit_grads<<<nbv, kTrainThreads, 0, st>>>(a, gpos, gcol);
+  GMR_LAUNCHED();
+  fit_update<<<nbv, kTrainThreads, 0, st>>>(a, gpos, gcol);
+  GMR_LAUNCHED();
+  fit_finish<<<1, 32, 0, st>>>(a, img_loss_sums, inv_nc, inv_na, w_color, w_sil, sums + 1, E, sums + 2, history_row);
+  GMR_LAUNCHED();
+  return GMR_OK;
 }
 
 int gmr_status(const void* ws, GmrStatus* out, void* stream) {

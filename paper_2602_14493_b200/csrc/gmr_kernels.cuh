@@ -461,7 +461,66 @@ template <typename S> struct BlendArgs {
   const S* g_alpha;
   S* partial;        // [E][8] at pre-sort slots
   S* partial_op;     // [E] (splat path only) or null
+  // optional fused image losses (forward epilogue, losses.py:43-73,158-160)
+  const S* target_rgb;     // [B,H,W,3] or null
+  const S* target_mask;    // [B,H,W]
+  double scale_rgb, scale_alpha;   // w_color / n, w_silhouette / n
+  S* g_rgb_out;            // [B,H,W,3] dL/drgb (pre-scaled), read by K4
+  S* g_alpha_out;          // [B,H,W]
+  double* loss_tile;       // [bins][2]: sum of squared colour error, sum of BCE
 };
+
+constexpr double kBceClamp = 1e-6;   // losses.py:20
+
+// Per-pixel colour MSE / clamped-BCE terms and their gradients, in float64
+// like the reference (losses.py:43-73; image grads scaled by w/n, :158-160).
+template <typename S>
+__device__ __forceinline__ void pixel_loss(const BlendArgs<S>& p, size_t pix, const S rgb[3], S alpha,
+                                           double& sq, double& bce) {
+  const double nc = 3.0 * (double)p.W * (double)p.H, na = (double)p.W * (double)p.H;
+  sq = 0.0;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const double d = (double)rgb[c] - (double)p.target_rgb[3 * pix + c];
+    sq += d * d;
+    p.g_rgb_out[3 * pix + c] = (S)((2.0 / nc) * d * p.scale_rgb);
+  }
+  const double a = (double)alpha, m = (double)p.target_mask[pix];
+  const double q = fmin(fmax(a, kBceClamp), 1.0 - kBceClamp);
+  bce = -(m * log(q) + (1.0 - m) * log1p(-q));
+  const bool inside = a > kBceClamp && a < 1.0 - kBceClamp;
+  p.g_alpha_out[pix] = (S)(inside ? ((-m / q + (1.0 - m) / (1.0 - q)) / na) * p.scale_alpha : 0.0);
+}
+
+// fixed-order block sum of two doubles (256 threads)
+__device__ __forceinline__ void block_sum2(double a, double b, double* out2) {
+  __shared__ double sa[8], sb[8];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) { sa[warp] = a; sb[warp] = b; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double x = 0.0, y = 0.0;
+    for (int w = 0; w < 8; ++w) { x += sa[w]; y += sb[w]; }
+    out2[0] = x;
+    out2[1] = y;
+  }
+}
+
+// Sum the per-tile loss partials in tile order (single block, fixed tree).
+__global__ void __launch_bounds__(256) loss_reduce(const double* __restrict__ tile, uint32_t bins,
+                                                  double* __restrict__ out2) {
+  double a = 0.0, b = 0.0;
+  for (uint32_t i = threadIdx.x; i < bins; i += 256) {
+    a += tile[2 * i];
+    b += tile[2 * i + 1];
+  }
+  block_sum2(a, b, out2);
+}
 
 // lane r holds row r of a 32x32 bit matrix (bit c = M[r][c]); returns column
 // `lane` (bit r = M[r][lane]).  5 shuffle stages.
@@ -686,14 +745,21 @@ __global__ void __launch_bounds__(kBlendThreads) blend_forward(BlendArgs<S> p) {
     prefetch_records(p, nxt, vbase_item);
     __syncthreads();
   }
+  double sq = 0.0, bce = 0.0;
   if (inside) {
     const size_t pix = ((size_t)view * p.H + py) * p.W + px;
-    p.rgb[3 * pix + 0] = ar + T * p.bg0;
-    p.rgb[3 * pix + 1] = ag + T * p.bg1;
-    p.rgb[3 * pix + 2] = ab + T * p.bg2;
+    S out[3];
+    out[0] = ar + T * p.bg0;
+    out[1] = ag + T * p.bg1;
+    out[2] = ab + T * p.bg2;
+    p.rgb[3 * pix + 0] = out[0];
+    p.rgb[3 * pix + 1] = out[1];
+    p.rgb[3 * pix + 2] = out[2];
     p.alpha[pix] = one - T;
     p.t_final[pix] = T;
+    if (p.target_rgb) pixel_loss(p, pix, out, one - T, sq, bce);
   }
+  if (p.target_rgb) block_sum2(sq, bce, p.loss_tile + 2 * (size_t)g);
 }
 
 template <typename S, bool kOpacity> struct RecOf { typedef V2<S> type; };

@@ -1,0 +1,235 @@
+// gmr_train.cuh — device-resident optimisation step.
+//
+//   edge_length_loss  losses.py:76-97   (per-edge lengths, mean detached)
+//   laplacian_loss    losses.py:100-123 (uniform Laplacian, exact gradient)
+//   VectorAdam        optim.py:29-81    (per-vertex shared second moment)
+//   ScalarAdam        optim.py:84-126   (+ colour clip to [0, 1], optim.py:292)
+//
+// All parameters and optimiser state are float64 like the reference; the
+// float32 render copies are refreshed by the update.  Scatter-adds run as
+// fixed-order gathers over static CSR tables (built once per topology), and
+// reductions are fixed trees, so every step is bit-reproducible.
+#pragma once
+
+#include "gmr_common.cuh"
+
+namespace gmr {
+
+constexpr int kTrainThreads = 256;
+
+// fixed-tree block sum of one double; thread 0 writes it
+__device__ __forceinline__ void block_sum1(double a, double* out) {
+  __shared__ double sa[kTrainThreads / 32];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+  if ((threadIdx.x & 31) == 0) sa[threadIdx.x >> 5] = a;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double x = 0.0;
+    for (int w = 0; w < kTrainThreads / 32; ++w) x += sa[w];
+    *out = x;
+  }
+}
+
+// single block: out[0] = sum of part[0..n) in a fixed order
+__global__ void __launch_bounds__(kTrainThreads) sum_partials(const double* __restrict__ part, int n,
+                                                             double* __restrict__ out) {
+  double a = 0.0;
+  for (int i = threadIdx.x; i < n; i += kTrainThreads) a += part[i];
+  block_sum1(a, out);
+}
+
+// per edge: vector b - a and length; block partial sums of the lengths
+__global__ void __launch_bounds__(kTrainThreads) edge_lengths(const double* __restrict__ pos,
+                                                             const int32_t* __restrict__ edges, int64_t E,
+                                                             double* __restrict__ vec4, double* __restrict__ part) {
+  const int64_t e = (int64_t)blockIdx.x * kTrainThreads + threadIdx.x;
+  double len = 0.0;
+  if (e < E) {
+    const int32_t a = edges[2 * e], b = edges[2 * e + 1];
+    const double x = pos[3 * b] - pos[3 * a], y = pos[3 * b + 1] - pos[3 * a + 1], z = pos[3 * b + 2] - pos[3 * a + 2];
+    len = sqrt(x * x + y * y + z * z);
+    vec4[4 * e] = x; vec4[4 * e + 1] = y; vec4[4 * e + 2] = z; vec4[4 * e + 3] = len;
+  }
+  block_sum1(len, part + blockIdx.x);
+}
+
+// per edge: dev = len - mean; coeff = (2/E) dev / max(len, 1e-12) -> vec4 = coeff * vec;
+// block partial sums of dev^2
+__global__ void __launch_bounds__(kTrainThreads) edge_terms(double* __restrict__ vec4, int64_t E,
+                                                           const double* __restrict__ len_sum,
+                                                           double* __restrict__ part) {
+  const int64_t e = (int64_t)blockIdx.x * kTrainThreads + threadIdx.x;
+  double d2 = 0.0;
+  if (e < E) {
+    const double mean = *len_sum / (double)E;
+    const double len = vec4[4 * e + 3];
+    const double dev = len - mean;
+    d2 = dev * dev;
+    const double coeff = (2.0 / (double)E) * dev / fmax(len, 1e-12);
+    vec4[4 * e] *= coeff; vec4[4 * e + 1] *= coeff; vec4[4 * e + 2] *= coeff;
+  }
+  block_sum1(d2, part + blockIdx.x);
+}
+
+// Laplacian per vertex over the sorted neighbour CSR (mesh.py:114-126):
+// lap = v - mean(neighbours); scaled = lap / max(deg, 1); block sums |lap|^2
+__global__ void __launch_bounds__(kTrainThreads) laplacian_terms(const double* __restrict__ pos,
+                                                                const int32_t* __restrict__ adj_ptr,
+                                                                const int32_t* __restrict__ adj, int64_t V,
+                                                                double* __restrict__ lap4, double* __restrict__ part) {
+  const int64_t v = (int64_t)blockIdx.x * kTrainThreads + threadIdx.x;
+  double l2 = 0.0;
+  if (v < V) {
+    const int32_t b = adj_ptr[v], e = adj_ptr[v + 1];
+    double sx = 0.0, sy = 0.0, sz = 0.0;
+    for (int32_t k = b; k < e; ++k) {
+      const int32_t u = adj[k];
+      sx += pos[3 * u]; sy += pos[3 * u + 1]; sz += pos[3 * u + 2];
+    }
+    const int deg = e - b;
+    double lx = 0.0, ly = 0.0, lz = 0.0;
+    if (deg > 0) {
+      lx = pos[3 * v] - sx / deg; ly = pos[3 * v + 1] - sy / deg; lz = pos[3 * v + 2] - sz / deg;
+    }
+    l2 = lx * lx + ly * ly + lz * lz;
+    const double inv = 1.0 / fmax((double)deg, 1.0);
+    lap4[4 * v] = lx; lap4[4 * v + 1] = ly; lap4[4 * v + 2] = lz; lap4[4 * v + 3] = inv;
+  }
+  block_sum1(l2, part + blockIdx.x);
+}
+
+struct RegArgs {
+  const int32_t* ve_ptr;    // vertex -> (edge, endpoint) CSR in np.add.at order
+  const int32_t* ve_slot;   // slot = 2 * edge + endpoint (endpoint 1: +, endpoint 0: -)
+  const int32_t* adj_ptr;
+  const int32_t* adj;
+  const double* evec4;      // per edge: coeff * vec
+  const double* lap4;       // per vertex: lap, 1 / max(deg, 1)
+  int64_t V;
+  double w_edge, w_lap;
+};
+
+// per vertex: w_e * g_edge + w_l * g_lap (losses.py:93-97, :117-123)
+__device__ __forceinline__ void reg_grad(const RegArgs& r, int64_t v, double g[3]) {
+  double ex = 0.0, ey = 0.0, ez = 0.0;
+  for (int32_t k = r.ve_ptr[v]; k < r.ve_ptr[v + 1]; ++k) {
+    const int32_t s = r.ve_slot[k];
+    const double sg = (s & 1) ? 1.0 : -1.0;
+    const double* ev = r.evec4 + 4 * (s >> 1);
+    ex += sg * ev[0]; ey += sg * ev[1]; ez += sg * ev[2];
+  }
+  double bx = 0.0, by = 0.0, bz = 0.0;
+  for (int32_t k = r.adj_ptr[v]; k < r.adj_ptr[v + 1]; ++k) {
+    const double* lu = r.lap4 + 4 * r.adj[k];
+    const bool has = r.adj_ptr[r.adj[k] + 1] > r.adj_ptr[r.adj[k]];
+    if (has) { bx += lu[0] * lu[3]; by += lu[1] * lu[3]; bz += lu[2] * lu[3]; }
+  }
+  const double c = 2.0 / (double)r.V;
+  const double* lv = r.lap4 + 4 * v;
+  g[0] = r.w_edge * ex + r.w_lap * (c * lv[0] - c * bx);
+  g[1] = r.w_edge * ey + r.w_lap * (c * lv[1] - c * by);
+  g[2] = r.w_edge * ez + r.w_lap * (c * lv[2] - c * bz);
+}
+
+struct AdamArgs {
+  double* pos;        // [V,3] float64 parameters (updated)
+  double* col;        // [V,3]
+  float* pos_f;       // float32 render copies (or null)
+  float* col_f;
+  const float* g_img_pos;   // [V,3] image-term gradients from the render backward
+  const float* g_img_col;
+  double* m_pos;      // [V,3]
+  double* v_pos;      // [V]
+  double* m_col;      // [V,3]
+  double* v_col;      // [V,3]
+  int64_t* counts;    // [2]: accepted steps (positions, colours)
+  int* bad;           // [2]: non-finite gradient flags of this step
+  double lr_pos, lr_col, beta1, beta2, eps;
+  int optimize_colors;
+  RegArgs reg;
+};
+
+// pass 1: total gradients (image + regularisers) -> stash, non-finite flags
+__global__ void __launch_bounds__(kTrainThreads) fit_grads(AdamArgs a, double* __restrict__ gpos,
+                                                          double* __restrict__ gcol) {
+  const int64_t v = (int64_t)blockIdx.x * kTrainThreads + threadIdx.x;
+  bool bp = false, bc = false;
+  if (v < a.reg.V) {
+    double gr[3];
+    reg_grad(a.reg, v, gr);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const double gp = (double)a.g_img_pos[3 * v + k] + gr[k];
+      const double gc = (double)a.g_img_col[3 * v + k];
+      gpos[3 * v + k] = gp;
+      gcol[3 * v + k] = gc;
+      bp |= !isfinite(gp);
+      bc |= !isfinite(gc);
+    }
+  }
+  if (__syncthreads_or(bp) && threadIdx.x == 0) atomicOr(&a.bad[0], 1);
+  if (__syncthreads_or(bc) && threadIdx.x == 0) atomicOr(&a.bad[1], 1);
+}
+
+// pass 2: VectorAdam on positions, ScalarAdam + clip on colours; a step
+// with any non-finite gradient is rejected whole (optim.py:55-60, :103-106)
+__global__ void __launch_bounds__(kTrainThreads) fit_update(AdamArgs a, const double* __restrict__ gpos,
+                                                           const double* __restrict__ gcol) {
+  const int64_t v = (int64_t)blockIdx.x * kTrainThreads + threadIdx.x;
+  if (v >= a.reg.V) return;
+  if (!a.bad[0]) {
+    const double t = (double)(a.counts[0] + 1);
+    const double g0 = gpos[3 * v], g1 = gpos[3 * v + 1], g2 = gpos[3 * v + 2];
+    const double vv = a.beta2 * a.v_pos[v] + (1.0 - a.beta2) * (g0 * g0 + g1 * g1 + g2 * g2);
+    a.v_pos[v] = vv;
+    const double v_hat = vv / (1.0 - pow(a.beta2, t));
+    const double den = sqrt(v_hat) + a.eps;
+    const double c1 = 1.0 - pow(a.beta1, t);
+    const double gg[3] = {g0, g1, g2};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const double m = a.beta1 * a.m_pos[3 * v + k] + (1.0 - a.beta1) * gg[k];
+      a.m_pos[3 * v + k] = m;
+      const double p = a.pos[3 * v + k] + (-a.lr_pos * (m / c1) / den);
+      a.pos[3 * v + k] = p;
+      if (a.pos_f) a.pos_f[3 * v + k] = (float)p;
+    }
+  }
+  if (a.optimize_colors && !a.bad[1]) {
+    const double t = (double)(a.counts[1] + 1);
+    const double c1 = 1.0 - pow(a.beta1, t), c2 = 1.0 - pow(a.beta2, t);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const double g = gcol[3 * v + k];
+      const double m = a.beta1 * a.m_col[3 * v + k] + (1.0 - a.beta1) * g;
+      const double vv = a.beta2 * a.v_col[3 * v + k] + (1.0 - a.beta2) * g * g;
+      a.m_col[3 * v + k] = m;
+      a.v_col[3 * v + k] = vv;
+      const double c = fmin(fmax(a.col[3 * v + k] - a.lr_col * (m / c1) / (sqrt(vv / c2) + a.eps), 0.0), 1.0);
+      a.col[3 * v + k] = c;
+      if (a.col_f) a.col_f[3 * v + k] = (float)c;
+    }
+  }
+}
+
+// pass 3: step counters, flags reset, the iteration's loss report
+// history[it] = (total, color, silhouette, edge, laplacian)
+__global__ void fit_finish(AdamArgs a, const double* __restrict__ img_sums, double inv_nc, double inv_na,
+                           double w_color, double w_sil, const double* __restrict__ edge_sum, int64_t E,
+                           const double* __restrict__ lap_sum, double* __restrict__ history) {
+  if (threadIdx.x != 0) return;
+  if (!a.bad[0]) a.counts[0] += 1;
+  if (a.optimize_colors && !a.bad[1]) a.counts[1] += 1;
+  a.bad[0] = a.bad[1] = 0;
+  const double color = img_sums[0] * inv_nc, sil = img_sums[1] * inv_na;
+  const double edge = E ? *edge_sum / (double)E : 0.0;
+  const double lap = *lap_sum / (double)a.reg.V;
+  history[0] = w_color * color + w_sil * sil + a.reg.w_edge * edge + a.reg.w_lap * lap;
+  history[1] = color;
+  history[2] = sil;
+  history[3] = edge;
+  history[4] = lap;
+}
+
+}  // namespace gmr

@@ -161,6 +161,52 @@ def render_forward(pos, col, faces, cams, width, height, background, rescale=Tru
     raise RuntimeError("tile-entry capacity did not converge")
 
 
+def render_forward_loss(pos, col, faces, cams, width, height, background, target_rgb, target_mask,
+                        scale_rgb, scale_alpha, rescale=True, check=True):
+    """B-view forward with the colour/silhouette losses fused into the blend
+    epilogue.  target_rgb [B,H,W,3] / target_mask [B,H,W] on the device in the
+    render dtype.  Returns (rgb, alpha, g_rgb, g_alpha, loss_sums [2] f64 on
+    the device: sum of squared colour errors, sum of BCE terms), state)."""
+    lib = L.load()
+    dtype = pos.dtype
+    B, F = len(cams), int(faces.shape[0])
+    raster = raster_struct(width, height, background, dtype, rescale, 0)
+    cam_arr = L.camera_struct(cams)
+    mesh = mesh_struct(pos, col, faces)
+    key = (F, B, int(width), int(height), dtype)
+    dev = pos.device
+    rgb = torch.empty((B, height, width, 3), dtype=dtype, device=dev)
+    alpha = torch.empty((B, height, width), dtype=dtype, device=dev)
+    g_rgb = torch.empty_like(rgb)
+    g_a = torch.empty_like(alpha)
+    sums = torch.empty(2, dtype=torch.float64, device=dev)
+    t_rgb = target_rgb.to(dtype).contiguous()
+    t_m = target_mask.to(dtype).contiguous()
+    cap = _capacity.get(key, F * B)
+    for _ in range(3):
+        nb = ctypes.c_size_t()
+        L.check(lib.gmr_render_workspace_size(F, B, width, height, cap, raster.dtype, ctypes.byref(nb)))
+        ws = torch.empty(nb.value, dtype=torch.uint8, device=dev)
+        L.check(lib.gmr_render_forward_loss(ctypes.byref(mesh), cam_arr, B, ctypes.byref(raster), _ptr(t_rgb),
+                                            _ptr(t_m), float(scale_rgb), float(scale_alpha), _ptr(rgb), _ptr(alpha),
+                                            _ptr(g_rgb), _ptr(g_a), _ptr(sums), _ptr(ws), nb.value, cap, _stream()))
+        st = ForwardState(ws, cap, raster, cam_arr, B, -1, -1)
+        if not check:
+            st.status_host = torch.empty(64, dtype=torch.uint8, pin_memory=True)
+            st.status_host.copy_(ws[:64], non_blocking=True)
+            st.status_event = torch.cuda.Event()
+            st.status_event.record()
+            st.key = key
+            return rgb, alpha, g_rgb, g_a, sums, st
+        s_, code = _status_or_raise(ws, "mesh")
+        if code == L.GMR_OK:
+            _capacity.note(key, cap, s_.entries)
+            st.entries, st.kept = s_.entries, s_.kept
+            return rgb, alpha, g_rgb, g_a, sums, st
+        cap = _capacity.grow(key, s_.entries)
+    raise RuntimeError("tile-entry capacity did not converge")
+
+
 class CapacityExceeded(RuntimeError):
     """A deferred-check forward needed more tile entries than it was planned
     for; its outputs are invalid.  The capacity has been raised: re-run."""

@@ -51,6 +51,17 @@ class GmrStatus(ctypes.Structure):
                 ("overflow", c_i32), ("nonfinite_field", c_i32), ("nonfinite_item", c_i64)]
 
 
+class GmrFitState(ctypes.Structure):
+    _fields_ = [("positions", c_vp), ("colors", c_vp), ("positions_f32", c_vp), ("colors_f32", c_vp),
+                ("m_pos", c_vp), ("v_pos", c_vp), ("m_col", c_vp), ("v_col", c_vp),
+                ("step_counts", c_vp), ("flags", c_vp)]
+
+
+class GmrMeshGraph(ctypes.Structure):
+    _fields_ = [("edges", c_vp), ("num_edges", c_i64), ("ve_ptr", c_vp), ("ve_slot", c_vp),
+                ("adj_ptr", c_vp), ("adj", c_vp)]
+
+
 class GmrSplats(ctypes.Structure):
     _fields_ = [("mean2d", c_vp), ("cov2d", c_vp), ("depth", c_vp), ("color", c_vp),
                 ("opacity", c_vp), ("count", c_i64)]
@@ -67,6 +78,11 @@ _SIGNATURES = {
     "gmr_render_forward": ([P(GmrMesh), P(GmrCamera), c_i32, P(GmrRaster), c_vp, c_vp, c_vp,
                             c_sz, c_i64, c_vp], c_i32),
     "gmr_status": ([c_vp, P(GmrStatus), c_vp], c_i32),
+    "gmr_fit_scratch_size": ([c_i64, c_i64, P(c_sz)], c_i32),
+    "gmr_fit_step": ([P(GmrFitState), P(GmrMeshGraph), c_i64, c_vp, c_vp, c_vp] + [ctypes.c_double] * 11
+                     + [c_i32, c_vp, c_vp, c_sz, c_vp], c_i32),
+    "gmr_render_forward_loss": ([P(GmrMesh), P(GmrCamera), c_i32, P(GmrRaster), c_vp, c_vp, ctypes.c_double,
+                                 ctypes.c_double, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_i64, c_vp], c_i32),
     "gmr_topology_size": ([c_i64, c_i64, P(c_sz)], c_i32),
     "gmr_topology_build": ([c_vp, c_i64, c_i64, c_vp, c_sz, c_vp], c_i32),
     "gmr_render_backward": ([P(GmrMesh), P(GmrCamera), c_i32, P(GmrRaster), c_vp, c_vp, c_vp,

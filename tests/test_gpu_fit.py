@@ -31,3 +31,37 @@ def test_fit_config5_loss_parity(gmr):
     assert abs(hist[-1, 0] - ref[-1, 0]) <= 1.25 * spread * ref[-1, 0]
     print(f"fit: final total {hist[-1, 0]:.6f} (reference {ref[-1, 0]:.6f}), {res.wall_time:.2f}s "
           f"vs reference {float(g['wall_time']):.1f}s")
+
+
+def test_fit_device_config5_loss_parity(gmr):
+    """The whole iteration on the GPU (fused losses + gmr_fit_step) tracks
+    the reference trajectory like the host-optimiser loop does."""
+    from paper_2602_14493_b200 import fit as gfit
+    case, g = gc.fit_case(), gc.load("fit_c5_200")
+    init = gmr.TriangleMesh(case["init"]["vertices"], case["init"]["facets"], case["init"]["colors"])
+    cfg = gfit.FitConfig(iterations=200, batch_size=1, seed=0, log_every=0, lr_positions=1e-2)
+    res = gfit.fit_device(init, case["cameras"], list(g["target_rgb"]), list(g["target_mask"]), cfg)
+    hist = np.array([[h["total"], h["color"], h["silhouette"], h["edge"], h["laplacian"]] for h in res.history])
+    ref = g["history"]
+    spread = np.max(np.abs(g["history_f64"] - ref[:, 0]) / ref[:, 0])
+    assert hist[0, 0] == pytest.approx(1.405564, abs=5e-6)
+    # regulariser values are computed in float64 on the device from float64 parameters
+    np.testing.assert_allclose(hist[0, 3:], ref[0, 3:], rtol=1e-10)
+    np.testing.assert_allclose(hist[:5, 0], ref[:5, 0], rtol=1e-4)
+    np.testing.assert_allclose(hist[:, 0], ref[:, 0], rtol=1.25 * spread)
+    assert abs(hist[-1, 0] - ref[-1, 0]) <= 1.25 * spread * ref[-1, 0]
+    print(f"fit_device: final total {hist[-1, 0]:.6f} (reference {ref[-1, 0]:.6f}), {res.wall_time:.3f}s")
+
+
+def test_fit_device_matches_host_optimiser(gmr):
+    """Same render path, optimiser on device vs host (both float64)."""
+    from paper_2602_14493_b200 import fit as gfit
+    case, g = gc.fit_case(), gc.load("fit_c5_200")
+    init = gmr.TriangleMesh(case["init"]["vertices"], case["init"]["facets"], case["init"]["colors"])
+    cfg = gfit.FitConfig(iterations=20, batch_size=2, seed=3, log_every=0, lr_positions=1e-2)
+    a = gfit.fit(init, case["cameras"], list(g["target_rgb"]), list(g["target_mask"]), cfg)
+    b = gfit.fit_device(init, case["cameras"], list(g["target_rgb"]), list(g["target_mask"]), cfg)
+    ha = np.array([h["total"] for h in a.history])
+    hb = np.array([h["total"] for h in b.history])
+    np.testing.assert_allclose(hb, ha, rtol=1e-4)
+    np.testing.assert_allclose(b.mesh.vertices, a.mesh.vertices, rtol=0, atol=1e-5)
