@@ -137,7 +137,7 @@ Layout plan(uint64_t faces, int views, int W, int H, uint64_t ecap, int dtype, b
                          radix_hist_words((uint32_t)std::min<uint64_t>(ecap, 0xffffffffu))) * 4);
   L.partial = take(ecap * 8 * s);
   L.partial_op = take(mesh ? 0 : ecap * s);
-  L.face_acc = take(mesh ? faces * 12 * s : 0);
+  L.face_acc = take(mesh ? faces * 12 * 8 : 0);
   L.corner = take(mesh ? faces * 18 * s : 0);
   L.aux = take(mesh ? L.items * 2 * s : 0);
   L.loss_tile = take(L.bins * 16);
@@ -369,7 +369,7 @@ int render_backward_t(const GmrMesh* m, const GmrCamera* cams, int B, const GmrR
     a.entry_off = at<uint32_t>(ws, L.entry_off);
     a.splat = at<Splat<S>>(ws, L.splat);
     a.partial = at<S>(ws, L.partial);
-    a.face_acc = at<S>(ws, L.face_acc);
+    a.face_acc = at<double>(ws, L.face_acc);
     if (F) {
       StageScope sc(kStFaceBwd, st);
       face_views_backward<S><<<grid_for(F, 128), 128, 0, st>>>(a, make_cams<S>(cams, v0, nv));
@@ -379,7 +379,7 @@ int render_backward_t(const GmrMesh* m, const GmrCamera* cams, int B, const GmrR
   if (F) {
     StageScope sc(kStFaceBwd, st);
     face_convert_backward<S><<<grid_for(F, 128), 128, 0, st>>>((const S*)m->positions, m->faces, (int64_t)F,
-                                                               r->rescale, at<S>(ws, L.face_acc),
+                                                               r->rescale, at<double>(ws, L.face_acc),
                                                                at<S>(ws, L.corner));
     GMR_LAUNCHED();
   }
@@ -459,8 +459,8 @@ template <typename S>
 int convert_backward_t(const GmrMesh* m, int rescale, const void* gm, const void* gc, const void* gcol, void* gp,
                        void* gcv, const void* topo, void* scratch, cudaStream_t st) {
   const int64_t F = m->num_faces, V = m->num_vertices;
-  S* acc = (S*)scratch;
-  S* corner = (S*)((char*)scratch + align_up(F * 12 * sizeof(S)));
+  double* acc = (double*)scratch;
+  S* corner = (S*)((char*)scratch + align_up(F * 12 * 8));
   if (F) {
     pack_face_grads<S><<<grid_for(F, 256), 256, 0, st>>>((const S*)gm, (const S*)gc, (const S*)gcol, F, acc);
     GMR_LAUNCHED();
@@ -795,7 +795,7 @@ int gmr_convert(const GmrMesh* mesh, int32_t rescale, int32_t dtype, void* means
 int gmr_convert_scratch_size(int64_t F, int32_t dtype, size_t* bytes) {
   if (!bytes || F < 0) return fail(GMR_EINVAL, "bad sizes");
   const size_t s = dtype == GMR_F64 ? 8 : 4;
-  *bytes = align_up(F * 12 * s) + align_up(F * 18 * s);
+  *bytes = align_up(F * 12 * 8) + align_up(F * 18 * s);
   return GMR_OK;
 }
 

@@ -52,8 +52,15 @@ __device__ __forceinline__ float exp_s(float x) { return expf(x); }
 __device__ __forceinline__ double exp_s(double x) { return exp(x); }
 __device__ __forceinline__ float sqrt_s(float x) { return sqrtf(x); }
 __device__ __forceinline__ double sqrt_s(double x) { return sqrt(x); }
-__device__ __forceinline__ float hypot_s(float a, float b) { return hypotf(a, b); }
-__device__ __forceinline__ double hypot_s(double a, double b) { return hypot(a, b); }
+// C99 / numpy semantics: hypot(+-inf, y) = +inf even when y is NaN (an
+// overflowed screen covariance keeps radius = inf, so the splat is kept and
+// then reported as non-finite, render.py:84-88,125-133,191-197)
+__device__ __forceinline__ float hypot_s(float a, float b) {
+  return (isinf(a) || isinf(b)) ? INFINITY : hypotf(a, b);
+}
+__device__ __forceinline__ double hypot_s(double a, double b) {
+  return (isinf(a) || isinf(b)) ? (double)INFINITY : hypot(a, b);
+}
 __device__ __forceinline__ float log_s(float x) { return logf(x); }
 __device__ __forceinline__ double log_s(double x) { return log(x); }
 __device__ __forceinline__ float floor_s(float x) { return floorf(x); }

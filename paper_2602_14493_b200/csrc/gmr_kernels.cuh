@@ -49,68 +49,80 @@ __device__ __forceinline__ unsigned long long order_key(double d) {
 // K1: facet -> Gaussian -> EWA projection -> cull -> screen record
 // ---------------------------------------------------------------------------
 
-template <typename S> struct FaceGeo {
-  S e[3][3];      // e1 = b-a, e2 = c-a, e3 = c-b
-  S n[3];         // unit normal (u / |u|, or u when degenerate)
-  S nu;           // |u| (1 when degenerate)
-  S area, kappa;
-  S mean[3];
+// Facet geometry of the embed route, always in float64 like the reference
+// (convert.py:239-276 runs in float64 whatever the render dtype; the render
+// dtype only starts at projection, render.py:105,113).
+struct FaceGeo {
+  double e[3][3];      // e1 = b-a, e2 = c-a, e3 = c-b
+  double n[3];         // unit normal (u / |u|, or u when degenerate)
+  double nu;           // |u| (1 when degenerate)
+  double area, kappa;
+  double mean[3];
   bool degenerate, clamped;
 };
 
 template <typename S>
 __device__ __forceinline__ void load_face(const S* __restrict__ pos, const int32_t* __restrict__ faces,
-                                          int64_t f, int rescale, FaceGeo<S>& g, int32_t idx[3]) {
+                                          int64_t f, int rescale, FaceGeo& g, int32_t idx[3]) {
   idx[0] = faces[3 * f + 0];
   idx[1] = faces[3 * f + 1];
   idx[2] = faces[3 * f + 2];
-  S v[3][3];
+  double v[3][3];
 #pragma unroll
   for (int c = 0; c < 3; ++c)
 #pragma unroll
-    for (int k = 0; k < 3; ++k) v[c][k] = pos[3 * (int64_t)idx[c] + k];
+    for (int k = 0; k < 3; ++k) v[c][k] = (double)pos[3 * (int64_t)idx[c] + k];
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     g.e[0][k] = v[1][k] - v[0][k];
     g.e[1][k] = v[2][k] - v[0][k];
     g.e[2][k] = v[2][k] - v[1][k];
-    g.mean[k] = (v[0][k] + v[1][k] + v[2][k]) / S(3);
+    g.mean[k] = (v[0][k] + v[1][k] + v[2][k]) / 3.0;
   }
-  S u0 = g.e[0][1] * g.e[1][2] - g.e[0][2] * g.e[1][1];
-  S u1 = g.e[0][2] * g.e[1][0] - g.e[0][0] * g.e[1][2];
-  S u2 = g.e[0][0] * g.e[1][1] - g.e[0][1] * g.e[1][0];
-  S nu = sqrt_s(u0 * u0 + u1 * u1 + u2 * u2);
-  g.area = S(0.5) * nu;
-  g.degenerate = g.area < S(kDegenerateArea);
-  g.nu = g.degenerate ? S(1) : nu;
+  const double u0 = g.e[0][1] * g.e[1][2] - g.e[0][2] * g.e[1][1];
+  const double u1 = g.e[0][2] * g.e[1][0] - g.e[0][0] * g.e[1][2];
+  const double u2 = g.e[0][0] * g.e[1][1] - g.e[0][1] * g.e[1][0];
+  const double nu = sqrt(u0 * u0 + u1 * u1 + u2 * u2);
+  g.area = 0.5 * nu;
+  g.degenerate = g.area < kDegenerateArea;
+  g.nu = g.degenerate ? 1.0 : nu;
   g.n[0] = u0 / g.nu;
   g.n[1] = u1 / g.nu;
   g.n[2] = u2 / g.nu;
-  S det2d = g.area * g.area / S(108);
-  g.clamped = det2d < S(kDetEps);
-  if (rescale) {
-    // convert.py:267 (== sqrt(108)/pi up to rounding when unclamped)
-    g.kappa = g.area / (S(kPi) * sqrt_s(g.clamped ? S(kDetEps) : det2d));
-  } else {
-    g.kappa = S(1);
-  }
+  const double det2d = g.area * g.area / 108.0;
+  g.clamped = det2d < kDetEps;
+  // convert.py:267 (== sqrt(108)/pi up to rounding when unclamped)
+  g.kappa = rescale ? g.area / (kPi * sqrt(g.clamped ? kDetEps : det2d)) : 1.0;
 }
 
-// world cov3d (upper triangle xx,xy,xz,yy,yz,zz) of the embed route
-template <typename S>
-__device__ __forceinline__ void face_cov3d(const FaceGeo<S>& g, S c[6]) {
+// world cov3d (upper triangle xx,xy,xz,yy,yz,zz) of the embed route, float64
+__device__ __forceinline__ void face_cov3d(const FaceGeo& g, double c[6]) {
   if (g.degenerate) {
-    c[0] = c[3] = c[5] = S(kSz2);
-    c[1] = c[2] = c[4] = S(0);
+    c[0] = c[3] = c[5] = kSz2;
+    c[1] = c[2] = c[4] = 0.0;
     return;
   }
   const int ii[6] = {0, 0, 0, 1, 1, 2}, jj[6] = {0, 1, 2, 1, 2, 2};
 #pragma unroll
   for (int q = 0; q < 6; ++q) {
     const int i = ii[q], j = jj[q];
-    S c3 = (g.e[0][i] * g.e[0][j] + g.e[1][i] * g.e[1][j] + g.e[2][i] * g.e[2][j]) / S(36);
-    c[q] = g.kappa * c3 + S(kSz2) * g.n[i] * g.n[j];
+    const double c3 = (g.e[0][i] * g.e[0][j] + g.e[1][i] * g.e[1][j] + g.e[2][i] * g.e[2][j]) / 36.0;
+    c[q] = g.kappa * c3 + kSz2 * g.n[i] * g.n[j];
   }
+}
+
+// cov2d = M2 Sigma M2^T in the render dtype (render.py:115-116)
+template <typename S>
+__device__ __forceinline__ void project_cov(const S m2[2][3], const S cv[6], S& a, S& b, S& c) {
+  const S sg[3][3] = {{cv[0], cv[1], cv[2]}, {cv[1], cv[3], cv[4]}, {cv[2], cv[4], cv[5]}};
+  S ms[2][3];
+#pragma unroll
+  for (int r = 0; r < 2; ++r)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) ms[r][j] = m2[r][0] * sg[0][j] + m2[r][1] * sg[1][j] + m2[r][2] * sg[2][j];
+  a = ms[0][0] * m2[0][0] + ms[0][1] * m2[0][1] + ms[0][2] * m2[0][2];
+  b = ms[0][0] * m2[1][0] + ms[0][1] * m2[1][1] + ms[0][2] * m2[1][2];
+  c = ms[1][0] * m2[1][0] + ms[1][1] * m2[1][1] + ms[1][2] * m2[1][2];
 }
 
 template <typename S>
@@ -157,7 +169,7 @@ __global__ void __launch_bounds__(256) mesh_to_splats(MeshFwdArgs<S> p, const __
   const bool live = f < p.F;
   uint32_t kept = 0;
   if (live) {
-    FaceGeo<S> g;
+    FaceGeo g;
     int32_t idx[3];
     load_face(p.pos, p.faces, f, p.rescale, g, idx);
     if (p.view0 == 0) {
@@ -168,12 +180,19 @@ __global__ void __launch_bounds__(256) mesh_to_splats(MeshFwdArgs<S> p, const __
       c.w = S(1);  // opacity (convert.py:326)
       p.col4[f] = c;
     }
-    // projected-edge form of M2 (kappa c3 + s_z^2 n n^T) M2^T
+    // the float64 Gaussian, cast to the render dtype (render.py:105,113)
+    double cov64[6];
+    face_cov3d(g, cov64);
+    S cov[6], mean[3];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) cov[q] = (S)cov64[q];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) mean[q] = (S)g.mean[q];
     for (int vv = 0; vv < p.nviews; ++vv) {
       const Cam<S>& cam = cams.cam[vv];
       const int64_t item = (int64_t)(p.view0 + vv) * p.F + f;
       S t[3];
-      cam_point(cam, g.mean, t);
+      cam_point(cam, mean, t);
       Splat<S> rec;
       uint32_t cnt = 0;
       uint2 rc = make_uint2(0, 0);
@@ -182,27 +201,7 @@ __global__ void __launch_bounds__(256) mesh_to_splats(MeshFwdArgs<S> p, const __
         S m2[2][3];
         cam_m2(cam, t, m2);
         S a, b, c;
-        if (g.degenerate) {
-          a = S(kSz2) * (m2[0][0] * m2[0][0] + m2[0][1] * m2[0][1] + m2[0][2] * m2[0][2]);
-          b = S(kSz2) * (m2[0][0] * m2[1][0] + m2[0][1] * m2[1][1] + m2[0][2] * m2[1][2]);
-          c = S(kSz2) * (m2[1][0] * m2[1][0] + m2[1][1] * m2[1][1] + m2[1][2] * m2[1][2]);
-        } else {
-          S pa = 0, pb = 0, pc = 0;
-#pragma unroll
-          for (int i = 0; i < 3; ++i) {
-            S x = m2[0][0] * g.e[i][0] + m2[0][1] * g.e[i][1] + m2[0][2] * g.e[i][2];
-            S y = m2[1][0] * g.e[i][0] + m2[1][1] * g.e[i][1] + m2[1][2] * g.e[i][2];
-            pa += x * x;
-            pb += x * y;
-            pc += y * y;
-          }
-          S nx = m2[0][0] * g.n[0] + m2[0][1] * g.n[1] + m2[0][2] * g.n[2];
-          S ny = m2[1][0] * g.n[0] + m2[1][1] * g.n[1] + m2[1][2] * g.n[2];
-          const S k36 = g.kappa / S(36);
-          a = k36 * pa + S(kSz2) * nx * nx;
-          b = k36 * pb + S(kSz2) * nx * ny;
-          c = k36 * pc + S(kSz2) * ny * ny;
-        }
+        project_cov(m2, cov, a, b, c);
         a = add_rn(a, Const<S>::dilation());
         c = add_rn(c, Const<S>::dilation());
         const S mx = add_rn(div_rn(mul_rn(cam.fx, t[0]), t[2]), cam.cx);
@@ -1050,22 +1049,28 @@ template <typename S> struct FaceBwdArgs {
   const uint32_t* entry_off;
   const Splat<S>* splat;
   const S* partial;
-  S* face_acc;   // [F][12]: g_mean3 (3), g_cov3 sym (6), g_col (3)
+  double* face_acc;   // [F][12]: g_mean3 (3), g_cov3 sym (6), g_col (3), summed over views in float64
 };
 
 template <typename S>
 __global__ void __launch_bounds__(128) face_views_backward(FaceBwdArgs<S> p, const __grid_constant__ CamBatch<S> cams) {
   const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= p.F) return;
-  FaceGeo<S> g;
+  FaceGeo g;
   int32_t idx[3];
   load_face(p.pos, p.faces, f, p.rescale, g, idx);
-  S cov[6];
-  face_cov3d(g, cov);
-  S acc[12];
+  // the forward's float64 Gaussian in the render dtype (render.py:378)
+  double cov64[6];
+  face_cov3d(g, cov64);
+  S cov[6], mean[3];
+#pragma unroll
+  for (int q = 0; q < 6; ++q) cov[q] = (S)cov64[q];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) mean[q] = (S)g.mean[q];
+  double acc[12];
   if (p.view0 == 0) {
 #pragma unroll
-    for (int q = 0; q < 12; ++q) acc[q] = S(0);
+    for (int q = 0; q < 12; ++q) acc[q] = 0.0;
   } else {
 #pragma unroll
     for (int q = 0; q < 12; ++q) acc[q] = p.face_acc[f * 12 + q];
@@ -1081,15 +1086,15 @@ __global__ void __launch_bounds__(128) face_views_backward(FaceBwdArgs<S> p, con
     conic_to_cov_grad(s, rec.a.z, rec.a.w, rec.b.x, gm, g2);
     const Cam<S>& cam = cams.cam[vv];
     S t[3], m2[2][3];
-    cam_point(cam, g.mean, t);
+    cam_point(cam, mean, t);
     cam_m2(cam, t, m2);
     // g_cov3d += M2^T G M2 (render.py:382), G = [[g0, g1], [g1, g2]]
     const int ii[6] = {0, 0, 0, 1, 1, 2}, jj[6] = {0, 1, 2, 1, 2, 2};
 #pragma unroll
     for (int q = 0; q < 6; ++q) {
       const int i = ii[q], j = jj[q];
-      acc[3 + q] += m2[0][i] * (g2[0] * m2[0][j] + g2[1] * m2[1][j]) +
-                    m2[1][i] * (g2[1] * m2[0][j] + g2[2] * m2[1][j]);
+      acc[3 + q] += (double)(m2[0][i] * (g2[0] * m2[0][j] + g2[1] * m2[1][j]) +
+                             m2[1][i] * (g2[1] * m2[0][j] + g2[2] * m2[1][j]));
     }
     // g_M2 = (G + G^T) M2 Sigma (render.py:383-384)
     S ms[2][3];
@@ -1120,10 +1125,10 @@ __global__ void __launch_bounds__(128) face_views_backward(FaceBwdArgs<S> p, con
             gm[0] * cam.fx * t[0] * iz2 - gm[1] * cam.fy * t[1] * iz2;
     // g_mean3d = g_t R (render.py:401)
 #pragma unroll
-    for (int k = 0; k < 3; ++k) acc[k] += gt0 * cam.R[k] + gt1 * cam.R[3 + k] + gt2 * cam.R[6 + k];
-    acc[9] += s[5];
-    acc[10] += s[6];
-    acc[11] += s[7];
+    for (int k = 0; k < 3; ++k) acc[k] += (double)(gt0 * cam.R[k] + gt1 * cam.R[3 + k] + gt2 * cam.R[6 + k]);
+    acc[9] += (double)s[5];
+    acc[10] += (double)s[6];
+    acc[11] += (double)s[7];
   }
 #pragma unroll
   for (int q = 0; q < 12; ++q) p.face_acc[f * 12 + q] = acc[q];
@@ -1135,49 +1140,49 @@ template <typename S>
 __global__ void __launch_bounds__(128) face_convert_backward(const S* __restrict__ pos,
                                                              const int32_t* __restrict__ faces,
                                                              int64_t F, int rescale,
-                                                             const S* __restrict__ face_acc,
+                                                             const double* __restrict__ face_acc,
                                                              S* __restrict__ corner) {
   const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= F) return;
-  FaceGeo<S> g;
+  FaceGeo g;
   int32_t idx[3];
   load_face(pos, faces, f, rescale, g, idx);
-  S a[12];
+  double a[12];
 #pragma unroll
   for (int q = 0; q < 12; ++q) a[q] = face_acc[f * 12 + q];
   // G symmetric (xx,xy,xz,yy,yz,zz); gsym = 2G
-  const S G[3][3] = {{a[3], a[4], a[5]}, {a[4], a[6], a[7]}, {a[5], a[7], a[8]}};
-  S ge[3][3];   // g_e1, g_e2, g_e3
+  const double G[3][3] = {{a[3], a[4], a[5]}, {a[4], a[6], a[7]}, {a[5], a[7], a[8]}};
+  double ge[3][3];   // g_e1, g_e2, g_e3 (float64 like convert.py:393-425)
   if (!g.degenerate) {
-    const S sk = g.kappa * S(2) / S(36);
+    const double sk = g.kappa * 2.0 / 36.0;
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
 #pragma unroll
       for (int r = 0; r < 3; ++r) {
-        const S* e = g.e[i == 2 ? 2 : i];
+        const double* e = g.e[i == 2 ? 2 : i];
         ge[i][r] = sk * (G[r][0] * e[0] + G[r][1] * e[1] + G[r][2] * e[2]);
       }
     }
-    S d_area = S(0);
+    double d_area = 0.0;
     if (rescale && g.clamped) {
-      S dk = 0;
+      double dk = 0.0;
 #pragma unroll
       for (int r = 0; r < 3; ++r)
 #pragma unroll
         for (int c = 0; c < 3; ++c)
-          dk += G[r][c] * (g.e[0][r] * g.e[0][c] + g.e[1][r] * g.e[1][c] + g.e[2][r] * g.e[2][c]) / S(36);
-      d_area = dk / (S(kPi) * sqrt_s(S(kDetEps)));
+          dk += G[r][c] * (g.e[0][r] * g.e[0][c] + g.e[1][r] * g.e[1][c] + g.e[2][r] * g.e[2][c]) / 36.0;
+      d_area = dk / (kPi * sqrt(kDetEps));
     }
-    S gn[3];
+    double gn[3];
 #pragma unroll
-    for (int r = 0; r < 3; ++r) gn[r] = S(kSz2) * S(2) * (G[r][0] * g.n[0] + G[r][1] * g.n[1] + G[r][2] * g.n[2]);
-    const S nd = g.n[0] * gn[0] + g.n[1] * gn[1] + g.n[2] * gn[2];
-    S gu[3];
+    for (int r = 0; r < 3; ++r) gn[r] = kSz2 * 2.0 * (G[r][0] * g.n[0] + G[r][1] * g.n[1] + G[r][2] * g.n[2]);
+    const double nd = g.n[0] * gn[0] + g.n[1] * gn[1] + g.n[2] * gn[2];
+    double gu[3];
 #pragma unroll
-    for (int r = 0; r < 3; ++r) gu[r] = (gn[r] - g.n[r] * nd) / g.nu + S(0.5) * d_area * g.n[r];
+    for (int r = 0; r < 3; ++r) gu[r] = (gn[r] - g.n[r] * nd) / g.nu + 0.5 * d_area * g.n[r];
     // g_e1 += e2 x g_u ; g_e2 += g_u x e1
-    const S* e1 = g.e[0];
-    const S* e2 = g.e[1];
+    const double* e1 = g.e[0];
+    const double* e2 = g.e[1];
     ge[0][0] += e2[1] * gu[2] - e2[2] * gu[1];
     ge[0][1] += e2[2] * gu[0] - e2[0] * gu[2];
     ge[0][2] += e2[0] * gu[1] - e2[1] * gu[0];
@@ -1188,16 +1193,16 @@ __global__ void __launch_bounds__(128) face_convert_backward(const S* __restrict
 #pragma unroll
     for (int i = 0; i < 3; ++i)
 #pragma unroll
-      for (int r = 0; r < 3; ++r) ge[i][r] = S(0);
+      for (int r = 0; r < 3; ++r) ge[i][r] = 0.0;
   }
   S* out = corner + f * 18;
 #pragma unroll
   for (int r = 0; r < 3; ++r) {
-    const S third = a[r] / S(3);
-    out[0 + r] = third - ge[0][r] - ge[1][r];
-    out[6 + r] = third + ge[0][r] - ge[2][r];
-    out[12 + r] = third + ge[1][r] + ge[2][r];
-    const S gc = a[9 + r] / S(3);
+    const double third = a[r] / 3.0;
+    out[0 + r] = (S)(third - ge[0][r] - ge[1][r]);
+    out[6 + r] = (S)(third + ge[0][r] - ge[2][r]);
+    out[12 + r] = (S)(third + ge[1][r] + ge[2][r]);
+    const S gc = (S)(a[9 + r] / 3.0);
     out[3 + r] = gc;
     out[9 + r] = gc;
     out[15 + r] = gc;
@@ -1290,17 +1295,17 @@ __global__ void __launch_bounds__(128) convert_forward(const S* __restrict__ pos
                                                        uint8_t* degenerate) {
   const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= F) return;
-  FaceGeo<S> g;
+  FaceGeo g;
   int32_t idx[3];
   load_face(pos, faces, f, rescale, g, idx);
-  S c[6];
+  double c[6];
   face_cov3d(g, c);
   const int map[9] = {0, 1, 2, 1, 3, 4, 2, 4, 5};
 #pragma unroll
-  for (int k = 0; k < 9; ++k) cov3d[f * 9 + k] = c[map[k]];
+  for (int k = 0; k < 9; ++k) cov3d[f * 9 + k] = (S)c[map[k]];
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
-    means[3 * f + k] = g.mean[k];
+    means[3 * f + k] = (S)g.mean[k];
     colors[3 * f + k] = (col[3 * (int64_t)idx[0] + k] + col[3 * (int64_t)idx[1] + k] + col[3 * (int64_t)idx[2] + k]) / S(3);
   }
   if (degenerate) degenerate[f] = g.degenerate ? 1 : 0;
@@ -1309,18 +1314,18 @@ __global__ void __launch_bounds__(128) convert_forward(const S* __restrict__ pos
 template <typename S>
 __global__ void __launch_bounds__(256) pack_face_grads(const S* __restrict__ gm, const S* __restrict__ gcov,
                                                       const S* __restrict__ gcol, int64_t F,
-                                                      S* __restrict__ face_acc) {
+                                                      double* __restrict__ face_acc) {
   const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= F) return;
   const S* G = gcov + f * 9;
-  S* o = face_acc + f * 12;
+  double* o = face_acc + f * 12;
   o[0] = gm[3 * f]; o[1] = gm[3 * f + 1]; o[2] = gm[3 * f + 2];
   // only (G + G^T)/2 matters (gsym and <G, c3> with c3 symmetric)
   o[3] = G[0];
-  o[4] = S(0.5) * (G[1] + G[3]);
-  o[5] = S(0.5) * (G[2] + G[6]);
+  o[4] = 0.5 * ((double)G[1] + (double)G[3]);
+  o[5] = 0.5 * ((double)G[2] + (double)G[6]);
   o[6] = G[4];
-  o[7] = S(0.5) * (G[5] + G[7]);
+  o[7] = 0.5 * ((double)G[5] + (double)G[7]);
   o[8] = G[8];
   o[9] = gcol[3 * f]; o[10] = gcol[3 * f + 1]; o[11] = gcol[3 * f + 2];
 }

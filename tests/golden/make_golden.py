@@ -118,6 +118,24 @@ def fit_case(name, iterations=200):
     print(name, hist[0], hist[-1], res.wall_time)
 
 
+def fit_prefix_case(name, iterations=5):
+    """Config 5 cut to a few iterations (the cosine schedule is over
+    `iterations`, so this is its own run): history, vertices and colours for
+    a tight short-horizon parity check before the trajectory turns chaotic."""
+    from meshsplat.optim import FitConfig, fit
+    case = gc.fit_case()
+    target = ref_mesh(case["target"])
+    cams = [ref_cam(c) for c in case["cameras"]]
+    views = [ms.render_mesh(target, c, dtype=np.float64) for c in cams]
+    init = ref_mesh(case["init"])
+    cfg = FitConfig(iterations=iterations, batch_size=1, seed=0, log_every=0, lr_positions=1e-2)
+    res = fit(init, cams, [v.rgb for v in views], [v.alpha for v in views], cfg)
+    hist = np.array([[h["total"], h["color"], h["silhouette"], h["edge"], h["laplacian"]] for h in res.history])
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), history=hist, vertices=res.mesh.vertices,
+                        colors=res.mesh.colors)
+    print(name, hist[:, 0])
+
+
 if __name__ == "__main__":
     render_case("c1_icosphere1280_128", gc.c1_case())
     render_case("octahedron_32", gc.octahedron_case())
@@ -128,3 +146,4 @@ if __name__ == "__main__":
     convert_case("convert_random50", gc.convert_case())
     if "--fit" in sys.argv:
         fit_case("fit_c5_200")
+        fit_prefix_case("fit_c5_5", 5)

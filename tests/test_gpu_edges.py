@@ -1,0 +1,132 @@
+"""Edge cases of the boundary and the binning pipeline (float64 vs oracle)."""
+
+import numpy as np
+import pytest
+
+import golden_cases as gc
+from oracle import gmr_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return float(np.abs(a - b).max() / max(1.0, np.abs(b).max()))
+
+
+def test_empty_mesh_renders_background(gmr):
+    mesh = gmr.TriangleMesh(np.zeros((3, 3)), np.zeros((0, 3), int))
+    cam = gc.identity_camera()
+    out, ctx = gmr.render_mesh(mesh, cam, background=(0.2, 0.4, 0.6), return_ctx=True)
+    assert np.allclose(out.rgb, (0.2, 0.4, 0.6)) and np.all(out.alpha == 0)
+    gv, gcol = gmr.render_backward(ctx, np.ones((32, 32, 3)), np.ones((32, 32)))
+    assert np.all(gv == 0) and np.all(gcol == 0)
+
+
+def test_everything_culled(gmr):
+    """reference test_render.py:433-440: mesh behind the camera."""
+    m = gmr.make_icosphere(80)
+    behind = m.with_vertices(np.asarray(m.vertices) + np.array([0, 0, -10.0]))
+    cam = gmr.Camera(rotation=np.eye(3), translation=np.zeros(3), fx=40, fy=40, cx=15.5, cy=15.5, width=32, height=32)
+    out, ctx = gmr.render_mesh(behind, cam, background=(0.1, 0.2, 0.3), return_ctx=True)
+    assert np.allclose(out.rgb, (0.1, 0.2, 0.3)) and np.all(out.alpha == 0)
+    gv, _ = gmr.render_backward(ctx, np.ones((32, 32, 3)), np.ones((32, 32)))
+    assert np.all(gv == 0)
+
+
+def test_many_views_one_call_chunks_cameras(gmr):
+    """70 views (> 64 per K1/K5 launch) in one device call == serial reference loop."""
+    import torch
+    from paper_2602_14493_b200 import engine
+    m = gmr.make_icosphere(80)
+    mesh = gmr.TriangleMesh(m.vertices, m.facets, gmr.seeded_colors(m.num_vertices, 1))
+    cams = gmr.sphere_views(70, 2.8, 24)
+    rng = np.random.default_rng(9)
+    g_rgb, g_a = rng.normal(size=(70, 24, 24, 3)), rng.normal(size=(70, 24, 24))
+    pos, col, faces = gmr.api._device_mesh(mesh, np.float64)
+    rgb, alpha, st = engine.render_forward(pos, col, faces, cams, 24, 24, (0.1, 0.1, 0.1))
+    gp, gcol = engine.render_backward(st, pos, col, faces, rgb, torch.as_tensor(g_rgb).cuda(),
+                                      torch.as_tensor(g_a).cuda())
+    ogv = np.zeros_like(mesh.vertices)
+    for v in (0, 33, 64, 69):
+        r, a, _ = orc.render(mesh.vertices, mesh.facets, mesh.colors, cams[v], (0.1, 0.1, 0.1))
+        assert np.abs(rgb[v].cpu().numpy() - r).max() <= 1e-10
+    for v, cam in enumerate(cams):
+        r, a, ctx = orc.render(mesh.vertices, mesh.facets, mesh.colors, cam, (0.1, 0.1, 0.1))
+        ogv += orc.render_grad(ctx, g_rgb[v], g_a[v])[0]
+    assert rel(gp.cpu().numpy(), ogv) <= 1e-8
+
+
+def test_large_partial_tile_image(gmr):
+    """Non-multiple-of-16 image (partial tiles on both edges), f64 vs oracle."""
+    m = gmr.make_geodesic_sphere(6, seed=4)
+    cam = gmr.look_at((0.2, -2.9, 0.7), (0, 0, 0), **gmr.default_intrinsics(301, 187))
+    rng = np.random.default_rng(10)
+    g_rgb, g_a = rng.normal(size=(187, 301, 3)), rng.normal(size=(187, 301))
+    out, ctx = gmr.render_mesh(m, cam, background=(0.3, 0.3, 0.3), return_ctx=True)
+    r, a, octx = orc.render(m.vertices, m.facets, m.colors, cam, (0.3, 0.3, 0.3))
+    assert np.abs(out.rgb - r).max() <= 1e-10 and np.abs(out.alpha - a).max() <= 1e-10
+    gv, gcol = gmr.render_backward(ctx, g_rgb, g_a)
+    ogv, ogc = orc.render_grad(octx, g_rgb, g_a)
+    assert rel(gv, ogv) <= 1e-8 and rel(gcol, ogc) <= 1e-8
+
+
+def test_capacity_overflow_recovers(gmr):
+    """A forward planned with too small an entry capacity reports the exact
+    count; the engine re-plans and re-runs to the same result."""
+    from paper_2602_14493_b200 import engine
+    case = gc.c1_case()
+    mesh = gmr.TriangleMesh(case["vertices"], case["facets"], case["colors"])
+    pos, col, faces = gmr.api._device_mesh(mesh, np.float64)
+    cam = case["camera"]
+    key = (len(mesh.facets), 1, 128, 128, pos.dtype)
+    ref, _, st0 = engine.render_forward(pos, col, faces, [cam], 128, 128, case["background"])
+    engine._capacity._cap[key] = 17   # far too small
+    rgb, _, st = engine.render_forward(pos, col, faces, [cam], 128, 128, case["background"])
+    assert st.entries == st0.entries == 5997 and st.capacity >= st.entries
+    assert np.array_equal(rgb.cpu().numpy(), ref.cpu().numpy())
+
+
+def test_nan_vertex_is_depth_culled_like_reference(gmr):
+    """A NaN mean fails the strict near < z < far test (render.py:108): the
+    facet is culled, not reported -- same as the oracle."""
+    from paper_2602_14493_b200 import engine
+    import torch
+    m = gmr.make_icosphere(80)
+    v = np.asarray(m.vertices).copy()
+    v[3, 0] = np.nan
+    cam = gmr.look_at((0, 0, 3), (0, 0, 0), **gmr.default_intrinsics(32, 32))
+    pos = torch.tensor(v, device="cuda")
+    col = torch.full_like(pos, 0.5)
+    faces = torch.tensor(np.asarray(m.facets, np.int32), device="cuda")
+    rgb, _, _ = engine.render_forward(pos, col, faces, [cam], 32, 32, (0, 0, 0))
+    cloud = orc.facet_gaussians(v, np.asarray(m.facets), np.full_like(v, 0.5))
+    s = orc.project(cloud, cam)
+    r, _ = orc.composite(s, 32, 32)
+    assert np.abs(rgb[0].cpu().numpy() - r).max() <= 1e-10
+
+
+@pytest.mark.parametrize("scale", [1e19, 1e20, 1e21])
+def test_overflowing_splat_raises_reference_error(gmr, scale):
+    """A finite but enormous sliver overflows its float32 screen covariance
+    while its radius stays +inf, so it is kept: the reference raises
+    ValueError("non-finite splat parameter 'cov2d' at splat 0")
+    (render.py:191-197) for exactly these inputs; so must the device path."""
+    v = np.array([(-scale, 0, 0), (scale, 0, 0), (0, 1, 0)], float)
+    mesh = gmr.TriangleMesh(v, [(0, 1, 2)])
+    cam = gmr.look_at((0.3, 0.2, 3), (0, 0, 0), **gmr.default_intrinsics(32, 32))
+    with pytest.raises(ValueError, match="non-finite splat parameter 'cov2d' at splat 0"):
+        gmr.render_mesh(mesh, cam, dtype=np.float32)
+
+
+def test_backward_shape_errors_match_reference(gmr):
+    case = gc.octahedron_case()
+    mesh = gmr.TriangleMesh(case["vertices"], case["facets"], case["colors"])
+    out, ctx = gmr.render_mesh(mesh, case["camera"], return_ctx=True)
+    with pytest.raises(ValueError, match="upstream gradient shapes"):
+        gmr.render_backward(ctx, np.zeros((31, 32, 3)), np.zeros((32, 32)))
+    cloud = gmr.convert_mesh(mesh)
+    with pytest.raises(ValueError, match="do not match"):
+        gmr.convert_backward(mesh, cloud, np.zeros((7, 3)), np.zeros((8, 3, 3)), np.zeros((8, 3)))
+    with pytest.raises(ValueError, match="unknown conversion path"):
+        gmr.convert_mesh(mesh, path="bogus")
