@@ -42,6 +42,9 @@ CONFIGS = {
                  desc="config3 batch 1: geodesic displaced sphere n=158 (499,280 faces), 800x800"),
     "c4": dict(mesh=("geodesic", 316), res=1024, views=8,
                desc="config4: geodesic displaced sphere n=316 (1,997,120 faces), 1024x1024"),
+    "views": dict(mesh=("geodesic", 158), res=256, views=253,
+                  desc="SURVEY 8f row 3: make_views of the config-3 mesh (499,280 faces), 253 hemisphere views "
+                       "256x256, float64 like the reference, 8-bit images to host"),
     "c5": dict(mesh=("fit", 1280), res=64, views=1,
                desc="config5: 200-iteration batch-1 inverse-rendering loop, icosphere(1280) -> grid cube, 20 views 64x64"),
 }
@@ -411,6 +414,53 @@ def run_fit(args, cfg):
     return line
 
 
+def run_views(args, cfg):
+    """batched forward-only dataset rendering
+    (dataset.render_view_images: device render + fused 8-bit quantisation,
+    images copied to pinned host memory).  One step = all 253 views."""
+    import numpy as np
+    import torch
+    import paper_2602_14493_b200 as gmr
+    from paper_2602_14493_b200 import dataset, lib
+    L = lib.load()
+    mesh = build_mesh(cfg)
+    n, W = cfg["views"], cfg["res"]
+    cams = gmr.hemisphere_cameras(n, 3.0, (W, W))
+    dt = np.float32 if args.views_f32 else np.float64
+    for _ in range(max(1, args.warmup)):
+        dataset.render_view_images(mesh, cams, BG, dt)
+    torch.cuda.synchronize()
+    n0 = L.gmr_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    steps = max(1, args.steps // 4)
+    e0.record()
+    for _ in range(steps):
+        rgb8, a8 = dataset.render_view_images(mesh, cams, BG, dt)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    launches = (L.gmr_launch_count() - n0) // steps
+    cpu = None
+    if not args.no_cpu:
+        from oracle import gmr_oracle as orc
+        t0 = time.perf_counter()
+        orc.render(mesh.vertices, mesh.facets, mesh.colors, cams[0], BG, True, dt)
+        sec = time.perf_counter() - t0
+        cpu = {"value": round(1.0 / sec, 4), "unit": "views/s", "cores": 1, "kind": "port",
+               "sample": f"one view, oracle render (numpy restatement of render_mesh), {sec:.1f} s"}
+    line = {"metric": "make_views forward-only views/s (8-bit images to host)", "value": round(n / (ms / 1e3), 1),
+            "unit": "views/s", "n_gpus": 1, "steps": steps, "warmup": max(1, args.warmup),
+            "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32" if args.views_f32 else "f64", "data": "synthetic (config-3 mesh)",
+            "config": {"workload": cfg["desc"], "views": n, "resolution": [W, W]},
+            "e2e": {"value": round(n / (ms / 1e3), 1), "unit": "views/s",
+                    "h2d_bytes_per_step": int(mesh.vertices.size * 16 + mesh.facets.size * 4),
+                    "d2h_bytes_per_step": int(rgb8.nbytes + a8.nbytes)},
+            "gpu_launches": int(launches), "cpu_baseline": cpu}
+    print(json.dumps(line), flush=True)
+    return line
+
+
 def run_reference(args, cfg):
     """CPU arm: the reference algorithm on the host cores (bounded samples)."""
     rank = int(os.environ.get("RANK", "0"))
@@ -461,12 +511,15 @@ def main():
     ap.add_argument("--cpu-tile-stride", type=int, default=16)
     ap.add_argument("--ref-face-stride", type=int, default=8)
     ap.add_argument("--ref-tile-stride", type=int, default=32)
+    ap.add_argument("--views-f32", action="store_true", help="--config views: render in float32")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg)
     elif args.config == "c5":
         run_fit(args, cfg)
+    elif args.config == "views":
+        run_views(args, cfg)
     else:
         run_gmr(args, cfg)
 

@@ -19,6 +19,7 @@
  *   losses.py:151-162  total_loss view loop          B views per gmr_render_* call
  *   losses.py:43-73    color_loss, silhouette_loss   gmr_render_forward_loss (fused)
  *   losses.py:76-123, optim.py:29-135, :271-295      gmr_fit_step (regularisers + Adam)
+ *   dataset.py:118-164 make_views (render + _save_png) gmr_render_images_u8
  *
  * Scalars: every floating-point buffer is either float32 (GMR_F32, the fast
  * path; `fit`'s default dtype, reference optim.py:161) or float64
@@ -133,6 +134,15 @@ int gmr_render_forward_loss(const GmrMesh* mesh, const GmrCamera* cameras, int32
                             void* rgb, void* alpha, void* g_rgb, void* g_alpha,
                             double* loss_sums, void* workspace, size_t workspace_bytes,
                             int64_t entry_capacity, void* stream);
+
+/* Forward only, 8-bit images: the render of gmr_render_forward quantised in
+ * the blend epilogue exactly as the reference's dataset writer does before
+ * PNG encoding (dataset.py:59-61: np.round(np.clip(float64(x), 0, 1) * 255),
+ * round half to even).  rgb8 [B,H,W,3] and alpha8 [B,H,W] are device uint8.
+ * Same workspace and entry-capacity contract as gmr_render_forward. */
+int gmr_render_images_u8(const GmrMesh* mesh, const GmrCamera* cameras, int32_t num_views,
+                         const GmrRaster* raster, uint8_t* rgb8, uint8_t* alpha8, void* workspace,
+                         size_t workspace_bytes, int64_t entry_capacity, void* stream);
 
 /* ---- device-resident optimisation step (reference optim.py / losses.py) -- */
 

@@ -182,10 +182,16 @@ struct LossArgs {
   double* sums;   // device [2]
 };
 
+// optional 8-bit outputs of a forward (dataset rendering)
+struct ImageArgs {
+  uint8_t* rgb8;
+  uint8_t* alpha8;
+};
+
 // Binning (K2) + blend forward (K3) over prepared item records.
 template <typename S>
 int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void* alpha,
-                  cudaStream_t st, const LossArgs* la = nullptr) {
+                  cudaStream_t st, const LossArgs* la = nullptr, const ImageArgs* ia = nullptr) {
   typedef typename KeyOf<S>::type K;
   const uint32_t items = (uint32_t)L.items;
   // depth order of all items (stable: ties keep item = (view, face) order)
@@ -265,6 +271,10 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
     a.g_alpha_out = (S*)la->g_alpha;
     a.loss_tile = at<double>(ws, L.loss_tile);
   }
+  if (ia) {
+    a.rgb8 = ia->rgb8;
+    a.alpha8 = ia->alpha8;
+  }
   if (L.bins) {
     StageScope sc(kStBlendFwd, st);
     blend_forward<S><<<(unsigned)L.bins, kBlendThreads, 0, st>>>(a);
@@ -279,7 +289,8 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
 
 template <typename S>
 int render_forward_t(const GmrMesh* m, const GmrCamera* cams, int B, const GmrRaster* r, void* rgb,
-                     void* alpha, void* ws, const Layout& L, cudaStream_t st, const LossArgs* la = nullptr) {
+                     void* alpha, void* ws, const Layout& L, cudaStream_t st, const LossArgs* la = nullptr,
+                     const ImageArgs* ia = nullptr) {
   reset_status<<<1, 1, 0, st>>>(at<DevStatus>(ws, L.status));
   GMR_LAUNCHED();
   const uint64_t F = L.faces;
@@ -311,7 +322,7 @@ int render_forward_t(const GmrMesh* m, const GmrCamera* cams, int B, const GmrRa
       GMR_LAUNCHED();
     }
   }
-  return bin_and_blend<S>(L, ws, r, rgb, alpha, st, la);
+  return bin_and_blend<S>(L, ws, r, rgb, alpha, st, la, ia);
 }
 
 template <typename S, bool kOpacity>
@@ -550,6 +561,22 @@ int gmr_render_forward_loss(const GmrMesh* mesh, const GmrCamera* cams, int32_t 
   cudaStream_t st = (cudaStream_t)stream;
   if (r->dtype == GMR_F64) return render_forward_t<double>(mesh, cams, B, r, rgb, alpha, ws, L, st, &la);
   return render_forward_t<float>(mesh, cams, B, r, rgb, alpha, ws, L, st, &la);
+}
+
+int gmr_render_images_u8(const GmrMesh* mesh, const GmrCamera* cams, int32_t B, const GmrRaster* r,
+                         uint8_t* rgb8, uint8_t* alpha8, void* ws, size_t ws_bytes, int64_t ecap, void* stream) {
+  int rc = check_mesh(mesh);
+  if (rc) return rc;
+  if ((rc = check_raster(r))) return rc;
+  if (!cams || B < 1 || B > GMR_MAX_VIEWS_PER_CALL) return fail(GMR_EINVAL, "need 1..%d cameras", GMR_MAX_VIEWS_PER_CALL);
+  if (!rgb8 || !alpha8 || !ws) return fail(GMR_EINVAL, "output or workspace pointer is null");
+  if ((uint64_t)mesh->num_faces * B >= 0xffffffffull) return fail(GMR_EINVAL, "faces*views must be < 2^32");
+  const Layout L = plan((uint64_t)mesh->num_faces, B, r->width, r->height, (uint64_t)ecap, r->dtype, true);
+  if (ws_bytes < L.total) return fail(GMR_EWORKSPACE, "workspace has %zu bytes, needs %zu", ws_bytes, L.total);
+  ImageArgs ia{rgb8, alpha8};
+  cudaStream_t st = (cudaStream_t)stream;
+  if (r->dtype == GMR_F64) return render_forward_t<double>(mesh, cams, B, r, nullptr, nullptr, ws, L, st, nullptr, &ia);
+  return render_forward_t<float>(mesh, cams, B, r, nullptr, nullptr, ws, L, st, nullptr, &ia);
 }
 
 int gmr_fit_scratch_size(int64_t V, int64_t E, size_t* bytes) {

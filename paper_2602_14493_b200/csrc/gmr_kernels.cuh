@@ -467,7 +467,17 @@ template <typename S> struct BlendArgs {
   S* g_rgb_out;            // [B,H,W,3] dL/drgb (pre-scaled), read by K4
   S* g_alpha_out;          // [B,H,W]
   double* loss_tile;       // [bins][2]: sum of squared colour error, sum of BCE
+  // optional 8-bit images (dataset.py:59-61 `_save_png`); rgb/alpha may then be null
+  uint8_t* rgb8;           // [B,H,W,3]
+  uint8_t* alpha8;         // [B,H,W]
 };
+
+// np.round(np.clip(float64(x), 0, 1) * 255).astype(uint8) (dataset.py:60-61):
+// float64 clip and product, round half to even (rint); NaN maps to 0.
+__device__ __forceinline__ uint8_t png_level(double x) {
+  if (!(x == x)) return 0;
+  return (uint8_t)rint(fmin(fmax(x, 0.0), 1.0) * 255.0);
+}
 
 constexpr double kBceClamp = 1e-6;   // losses.py:20
 
@@ -751,10 +761,18 @@ __global__ void __launch_bounds__(kBlendThreads) blend_forward(BlendArgs<S> p) {
     out[0] = ar + T * p.bg0;
     out[1] = ag + T * p.bg1;
     out[2] = ab + T * p.bg2;
-    p.rgb[3 * pix + 0] = out[0];
-    p.rgb[3 * pix + 1] = out[1];
-    p.rgb[3 * pix + 2] = out[2];
-    p.alpha[pix] = one - T;
+    if (p.rgb) {
+      p.rgb[3 * pix + 0] = out[0];
+      p.rgb[3 * pix + 1] = out[1];
+      p.rgb[3 * pix + 2] = out[2];
+      p.alpha[pix] = one - T;
+    }
+    if (p.rgb8) {
+      p.rgb8[3 * pix + 0] = png_level((double)out[0]);
+      p.rgb8[3 * pix + 1] = png_level((double)out[1]);
+      p.rgb8[3 * pix + 2] = png_level((double)out[2]);
+      p.alpha8[pix] = png_level((double)(one - T));
+    }
     p.t_final[pix] = T;
     if (p.target_rgb) pixel_loss(p, pix, out, one - T, sq, bce);
   }

@@ -207,6 +207,34 @@ def render_forward_loss(pos, col, faces, cams, width, height, background, target
     raise RuntimeError("tile-entry capacity did not converge")
 
 
+def render_images_u8(pos, col, faces, cams, width, height, background, rescale=True):
+    """B-view forward straight to 8-bit images (rgb8 [B,H,W,3], alpha8
+    [B,H,W] uint8 on the device), quantised in the blend epilogue the way
+    the reference's dataset writer does (dataset.py:59-61)."""
+    lib = L.load()
+    dtype = pos.dtype
+    B, F = len(cams), int(faces.shape[0])
+    raster = raster_struct(width, height, background, dtype, rescale, 0)
+    cam_arr = L.camera_struct(cams)
+    mesh = mesh_struct(pos, col, faces)
+    key = (F, B, int(width), int(height), dtype)
+    cap = _capacity.get(key, F * B)
+    rgb8 = torch.empty((B, height, width, 3), dtype=torch.uint8, device=pos.device)
+    a8 = torch.empty((B, height, width), dtype=torch.uint8, device=pos.device)
+    for _ in range(3):
+        nb = ctypes.c_size_t()
+        L.check(lib.gmr_render_workspace_size(F, B, width, height, cap, raster.dtype, ctypes.byref(nb)))
+        ws = torch.empty(nb.value, dtype=torch.uint8, device=pos.device)
+        L.check(lib.gmr_render_images_u8(ctypes.byref(mesh), cam_arr, B, ctypes.byref(raster), _ptr(rgb8),
+                                         _ptr(a8), _ptr(ws), nb.value, cap, _stream()))
+        st, code = _status_or_raise(ws, "mesh")
+        if code == L.GMR_OK:
+            _capacity.note(key, cap, st.entries)
+            return rgb8, a8
+        cap = _capacity.grow(key, st.entries)
+    raise RuntimeError("tile-entry capacity did not converge")
+
+
 class CapacityExceeded(RuntimeError):
     """A deferred-check forward needed more tile entries than it was planned
     for; its outputs are invalid.  The capacity has been raised: re-run."""

@@ -143,3 +143,15 @@ def fit_case():
     target = make_grid_cube_normalized(4)
     init = make_icosphere(1280)
     return dict(target=_mesh_dict(target), init=_mesh_dict(init), cameras=sphere_views(20, 3.0, 64))
+
+
+def views_case():
+    """SURVEY §8f row 3 (make_views, dataset.py:118-164): a seeded-colour
+    icosphere(320) stretched off-centre (so normalize_mesh does work), 13
+    hemisphere views at 64x48 on a non-black background (13 > HOLDOUT_STRIDE:
+    two hold-out views)."""
+    m = make_icosphere(320)
+    v = m.vertices * np.array([1.3, 0.8, 1.0]) + np.array([0.2, -0.1, 0.05])
+    col = np.random.default_rng(7).random((len(v), 3)) * 0.8 + 0.1
+    return dict(vertices=v, facets=m.facets, colors=col, n_views=13, resolution=(64, 48),
+                radius=3.0, background=(0.1, 0.2, 0.3))

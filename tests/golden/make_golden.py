@@ -118,6 +118,30 @@ def fit_case(name, iterations=200):
     print(name, hist[0], hist[-1], res.wall_time)
 
 
+def views_case(name):
+    """make_views (dataset.py:118-164) into a temp dir: the decoded 8-bit
+    images, the SHA-256 of every written file, and the text files."""
+    import hashlib
+    import tempfile
+    c = gc.views_case()
+    with tempfile.TemporaryDirectory() as d:
+        ds = ms.make_views(ms.TriangleMesh(c["vertices"], c["facets"], c["colors"]), n_views=c["n_views"],
+                           resolution=c["resolution"], radius=c["radius"], out_dir=d,
+                           background=c["background"])
+        from PIL import Image
+        rgb = np.array([np.asarray(Image.open(p)) for p in ds.rgb_paths])
+        mask = np.array([np.asarray(Image.open(p)) for p in ds.mask_paths])
+        names = sorted(os.listdir(d))
+        sha = np.array([hashlib.sha256(open(os.path.join(d, n), "rb").read()).hexdigest() for n in names])
+        cams = open(os.path.join(d, "cameras.txt")).read()
+        meta = open(os.path.join(d, "metadata.txt")).read()
+        ply = open(os.path.join(d, "target_mesh.ply")).read()
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), rgb=rgb, mask=mask, names=np.array(names), sha=sha,
+                        cameras_txt=np.array(cams), metadata_txt=np.array(meta), ply_txt=np.array(ply),
+                        train=np.array(ds.train_indices), holdout=np.array(ds.holdout_indices))
+    print(name, rgb.shape, mask.shape, len(names))
+
+
 def fit_prefix_case(name, iterations=5):
     """Config 5 cut to a few iterations (the cosine schedule is over
     `iterations`, so this is its own run): history, vertices and colours for
@@ -144,6 +168,7 @@ if __name__ == "__main__":
     splat_case("splats_closed_form_32", gc.closed_form_splat_case())
     loss_case("loss_octa_3views_16", gc.loss_case())
     convert_case("convert_random50", gc.convert_case())
+    views_case("views_ico320_13")
     if "--fit" in sys.argv:
         fit_case("fit_c5_200")
         fit_prefix_case("fit_c5_5", 5)
