@@ -20,6 +20,9 @@
  *   losses.py:43-73    color_loss, silhouette_loss   gmr_render_forward_loss (fused)
  *   losses.py:76-123, optim.py:29-135, :271-295      gmr_fit_step (regularisers + Adam)
  *   dataset.py:118-164 make_views (render + _save_png) gmr_render_images_u8
+ *   convert.py:497-532 export_gaussians              gmr_export_gaussians
+ *   metrics.py:40-86   chamfer / normal consistency  gmr_chamfer_nc, gmr_nearest
+ *   metrics.py:89-172  psnr, ssim, image_metrics     gmr_image_metrics
  *
  * Scalars: every floating-point buffer is either float32 (GMR_F32, the fast
  * path; `fit`'s default dtype, reference optim.py:161) or float64
@@ -258,6 +261,58 @@ int gmr_convert_backward(const GmrMesh* mesh, int32_t rescale, int32_t dtype,
                          const void* grad_colors, void* grad_positions, void* grad_colors_v,
                          const void* topology, void* scratch, size_t scratch_bytes, void* stream);
 int gmr_convert_scratch_size(int64_t num_faces, int32_t dtype, size_t* bytes);
+
+/* ---- export and evaluation (all float64 inputs) ------- */
+
+/* export_gaussians (convert.py:497-532): per Gaussian, the 14 float32 fields
+ * of the splat-viewer PLY record (x y z, f_dc_0..2, opacity logit, log
+ * scale_0..2, rot_0..3 = unit quaternion w x y z with w >= 0), from means
+ * [n,3], cov3d [n,3,3] (lower triangle read, as eigh does), colors [n,3],
+ * opacities [n].  records [n,14] on the device; the caller writes the header.
+ * Eigenvectors of repeated eigenvalues are not unique, so rot/scale match the
+ * reference as a factorisation (R diag(s^2) R^T = cov3d), not bit for bit. */
+int gmr_export_gaussians(const double* means, const double* cov3d, const double* colors,
+                         const double* opacities, int64_t n, float* records, void* stream);
+
+/* sample_surface (mesh.py:560-622) in two steps.  gmr_surface_prepare: per
+ * facet area / unit normal (placeholder (0,0,1) below area 1e-12) / sorted
+ * corner indices, the total area as numpy's pairwise sum and the CDF as the
+ * sequential cumsum / total -- all with numpy's float64 rounding -- into
+ * `prep` (device); total_out (device, may be null) gets the total area.
+ * gmr_surface_sample: for n uniform triples u (device [n,3], the reference's
+ * Philox stream), facet = searchsorted(cdf, u0, 'left') clipped to F-1,
+ * (u1, u2) folded when u1 + u2 > 1, point = a + b1 (b - a) + b2 (c - a) over
+ * the sorted corners, normal = the facet normal. */
+int gmr_surface_prepare_size(int64_t num_faces, size_t* bytes);
+int gmr_surface_prepare(const double* positions, const int32_t* faces, int64_t num_vertices,
+                        int64_t num_faces, void* prep, size_t prep_bytes, double* total_out, void* stream);
+int gmr_surface_sample(const double* positions, int64_t num_faces, const void* prep,
+                       const double* uniforms, int64_t n, double* points, double* normals, void* stream);
+
+/* cKDTree(points).query(queries) by exact float64 brute force:
+ * d2[i] = (distance to the nearest point)^2 computed as cKDTree returns it
+ * (sqrt of ((dx^2 + dy^2) + dz^2), then squared), index[i] its point index
+ * (ties: lowest index).  index may be null. */
+int gmr_nearest_scratch_size(int64_t n_queries, int64_t n_points, size_t* bytes);
+int gmr_nearest(const double* queries, int64_t n_queries, const double* points, int64_t n_points,
+                double* d2, int32_t* index, void* scratch, size_t scratch_bytes, void* stream);
+
+/* One Chamfer / normal-consistency pass (metrics.py:40-46, 69-77) between
+ * sample sets a and b: out4 (device) = (mean d2 a->b, mean d2 b->a,
+ * mean |n_a . n_nn(a)|, mean |n_b . n_nn(b)|).  Normals may be null (then
+ * out4[2..3] are not written). */
+int gmr_chamfer_scratch_size(int64_t n_a, int64_t n_b, size_t* bytes);
+int gmr_chamfer_nc(const double* points_a, const double* normals_a, int64_t n_a,
+                   const double* points_b, const double* normals_b, int64_t n_b, double* out4,
+                   void* scratch, size_t scratch_bytes, void* stream);
+
+/* PSNR / SSIM inputs (metrics.py:89-160) for B image pairs [B,H,W,C]:
+ * mse[b] = mean squared difference (PSNR = min(10 log10(1/mse), 99) on the
+ * host), ssim[b] = channel-averaged single-scale SSIM (11-tap Gaussian,
+ * sigma 1.5, reflect borders, interior mean).  ssim may be null. */
+int gmr_image_metrics_scratch_size(int32_t B, int32_t H, int32_t W, int32_t C, size_t* bytes);
+int gmr_image_metrics(const double* a, const double* b, int32_t B, int32_t H, int32_t W, int32_t C,
+                      double* mse, double* ssim, void* scratch, size_t scratch_bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -13,7 +13,7 @@ from .mesh import MeshError, TriangleMesh, make_geodesic_sphere, make_icosphere,
 _API = ("RenderOutput", "RenderContext", "Splat2D", "GaussianCloud", "LossWeights", "LossReport",
         "render_mesh", "render_backward", "rasterize", "rasterize_backward", "convert_mesh",
         "convert_backward", "total_loss", "color_loss", "silhouette_loss", "edge_length_loss",
-        "laplacian_loss", "ALPHA_CLAMP", "CONTRIB_FLOOR", "TRANSMITTANCE_STOP", "DILATION", "TILE")
+        "laplacian_loss", "export_gaussians", "ALPHA_CLAMP", "CONTRIB_FLOOR", "TRANSMITTANCE_STOP", "DILATION", "TILE")
 _ENGINE = ("render_views", "GMRRender")
 
 
@@ -26,7 +26,7 @@ def __getattr__(name):
     if name in _ENGINE:
         from . import engine
         return getattr(engine, name)
-    if name in ("api", "engine", "parallel"):
+    if name in ("api", "engine", "parallel", "metrics", "dataset", "fit"):
         import importlib
         return importlib.import_module(f".{name}", __name__)
     raise AttributeError(name)

@@ -257,6 +257,34 @@ def convert_mesh(mesh, path: str = "embed", rescale: bool = True) -> GaussianClo
                          opacities=np.ones(m), degenerate=degen.cpu().numpy(), path="embed", rescale=rescale)
 
 
+EXPORT_PROPS = ("x", "y", "z", "f_dc_0", "f_dc_1", "f_dc_2", "opacity", "scale_0", "scale_1", "scale_2",
+                "rot_0", "rot_1", "rot_2", "rot_3")
+
+
+def export_gaussians(cloud, path) -> None:
+    """Splat-viewer PLY (binary little-endian, 14 float32 per Gaussian)
+    (convert.py:484-532).  The per-Gaussian eigendecomposition, quaternion,
+    logit and SH-DC terms run on the device (gmr_export_gaussians); the host
+    writes the header and the record bytes."""
+    import ctypes
+
+    from . import lib as L
+    n = len(cloud.means)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    t = lambda x, shape: torch.tensor(np.ascontiguousarray(np.asarray(x, np.float64).reshape(shape)), device=dev)
+    means, cov = t(cloud.means, (n, 3)), t(cloud.cov3d, (n, 3, 3))
+    cols, ops = t(cloud.colors, (n, 3)), t(cloud.opacities, (n,))
+    rec = torch.empty((n, len(EXPORT_PROPS)), dtype=torch.float32, device=dev)
+    L.check(L.load().gmr_export_gaussians(means.data_ptr(), cov.data_ptr(), cols.data_ptr(), ops.data_ptr(), n,
+                                          rec.data_ptr(), ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    head = ["ply", "format binary_little_endian 1.0", f"element vertex {n}"]
+    head += [f"property float {p}" for p in EXPORT_PROPS] + ["end_header"]
+    body = rec.cpu().numpy().astype("<f4").tobytes()
+    with open(path, "wb") as fh:
+        fh.write(("\n".join(head) + "\n").encode("ascii"))
+        fh.write(body)
+
+
 def convert_backward(mesh, cloud, grad_means, grad_cov3ds, grad_colors):
     """Facet grads -> vertex grads in np.add.at order (convert.py:371-437)."""
     if getattr(cloud, "path", "embed") != "embed":

@@ -16,6 +16,7 @@
 
 #include "gmr_kernels.cuh"
 #include "gmr_train.cuh"
+#include "gmr_eval.cuh"
 
 using namespace gmr;
 
@@ -838,6 +839,224 @@ int gmr_convert_backward(const GmrMesh* mesh, int32_t rescale, int32_t dtype, co
   cudaStream_t st = (cudaStream_t)stream;
   if (dtype == GMR_F64) return convert_backward_t<double>(mesh, rescale, gm, gc, gcol, gp, gcv, topo, scratch, st);
   return convert_backward_t<float>(mesh, rescale, gm, gc, gcol, gp, gcv, topo, scratch, st);
+}
+
+// ---- export and evaluation metrics ------------------------
+
+int gmr_export_gaussians(const double* means, const double* cov3d, const double* colors, const double* opacities,
+                         int64_t n, float* records, void* stream) {
+  if (n < 0) return fail(GMR_EINVAL, "negative count");
+  if (n == 0) return GMR_OK;
+  if (!means || !cov3d || !colors || !opacities || !records) return fail(GMR_EINVAL, "null pointer argument");
+  export_records<<<grid_for((uint64_t)n, 128), 128, 0, (cudaStream_t)stream>>>(means, cov3d, colors, opacities, n,
+                                                                               records);
+  GMR_LAUNCHED();
+  return GMR_OK;
+}
+
+namespace {
+int nn_chunks(int64_t n, int64_t m) {
+  const int64_t qblocks = (n + kNnThreads * kNnQ - 1) / (kNnThreads * kNnQ);
+  int64_t c = (4 * 148 + qblocks - 1) / std::max<int64_t>(qblocks, 1);
+  c = std::min<int64_t>(c, std::max<int64_t>(1, (m + kNnTile - 1) / kNnTile));
+  return (int)std::max<int64_t>(1, std::min<int64_t>(c, 64));
+}
+size_t nn_bytes(int64_t n, int64_t m) {
+  const int c = nn_chunks(n, m);
+  return align_up((size_t)c * n * 8) + align_up((size_t)c * n * 4);
+}
+int nn_run(const double* q, int64_t n, const double* pts, int64_t m, const double* qn, const double* pn,
+           double* d2, double* cosv, int32_t* idx, void* scratch, cudaStream_t st) {
+  const int c = nn_chunks(n, m);
+  const int64_t chunk = (m + c - 1) / c;
+  double* bd = (double*)scratch;
+  int32_t* bi = (int32_t*)((char*)scratch + align_up((size_t)c * n * 8));
+  dim3 grid((unsigned)((n + kNnThreads * kNnQ - 1) / (kNnThreads * kNnQ)), (unsigned)c);
+  nn_partial<<<grid, kNnThreads, 0, st>>>(q, n, pts, m, chunk, bd, bi);
+  GMR_LAUNCHED();
+  nn_merge<<<grid_for((uint64_t)n, 256), 256, 0, st>>>(bd, bi, n, c, qn, pn, d2, cosv, idx);
+  GMR_LAUNCHED();
+  return GMR_OK;
+}
+constexpr int kSumBlocks = 148;
+}  // namespace
+
+int gmr_nearest_scratch_size(int64_t n, int64_t m, size_t* bytes) {
+  if (!bytes || n < 0 || m < 1) return fail(GMR_EINVAL, "bad sizes");
+  *bytes = nn_bytes(n, m);
+  return GMR_OK;
+}
+
+int gmr_nearest(const double* queries, int64_t n, const double* points, int64_t m, double* d2, int32_t* index,
+                void* scratch, size_t scratch_bytes, void* stream) {
+  if (n < 0 || m < 1) return fail(GMR_EINVAL, "need n >= 0 queries and m >= 1 points");
+  if (n == 0) return GMR_OK;
+  if (!queries || !points || !d2 || !scratch) return fail(GMR_EINVAL, "null pointer argument");
+  if (m >= 0x7fffffff) return fail(GMR_EINVAL, "too many points");
+  if (scratch_bytes < nn_bytes(n, m)) return fail(GMR_EWORKSPACE, "scratch too small");
+  return nn_run(queries, n, points, m, nullptr, nullptr, d2, nullptr, index, scratch, (cudaStream_t)stream);
+}
+
+int gmr_chamfer_scratch_size(int64_t na, int64_t nb, size_t* bytes) {
+  if (!bytes || na < 1 || nb < 1) return fail(GMR_EINVAL, "bad sizes");
+  const int64_t mx = std::max(na, nb);
+  *bytes = std::max(nn_bytes(na, nb), nn_bytes(nb, na)) + 2 * align_up((size_t)mx * 8) + align_up(kSumBlocks * 8);
+  return GMR_OK;
+}
+
+int gmr_chamfer_nc(const double* pts_a, const double* nrm_a, int64_t na, const double* pts_b, const double* nrm_b,
+                   int64_t nb, double* out4, void* scratch, size_t scratch_bytes, void* stream) {
+  if (na < 1 || nb < 1) return fail(GMR_EINVAL, "need at least one sample on each side");
+  if (!pts_a || !pts_b || !out4 || !scratch) return fail(GMR_EINVAL, "null pointer argument");
+  if (na >= 0x7fffffff || nb >= 0x7fffffff) return fail(GMR_EINVAL, "too many samples");
+  size_t need;
+  gmr_chamfer_scratch_size(na, nb, &need);
+  if (scratch_bytes < need) return fail(GMR_EWORKSPACE, "scratch too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t mx = std::max(na, nb);
+  char* base = (char*)scratch;
+  const size_t nnb = std::max(nn_bytes(na, nb), nn_bytes(nb, na));
+  double* d2 = (double*)(base + nnb);
+  double* cs = (double*)(base + nnb + align_up((size_t)mx * 8));
+  double* part = (double*)(base + nnb + 2 * align_up((size_t)mx * 8));
+  const bool normals = nrm_a && nrm_b;
+  // a -> b: out[0] = mean d^2, out[2] = mean |cos|; b -> a: out[1], out[3]
+  for (int dir = 0; dir < 2; ++dir) {
+    const double* q = dir ? pts_b : pts_a;
+    const double* p = dir ? pts_a : pts_b;
+    const int64_t n = dir ? nb : na, m = dir ? na : nb;
+    int rc = nn_run(q, n, p, m, normals ? (dir ? nrm_b : nrm_a) : nullptr, normals ? (dir ? nrm_a : nrm_b) : nullptr,
+                    d2, normals ? cs : nullptr, nullptr, scratch, st);
+    if (rc) return rc;
+    block_sums<<<kSumBlocks, 256, 0, st>>>(d2, n, part);
+    GMR_LAUNCHED();
+    final_sum<<<1, 32, 0, st>>>(part, kSumBlocks, 1.0 / (double)n, out4 + dir);
+    GMR_LAUNCHED();
+    if (normals) {
+      block_sums<<<kSumBlocks, 256, 0, st>>>(cs, n, part);
+      GMR_LAUNCHED();
+      final_sum<<<1, 32, 0, st>>>(part, kSumBlocks, 1.0 / (double)n, out4 + 2 + dir);
+      GMR_LAUNCHED();
+    }
+  }
+  return GMR_OK;
+}
+
+int gmr_surface_prepare_size(int64_t F, size_t* bytes) {
+  if (!bytes || F < 1 || F > kSurfaceMaxFaces) return fail(GMR_EINVAL, "need 1..%lld facets", (long long)kSurfaceMaxFaces);
+  *bytes = 4 * align_up(F * 8) + align_up(F * 24) + align_up(F * 12) + align_up(64) + align_up(kPwMaxLeaves * 16);
+  return GMR_OK;
+}
+
+namespace {
+struct SurfaceLayout {
+  double *area, *cdf, *total, *nrm;
+  int32_t* fsorted;
+  int64_t* leaf_off;
+  double* leaf_sum;
+};
+SurfaceLayout surface_layout(void* prep, int64_t F) {
+  char* b = (char*)prep;
+  SurfaceLayout L;
+  L.area = (double*)b; b += align_up(F * 8);
+  L.cdf = (double*)b; b += align_up(F * 8);
+  L.nrm = (double*)b; b += align_up(F * 24);
+  L.fsorted = (int32_t*)b; b += align_up(F * 12);
+  L.total = (double*)b; b += align_up(64);
+  L.leaf_off = (int64_t*)b; b += align_up(kPwMaxLeaves * 8);
+  L.leaf_sum = (double*)b;
+  return L;
+}
+}  // namespace
+
+int gmr_surface_prepare(const double* positions, const int32_t* faces, int64_t V, int64_t F, void* prep,
+                        size_t prep_bytes, double* total_out, void* stream) {
+  size_t need;
+  int rc = gmr_surface_prepare_size(F, &need);
+  if (rc) return rc;
+  if (!positions || !faces || !prep || V < 1) return fail(GMR_EINVAL, "null or empty argument");
+  if (prep_bytes < need) return fail(GMR_EWORKSPACE, "prepared buffer too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  SurfaceLayout L = surface_layout(prep, F);
+  surface_faces<<<grid_for((uint64_t)F, 256), 256, 0, st>>>(positions, faces, F, L.area, L.nrm, L.fsorted);
+  GMR_LAUNCHED();
+  pairwise_total<<<1, kPwThreads, 0, st>>>(L.area, F, L.leaf_off, L.leaf_sum, L.total);
+  GMR_LAUNCHED();
+  cumsum_seq<<<1, 32, 0, st>>>(L.area, F, L.cdf);
+  GMR_LAUNCHED();
+  cdf_divide<<<grid_for((uint64_t)F, 256), 256, 0, st>>>(L.cdf, F, L.total);
+  GMR_LAUNCHED();
+  if (total_out) GMR_CUDA(cudaMemcpyAsync(total_out, L.total, 8, cudaMemcpyDeviceToDevice, st));
+  return GMR_OK;
+}
+
+int gmr_surface_sample(const double* positions, int64_t F, const void* prep, const double* uniforms, int64_t n,
+                       double* points, double* normals, void* stream) {
+  if (F < 1 || F > kSurfaceMaxFaces || n < 0) return fail(GMR_EINVAL, "bad sizes");
+  if (n == 0) return GMR_OK;
+  if (!positions || !prep || !uniforms || !points || !normals) return fail(GMR_EINVAL, "null pointer argument");
+  SurfaceLayout L = surface_layout((void*)prep, F);
+  surface_points<<<grid_for((uint64_t)n, 256), 256, 0, (cudaStream_t)stream>>>(positions, L.fsorted, L.nrm, L.cdf, F,
+                                                                               uniforms, n, points, normals);
+  GMR_LAUNCHED();
+  return GMR_OK;
+}
+
+int gmr_image_metrics_scratch_size(int32_t B, int32_t H, int32_t W, int32_t C, size_t* bytes) {
+  if (!bytes || B < 1 || H < 1 || W < 1 || C < 1) return fail(GMR_EINVAL, "bad sizes");
+  const size_t px = (size_t)B * H * W;
+  *bytes = align_up(px * C * 8) + align_up(px * 5 * 8) + align_up(px * 8) + align_up(kSsimWin * 8);
+  return GMR_OK;
+}
+
+int gmr_image_metrics(const double* a, const double* b, int32_t B, int32_t H, int32_t W, int32_t C, double* mse,
+                      double* ssim, void* scratch, size_t scratch_bytes, void* stream) {
+  if (B < 1 || H < 1 || W < 1 || C < 1) return fail(GMR_EINVAL, "bad image shape");
+  if (!a || !b || !mse || !scratch) return fail(GMR_EINVAL, "null pointer argument");
+  if (ssim && (H < kSsimWin || W < kSsimWin))
+    return fail(GMR_EINVAL, "images must be at least %d pixels on each side", kSsimWin);
+  size_t need;
+  gmr_image_metrics_scratch_size(B, H, W, C, &need);
+  if (scratch_bytes < need) return fail(GMR_EWORKSPACE, "scratch too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t px = (size_t)B * H * W;
+  char* base = (char*)scratch;
+  double* sq = (double*)base;
+  double* tmp = (double*)(base + align_up(px * C * 8));
+  double* smap = (double*)(base + align_up(px * C * 8) + align_up(px * 5 * 8));
+  double* kern = (double*)(base + align_up(px * C * 8) + align_up(px * 5 * 8) + align_up(px * 8));
+  // PSNR: per-image mean squared error (metrics.py:96)
+  sq_diff<<<grid_for(px * C, 256), 256, 0, st>>>(a, b, (int64_t)(px * C), sq);
+  GMR_LAUNCHED();
+  image_sums<<<B, 256, 0, st>>>(sq, (int64_t)H * W * C, 1.0 / ((double)H * W * C), mse, 0);
+  GMR_LAUNCHED();
+  if (!ssim) return GMR_OK;
+  // Gaussian window (metrics.py:102-106) in float64, k / k.sum() with the
+  // sum in numpy's pairwise order for 11 terms (8 lanes, then the tail)
+  static const struct Window {
+    double k[kSsimWin];
+    Window() {
+      for (int i = 0; i < kSsimWin; ++i) {
+        const double x = (double)(i - kSsimHalf);
+        k[i] = exp(-(x * x) / (2.0 * 1.5 * 1.5));
+      }
+      double s = ((k[0] + k[1]) + (k[2] + k[3])) + ((k[4] + k[5]) + (k[6] + k[7]));
+      for (int i = 8; i < kSsimWin; ++i) s += k[i];
+      for (int i = 0; i < kSsimWin; ++i) k[i] /= s;
+    }
+  } window;
+  GMR_CUDA(cudaMemcpyAsync(kern, window.k, sizeof(window.k), cudaMemcpyHostToDevice, st));
+  const double c1 = (0.01 * 1.0) * (0.01 * 1.0), c2 = (0.03 * 1.0) * (0.03 * 1.0);
+  const double inner = (double)(H - 2 * kSsimHalf) * (double)(W - 2 * kSsimHalf);
+  for (int ch = 0; ch < C; ++ch) {
+    ssim_axis0<<<grid_for(px, 256), 256, 0, st>>>(a, b, B, H, W, C, ch, kern, tmp);
+    GMR_LAUNCHED();
+    ssim_axis1<<<grid_for(px, 256), 256, 0, st>>>(tmp, B, H, W, kern, c1, c2, smap);
+    GMR_LAUNCHED();
+    image_sums<<<B, 256, 0, st>>>(smap, (int64_t)H * W, 1.0 / (inner * C), ssim, ch > 0);
+    GMR_LAUNCHED();
+  }
+  return GMR_OK;
 }
 
 }  // extern "C"

@@ -86,6 +86,16 @@ _SIGNATURES = {
     "gmr_render_images_u8": ([P(GmrMesh), P(GmrCamera), c_i32, P(GmrRaster), c_vp, c_vp, c_vp, c_sz, c_i64,
                               c_vp], c_i32),
     "gmr_topology_size": ([c_i64, c_i64, P(c_sz)], c_i32),
+    "gmr_export_gaussians": ([c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp], c_i32),
+    "gmr_surface_prepare_size": ([c_i64, P(c_sz)], c_i32),
+    "gmr_surface_prepare": ([c_vp, c_vp, c_i64, c_i64, c_vp, c_sz, c_vp, c_vp], c_i32),
+    "gmr_surface_sample": ([c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp], c_i32),
+    "gmr_nearest_scratch_size": ([c_i64, c_i64, P(c_sz)], c_i32),
+    "gmr_nearest": ([c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp, c_sz, c_vp], c_i32),
+    "gmr_chamfer_scratch_size": ([c_i64, c_i64, P(c_sz)], c_i32),
+    "gmr_chamfer_nc": ([c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_sz, c_vp], c_i32),
+    "gmr_image_metrics_scratch_size": ([c_i32, c_i32, c_i32, c_i32, P(c_sz)], c_i32),
+    "gmr_image_metrics": ([c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp, c_sz, c_vp], c_i32),
     "gmr_topology_build": ([c_vp, c_i64, c_i64, c_vp, c_sz, c_vp], c_i32),
     "gmr_render_backward": ([P(GmrMesh), P(GmrCamera), c_i32, P(GmrRaster), c_vp, c_vp, c_vp,
                              c_vp, c_vp, c_vp, c_vp, c_sz, c_i64, c_vp], c_i32),

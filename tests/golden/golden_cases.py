@@ -155,3 +155,22 @@ def views_case():
     col = np.random.default_rng(7).random((len(v), 3)) * 0.8 + 0.1
     return dict(vertices=v, facets=m.facets, colors=col, n_views=13, resolution=(64, 48),
                 radius=3.0, background=(0.1, 0.2, 0.3))
+
+
+def eval_case():
+    """a target icosphere(320) and a prediction with seeded
+    vertex noise and one collapsed (degenerate) facet; image pairs of three
+    shapes for PSNR / SSIM."""
+    gt = make_icosphere(320)
+    rng = np.random.default_rng(11)
+    pv = gt.vertices + 0.02 * rng.standard_normal(gt.vertices.shape)
+    pf = np.array(gt.facets)
+    pv[pf[7, 2]] = 0.5 * (pv[pf[7, 0]] + pv[pf[7, 1]])   # facet 7 becomes degenerate
+    col = rng.random((len(pv), 3)) * 0.8 + 0.1
+    imgs = []
+    for shape in ((32, 24, 3), (17, 40), (64, 48, 3)):
+        a = rng.random(shape)
+        b = np.clip(a + 0.05 * rng.standard_normal(shape), 0, 1)
+        imgs.append((a, b))
+    return dict(gt_vertices=gt.vertices, gt_facets=gt.facets, pred_vertices=pv, pred_facets=pf, pred_colors=col,
+                n_samples=3000, images=imgs)

@@ -142,6 +142,42 @@ def views_case(name):
     print(name, rgb.shape, mask.shape, len(names))
 
 
+def eval_case(name):
+    """export_gaussians (convert.py:497-532), sample_surface (mesh.py:580-622),
+    chamfer_distance / normal_consistency (metrics.py:40-86), psnr / ssim /
+    image_metrics (metrics.py:89-172)."""
+    import tempfile
+    from meshsplat import metrics as mt
+    from meshsplat.mesh import sample_surface
+    c = gc.eval_case()
+    gt = ms.TriangleMesh(c["gt_vertices"], c["gt_facets"])
+    pred = ms.TriangleMesh(c["pred_vertices"], c["pred_facets"], c["pred_colors"])
+    n = c["n_samples"]
+    out = {}
+    sp, sn = sample_surface(pred, 70000, seed=3)   # two 2^16-sample chunks
+    sel = np.r_[0:100, 65500:65600, 69900:70000]
+    out["samples_sel"], out["snormals_sel"] = sp[sel], sn[sel]
+    out["samples_sum"] = np.array([sp.sum(), (sp * sp).sum(), sn.sum()])
+    out["cd"] = mt.chamfer_distance(pred, gt, n_samples=n, seed=0)
+    out["nc"] = mt.normal_consistency(pred, gt, n_samples=n, seed=0)
+    out["cd_fixed"] = mt.chamfer_distance(pred, gt, n_samples=n, seed=2, gt_seed=5)
+    out["nc_fixed"] = mt.normal_consistency(pred, gt, n_samples=n, seed=2, gt_seed=5)
+    out["cd_self"] = mt.chamfer_distance(gt, gt, n_samples=n, seed=4, gt_seed=4)
+    for i, (a, b) in enumerate(c["images"]):
+        out[f"psnr{i}"] = mt.psnr(a, b)
+        out[f"ssim{i}"] = mt.ssim(a, b)
+    out["psnr_same"] = mt.psnr(c["images"][0][0], c["images"][0][0])
+    pv, sv = mt.image_metrics([c["images"][0][0], c["images"][2][0]], [c["images"][0][1], c["images"][2][1]])
+    out["im_psnr"], out["im_ssim"] = np.array(pv), np.array(sv)
+    cloud = ms.convert_mesh(pred)
+    with tempfile.TemporaryDirectory() as d:
+        ms.export_gaussians(cloud, os.path.join(d, "g.ply"))
+        out["export_bytes"] = np.frombuffer(open(os.path.join(d, "g.ply"), "rb").read(), np.uint8)
+    out["cloud_cov3d"] = cloud.cov3d
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+    print(name, {k: (np.shape(v) if np.ndim(v) else float(v)) for k, v in out.items()})
+
+
 def fit_prefix_case(name, iterations=5):
     """Config 5 cut to a few iterations (the cosine schedule is over
     `iterations`, so this is its own run): history, vertices and colours for
@@ -169,6 +205,7 @@ if __name__ == "__main__":
     loss_case("loss_octa_3views_16", gc.loss_case())
     convert_case("convert_random50", gc.convert_case())
     views_case("views_ico320_13")
+    eval_case("eval_ico320")
     if "--fit" in sys.argv:
         fit_case("fit_c5_200")
         fit_prefix_case("fit_c5_5", 5)
