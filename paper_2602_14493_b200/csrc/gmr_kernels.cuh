@@ -571,8 +571,12 @@ __device__ __forceinline__ void tile_coverage(const V4<S>& a, const V4<S>& b, in
   }
 }
 
-// 1 / (1 - alpha) with 1 - alpha >= 0.01 (alpha clamp)
-__device__ __forceinline__ float inv_om(float om) { return __fdividef(1.0f, om); }
+// 1 / (1 - alpha) with 1 - alpha >= 0.01 (alpha clamp): no denormal range
+__device__ __forceinline__ float inv_om(float om) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(om));
+  return r;
+}
 __device__ __forceinline__ double inv_om(double om) { return 1.0 / om; }
 
 // Per-pixel alpha of a staged splat (render.py:251-256).  `q` holds the
