@@ -686,6 +686,24 @@ struct BitWalk {
     bits &= bits - 1;
     return c * 32 + k;
   }
+  // Up to two candidates from the current chunk (j2 = -1 if it has only one
+  // left); refills from the next non-empty chunk only when the current one
+  // is exhausted, so the common path is straight-line.  false = done.
+  template <int NB>
+  __device__ __forceinline__ bool pair(const uint32_t (&tw)[NB / 32][kBlendThreads], int& j1, int& j2) {
+    if (__builtin_expect(bits == 0, 0)) {
+      do {
+        if (++c >= nch) return false;
+        bits = tw[c][threadIdx.x];
+      } while (!bits);
+    }
+    const int base = c << 5;
+    j1 = base + __ffs(bits) - 1;
+    bits &= bits - 1;
+    j2 = bits ? base + __ffs(bits) - 1 : -1;
+    bits &= bits - 1;   // no-op when empty
+    return true;
+  }
   __device__ __forceinline__ void stop() { bits = 0; nch = 0; }
 };
 
@@ -716,8 +734,7 @@ __global__ void __launch_bounds__(kBlendThreads) blend_forward(BlendArgs<S> p) {
     it.start<kFwdBatch>(sm.tw, n, done);
     // two candidates per trip: their alphas are independent, only the
     // transmittance update is sequential (front-to-back order kept)
-    for (int j1; (j1 = it.next<kFwdBatch>(sm.tw)) >= 0;) {
-      const int j2 = it.next<kFwdBatch>(sm.tw);
+    for (int j1, j2; it.pair<kFwdBatch>(sm.tw, j1, j2);) {
       const V2<S> m1 = sm.mean[j1];
       S ep, raw;
       const S a1 = Eval<S>::alpha(sub_rn(fpx, m1.x), sub_rn(fpy, m1.y), sm.q[j1], ep, raw);
@@ -912,8 +929,7 @@ __global__ void __launch_bounds__(kBlendThreads, 5) blend_backward(BlendArgs<S> 
       BitWalk it;
       it.start<kBwdBatch>(sm.st.tw, n, done);
       const uint32_t my_word_shift = 8 * (warp & 3);
-      for (int j1; (j1 = it.next<kBwdBatch>(sm.st.tw)) >= 0;) {
-        const int j2 = it.next<kBwdBatch>(sm.st.tw);
+      for (int j1, j2; it.pair<kBwdBatch>(sm.st.tw, j1, j2);) {
         int js[2] = {j1, j2};
         S as[2], eps[2], raws[2];
         {
