@@ -1113,13 +1113,25 @@ __global__ void __launch_bounds__(128) face_views_backward(FaceBwdArgs<S> p, con
 #pragma unroll
     for (int q = 0; q < 12; ++q) acc[q] = p.face_acc[f * 12 + q];
   }
-  for (int vv = 0; vv < p.nviews; ++vv) {
-    const int64_t item = (int64_t)(p.view0 + vv) * p.F + f;
-    const uint32_t cnt = p.count[item];
+  // the face's partials of consecutive views are one contiguous run
+  // (item_offsets: face-major), so only the first offset is loaded; the
+  // counts of a group of 8 views are loaded together, ahead of their use
+  uint32_t off = p.entry_off[(int64_t)p.view0 * p.F + f];
+  for (int v8 = 0; v8 < p.nviews; v8 += 8) {
+   uint32_t cn[8];
+#pragma unroll
+   for (int k = 0; k < 8; ++k)
+     cn[k] = (v8 + k < p.nviews) ? p.count[(int64_t)(p.view0 + v8 + k) * p.F + f] : 0u;
+#pragma unroll
+   for (int k = 0; k < 8; ++k) {
+    const int vv = v8 + k;
+    const uint32_t cnt = cn[k];
     if (!cnt) continue;
-    S s[8];
-    sum_entries(p.partial, p.entry_off[item], cnt, s);
+    const int64_t item = (int64_t)(p.view0 + vv) * p.F + f;
     const Splat<S> rec = p.splat[item];
+    S s[8];
+    sum_entries(p.partial, off, cnt, s);
+    off += cnt;
     S gm[2], g2[3];
     conic_to_cov_grad(s, rec.a.z, rec.a.w, rec.b.x, gm, g2);
     const Cam<S>& cam = cams.cam[vv];
@@ -1167,6 +1179,7 @@ __global__ void __launch_bounds__(128) face_views_backward(FaceBwdArgs<S> p, con
     acc[9] += (double)s[5];
     acc[10] += (double)s[6];
     acc[11] += (double)s[7];
+   }
   }
 #pragma unroll
   for (int q = 0; q < 12; ++q) p.face_acc[f * 12 + q] = acc[q];
