@@ -278,6 +278,10 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
   }
   if (L.bins) {
     StageScope sc(kStBlendFwd, st);
+    // all of the SM's unified L1/shared memory as shared memory: the
+    // default carveout would cap residency below what registers allow
+    GMR_CUDA(cudaFuncSetAttribute(blend_forward<S>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                  (int)cudaSharedmemCarveoutMaxShared));
     blend_forward<S><<<(unsigned)L.bins, kBlendThreads, 0, st>>>(a);
     GMR_LAUNCHED();
   }
@@ -353,6 +357,8 @@ int blend_backward_launch(const Layout& L, void* ws, const GmrRaster* r, const v
   a.partial_op = kOpacity ? at<S>(ws, L.partial_op) : nullptr;
   const size_t dyn = sizeof(BwdSmem<S, kOpacity>);
   GMR_CUDA(cudaFuncSetAttribute(blend_backward<S, kOpacity>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+  GMR_CUDA(cudaFuncSetAttribute(blend_backward<S, kOpacity>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                (int)cudaSharedmemCarveoutMaxShared));
   if (L.bins) {
     StageScope sc(kStBlendBwd, st);
     blend_backward<S, kOpacity><<<(unsigned)L.bins, kBlendThreads, dyn, st>>>(a);

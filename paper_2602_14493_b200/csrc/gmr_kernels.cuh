@@ -708,7 +708,7 @@ struct BitWalk {
 };
 
 template <typename S>
-__global__ void __launch_bounds__(kBlendThreads) blend_forward(BlendArgs<S> p) {
+__global__ void __launch_bounds__(kBlendThreads, 6) blend_forward(BlendArgs<S> p) {
   __shared__ StageSmem<S, kFwdBatch> sm;
   const uint32_t g = blockIdx.x;
   const uint32_t view = g / p.tiles_per_view, t = g % p.tiles_per_view;
