@@ -544,9 +544,15 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
   return x;
 }
 
-// Coverage of one splat in the tile with pixel origin (x0, y0): tile bit
-// y*16 + x, OR-ed row by row into 8 zeroed words `w` (word i = rows 2i,
-// 2i+1; shared memory, so the row index may be dynamic).
+// Pixel layout of a tile CTA: warp w owns the 8x4 block at columns
+// 8 (w & 1) .. +7, rows 4 (w >> 1) .. +3; lane l is column l & 7, row l >> 3
+// of it.  Square blocks keep a warp's lanes on nearly the same splats.
+__device__ __forceinline__ int tile_col(int t) { return ((t >> 2) & 8) + (t & 7); }
+__device__ __forceinline__ int tile_row(int t) { return ((t >> 4) & 12) + ((t >> 3) & 3); }
+
+// Coverage of one splat in the tile with pixel origin (x0, y0), OR-ed row
+// by row into 8 zeroed words `w`: word w holds warp w's 8x4 block, bit
+// 8 (row & 3) + (col & 7) (shared memory, so the indices may be dynamic).
 template <typename S>
 __device__ __forceinline__ void tile_coverage(const V4<S>& a, const V4<S>& b, int x0, int y0, uint32_t* w) {
   const S mx = a.x, my = a.y, ca = a.z, cb = a.w, cc = b.x, ex = b.y, ey = b.z, tau = b.w;
@@ -567,7 +573,9 @@ __device__ __forceinline__ void tile_coverage(const V4<S>& a, const V4<S>& b, in
     if (lo > hi) continue;
     const int ilo = (int)lo, ihi = (int)hi;
     const uint32_t bits = (0xffffu >> (15 - (ihi - ilo))) << ilo;
-    w[r >> 1] |= bits << ((r & 1) * 16);
+    const int wi = (r >> 2) << 1, sh = (r & 3) << 3;
+    w[wi] |= (bits & 0xffu) << sh;
+    w[wi + 1] |= (bits >> 8) << sh;
   }
 }
 
@@ -715,7 +723,7 @@ __global__ void __launch_bounds__(kBlendThreads, 6) blend_forward(BlendArgs<S> p
   const int tx = (int)(t % (uint32_t)p.tiles_x), ty = (int)(t / (uint32_t)p.tiles_x);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int x0 = tx * kTile, y0 = ty * kTile;
-  const int px = x0 + (lane & 15), py = y0 + 2 * warp + (lane >> 4);
+  const int px = x0 + tile_col(threadIdx.x), py = y0 + tile_row(threadIdx.x);
   const bool inside = px < p.W && py < p.H;
   const S fpx = S(px), fpy = S(py);
   const S one = S(1);
@@ -843,7 +851,7 @@ __global__ void __launch_bounds__(kBlendThreads, 5) blend_backward(BlendArgs<S> 
   const int tx = (int)(t % (uint32_t)p.tiles_x), ty = (int)(t / (uint32_t)p.tiles_x);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int x0 = tx * kTile, y0 = ty * kTile;
-  const int px = x0 + (lane & 15), py = y0 + 2 * warp + (lane >> 4);
+  const int px = x0 + tile_col(threadIdx.x), py = y0 + tile_row(threadIdx.x);
   const bool inside = px < p.W && py < p.H;
   const S fpx = S(px), fpy = S(py);
   const S one = S(1);
@@ -997,7 +1005,7 @@ __global__ void __launch_bounds__(kBlendThreads, 5) blend_backward(BlendArgs<S> 
         const Rec s = sm.rec[r];
         const int q = sm.rq[r];
         const V4<S> pd = sm.pix[q];
-        const S dx = ex0 + S(q & 15), dy = ey0 + S(q >> 4);
+        const S dx = ex0 + S(tile_col(q)), dy = ey0 + S(tile_row(q));
         const S dpx = s.x * dx, dpy = s.x * dy;
         acc[0] += dpx;
         acc[1] += dpy;
