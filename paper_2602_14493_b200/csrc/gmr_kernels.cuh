@@ -820,9 +820,9 @@ template <typename S, bool kOpacity> struct BwdSmem {
   uint32_t pre[kBwdBatch][2];       // per entry: covered-pixel count before each row pair (bytes)
   uint32_t off[kBwdBatch + 1];      // per entry: first record (exclusive scan of covered counts)
   uint32_t scan_tmp[8];
-  V4<S> pix[kBlendThreads];         // per pixel: g_r, g_g, g_b
+  V4<S> pix[kBlendThreads];         // per tile pixel (col + 16 row): g_r, g_g, g_b
   Rec rec[kCap];                    // per (entry, covered pixel in row-major order): (dp, w[, dL/dalpha * ep])
-  uint8_t rq[kCap];                 // tile pixel of each record
+  uint8_t rq[kCap];                 // tile pixel (col + 16 row) of each record
 };
 
 // Backward (render.py:294-361).  Per batch of staged entries:
@@ -867,7 +867,10 @@ __global__ void __launch_bounds__(kBlendThreads, 5) blend_backward(BlendArgs<S> 
     Ctot = mypix.x * p.rgb[3 * pix] + mypix.y * p.rgb[3 * pix + 1] + mypix.z * p.rgb[3 * pix + 2] - gbg * tf;
     bterm = (gbg - p.g_alpha[pix]) * tf;
   }
-  sm.pix[tid] = mypix;
+  // per-pixel data and record pixel ids use the natural tile index
+  // col + 16 row (pass 2 recovers the offsets with two bit operations)
+  const int my_pix = tile_col(tid) + 16 * tile_row(tid);
+  sm.pix[my_pix] = mypix;
   S T = one, P = 0;
   bool done = !inside;
   const uint32_t start = p.bounds[g], end = p.bounds[g + 1];
@@ -977,7 +980,7 @@ __global__ void __launch_bounds__(kBlendThreads, 5) blend_backward(BlendArgs<S> 
           const uint32_t r = sm.off[j] + ((pw >> my_word_shift) & 255u) +
                              (uint32_t)__popc(sm.st.cov[j][warp] & lt);
           sm.rec[r] = s;
-          sm.rq[r] = (uint8_t)tid;
+          sm.rq[r] = (uint8_t)my_pix;
           T = test;
         }
         if (stop) {
@@ -1005,7 +1008,7 @@ __global__ void __launch_bounds__(kBlendThreads, 5) blend_backward(BlendArgs<S> 
         const Rec s = sm.rec[r];
         const int q = sm.rq[r];
         const V4<S> pd = sm.pix[q];
-        const S dx = ex0 + S(tile_col(q)), dy = ey0 + S(tile_row(q));
+        const S dx = ex0 + S(q & 15), dy = ey0 + S(q >> 4);
         const S dpx = s.x * dx, dpy = s.x * dy;
         acc[0] += dpx;
         acc[1] += dpy;
