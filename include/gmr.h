@@ -131,6 +131,20 @@ int gmr_render_forward(const GmrMesh* mesh, const GmrCamera* cameras, int32_t nu
  * BCE (scale_rgb = w_c/n, scale_alpha = w_s/n), and loss_sums (device, 2
  * doubles) = (sum of squared colour errors, sum of BCE terms) over all
  * pixels of all views -- divide by 3HW and HW for the per-view means. */
+/* gmr_render_forward with an early status: right after binning has counted
+ * the tile entries (before sorting and blending), the 64-byte status (the
+ * layout gmr_status reads: entries, kept, first non-finite item per field,
+ * overflow flag) is copied to `status_host` (pinned host memory, may be
+ * null) and `status_event` (a cudaEvent_t, may be null) is recorded.  A host
+ * that waits on the event can validate the call (capacity, non-finite input)
+ * while the forward is still blending, and enqueue follow-up work without
+ * draining the stream.  On overflow the remaining stages stay within the
+ * workspace and their outputs are invalid. */
+int gmr_render_forward_ex(const GmrMesh* mesh, const GmrCamera* cameras, int32_t num_views,
+                          const GmrRaster* raster, void* rgb, void* alpha, void* workspace,
+                          size_t workspace_bytes, int64_t entry_capacity, void* status_host,
+                          void* status_event, void* stream);
+
 int gmr_render_forward_loss(const GmrMesh* mesh, const GmrCamera* cameras, int32_t num_views,
                             const GmrRaster* raster, const void* target_rgb,
                             const void* target_mask, double scale_rgb, double scale_alpha,

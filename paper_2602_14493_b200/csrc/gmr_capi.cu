@@ -192,7 +192,8 @@ struct ImageArgs {
 // Binning (K2) + blend forward (K3) over prepared item records.
 template <typename S>
 int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void* alpha,
-                  cudaStream_t st, const LossArgs* la = nullptr, const ImageArgs* ia = nullptr) {
+                  cudaStream_t st, const LossArgs* la = nullptr, const ImageArgs* ia = nullptr,
+                  void* status_host = nullptr, void* status_event = nullptr) {
   typedef typename KeyOf<S>::type K;
   const uint32_t items = (uint32_t)L.items;
   // depth order of all items (stable: ties keep item = (view, face) order)
@@ -218,6 +219,11 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
   }
   scan_top<<<1, 256, 0, st>>>(bsum, nb, dst, (unsigned long long)L.ecap, nent);
   GMR_LAUNCHED();
+  // the status is final here (K1's non-finite items, the entry count and the
+  // capacity verdict): publish it early so the host can validate the call
+  // while the rest of the forward runs
+  if (status_host) GMR_CUDA(cudaMemcpyAsync(status_host, dst, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
+  if (status_event) GMR_CUDA(cudaEventRecord((cudaEvent_t)status_event, st));
   uint32_t* ek[2] = {at<uint32_t>(ws, L.ekey[0]), at<uint32_t>(ws, L.ekey[1])};
   uint32_t* ev[2] = {at<uint32_t>(ws, L.eval[0]), at<uint32_t>(ws, L.eval[1])};
   if (items) {
@@ -295,7 +301,7 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
 template <typename S>
 int render_forward_t(const GmrMesh* m, const GmrCamera* cams, int B, const GmrRaster* r, void* rgb,
                      void* alpha, void* ws, const Layout& L, cudaStream_t st, const LossArgs* la = nullptr,
-                     const ImageArgs* ia = nullptr) {
+                     const ImageArgs* ia = nullptr, void* status_host = nullptr, void* status_event = nullptr) {
   reset_status<<<1, 1, 0, st>>>(at<DevStatus>(ws, L.status));
   GMR_LAUNCHED();
   const uint64_t F = L.faces;
@@ -327,7 +333,7 @@ int render_forward_t(const GmrMesh* m, const GmrCamera* cams, int B, const GmrRa
       GMR_LAUNCHED();
     }
   }
-  return bin_and_blend<S>(L, ws, r, rgb, alpha, st, la, ia);
+  return bin_and_blend<S>(L, ws, r, rgb, alpha, st, la, ia, status_host, status_event);
 }
 
 template <typename S, bool kOpacity>
@@ -549,6 +555,23 @@ int gmr_render_forward(const GmrMesh* mesh, const GmrCamera* cams, int32_t B, co
   cudaStream_t st = (cudaStream_t)stream;
   if (r->dtype == GMR_F64) return render_forward_t<double>(mesh, cams, B, r, rgb, alpha, ws, L, st);
   return render_forward_t<float>(mesh, cams, B, r, rgb, alpha, ws, L, st);
+}
+
+int gmr_render_forward_ex(const GmrMesh* mesh, const GmrCamera* cams, int32_t B, const GmrRaster* r, void* rgb,
+                          void* alpha, void* ws, size_t ws_bytes, int64_t ecap, void* status_host,
+                          void* status_event, void* stream) {
+  int rc = check_mesh(mesh);
+  if (rc) return rc;
+  if ((rc = check_raster(r))) return rc;
+  if (!cams || B < 1 || B > GMR_MAX_VIEWS_PER_CALL) return fail(GMR_EINVAL, "need 1..%d cameras", GMR_MAX_VIEWS_PER_CALL);
+  if (!rgb || !alpha || !ws) return fail(GMR_EINVAL, "output or workspace pointer is null");
+  if ((uint64_t)mesh->num_faces * B >= 0xffffffffull) return fail(GMR_EINVAL, "faces*views must be < 2^32");
+  const Layout L = plan((uint64_t)mesh->num_faces, B, r->width, r->height, (uint64_t)ecap, r->dtype, true);
+  if (ws_bytes < L.total) return fail(GMR_EWORKSPACE, "workspace has %zu bytes, needs %zu", ws_bytes, L.total);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (r->dtype == GMR_F64)
+    return render_forward_t<double>(mesh, cams, B, r, rgb, alpha, ws, L, st, nullptr, nullptr, status_host, status_event);
+  return render_forward_t<float>(mesh, cams, B, r, rgb, alpha, ws, L, st, nullptr, nullptr, status_host, status_event);
 }
 
 int gmr_render_forward_loss(const GmrMesh* mesh, const GmrCamera* cams, int32_t B, const GmrRaster* r,

@@ -151,14 +151,35 @@ def render_forward(pos, col, faces, cams, width, height, background, rescale=Tru
         nb = ctypes.c_size_t()
         L.check(lib.gmr_render_workspace_size(F, B, width, height, cap, raster.dtype, ctypes.byref(nb)))
         ws = torch.empty(nb.value, dtype=torch.uint8, device=pos.device)
-        L.check(lib.gmr_render_forward(ctypes.byref(mesh), cam_arr, B, ctypes.byref(raster), _ptr(rgb),
-                                       _ptr(alpha), _ptr(ws), nb.value, cap, _stream()))
-        st, code = _status_or_raise(ws, "mesh", item_to_index)
-        if code == L.GMR_OK:
-            _capacity.note(key, cap, st.entries)
-            return rgb, alpha, ForwardState(ws, cap, raster, cam_arr, B, st.entries, st.kept)
-        cap = _capacity.grow(key, st.entries)
+        # the status arrives as soon as binning has counted the entries: the
+        # call is validated while the forward still sorts and blends, so the
+        # caller's next launches queue behind it without draining the stream
+        status = torch.empty(64, dtype=torch.uint8, pin_memory=True)
+        ev = torch.cuda.Event()
+        ev.record()   # torch creates the CUDA event lazily, on its first record
+        assert ev.cuda_event, "CUDA event not created"
+        L.check(lib.gmr_render_forward_ex(ctypes.byref(mesh), cam_arr, B, ctypes.byref(raster), _ptr(rgb),
+                                          _ptr(alpha), _ptr(ws), nb.value, cap, ctypes.c_void_p(status.data_ptr()),
+                                          ctypes.c_void_p(ev.cuda_event), _stream()))
+        ev.synchronize()
+        entries, kept, bad, overflow = _parse_status(status.numpy())
+        for field in range(6):
+            if bad[field] != 0xFFFFFFFF:
+                idx = int(bad[field]) if item_to_index is None else item_to_index(int(bad[field]))
+                raise ValueError(f"non-finite splat parameter {_FIELDS[field]!r} at splat {idx}")
+        if not overflow:
+            _capacity.note(key, cap, entries)
+            return rgb, alpha, ForwardState(ws, cap, raster, cam_arr, B, entries, kept)
+        cap = _capacity.grow(key, entries)
     raise RuntimeError("tile-entry capacity did not converge")
+
+
+def _parse_status(raw):
+    """(entries, kept, first non-finite item per field, overflow) of the
+    64-byte device status (DevStatus in csrc/gmr_common.cuh)."""
+    entries, kept = (int(x) for x in raw[:16].view(np.uint64))
+    words = raw[16:48].view(np.uint32)
+    return entries, kept, words[:6], int(words[6])
 
 
 def render_forward_loss(pos, col, faces, cams, width, height, background, target_rgb, target_mask,
@@ -245,10 +266,7 @@ def check_status(state: ForwardState, key=None):
     forward (its status copy event), not for work enqueued after it."""
     key = getattr(state, "key", key)
     state.status_event.synchronize()
-    raw = state.status_host.numpy()
-    entries, kept = (int(x) for x in raw[:16].view(np.uint64))
-    words = raw[16:48].view(np.uint32)
-    bad, overflow = words[:6], int(words[6])
+    entries, kept, bad, overflow = _parse_status(state.status_host.numpy())
     state.entries, state.kept = entries, kept
     for field in range(6):
         if bad[field] != 0xFFFFFFFF:

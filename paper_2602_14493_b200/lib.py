@@ -83,6 +83,8 @@ _SIGNATURES = {
                      + [c_i32, c_vp, c_vp, c_sz, c_vp], c_i32),
     "gmr_render_forward_loss": ([P(GmrMesh), P(GmrCamera), c_i32, P(GmrRaster), c_vp, c_vp, ctypes.c_double,
                                  ctypes.c_double, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_i64, c_vp], c_i32),
+    "gmr_render_forward_ex": ([P(GmrMesh), P(GmrCamera), c_i32, P(GmrRaster), c_vp, c_vp, c_vp, c_sz, c_i64,
+                               c_vp, c_vp, c_vp], c_i32),
     "gmr_render_images_u8": ([P(GmrMesh), P(GmrCamera), c_i32, P(GmrRaster), c_vp, c_vp, c_vp, c_sz, c_i64,
                               c_vp], c_i32),
     "gmr_topology_size": ([c_i64, c_i64, P(c_sz)], c_i32),
