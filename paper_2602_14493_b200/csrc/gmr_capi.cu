@@ -217,7 +217,7 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
     scan_reduce<<<nb, 256, 0, st>>>(order, count, items, bsum);
     GMR_LAUNCHED();
   }
-  scan_top<<<1, 256, 0, st>>>(bsum, nb, dst, (unsigned long long)L.ecap, nent);
+  scan_top<<<1, kTopThreads, 0, st>>>(bsum, nb, dst, (unsigned long long)L.ecap, nent);
   GMR_LAUNCHED();
   // the status is final here (K1's non-finite items, the entry count and the
   // capacity verdict): publish it early so the host can validate the call
@@ -234,7 +234,7 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
     const int fb = (int)((L.faces + 255) / 256);
     face_counts<<<fb, 256, 0, st>>>(count, (uint32_t)L.faces, L.views, at<uint32_t>(ws, L.offs), bsum);
     GMR_LAUNCHED();
-    scan_inplace<<<1, 256, 0, st>>>(bsum, fb);
+    scan_inplace<<<1, kTopThreads, 0, st>>>(bsum, fb);
     GMR_LAUNCHED();
     item_offsets<<<fb, 256, 0, st>>>(count, (uint32_t)L.faces, L.views, at<uint32_t>(ws, L.offs), bsum,
                                      at<uint32_t>(ws, L.entry_off));
@@ -247,7 +247,7 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
     StageScope sc(kStTileSort, st);
     ecur = radix_sort_pairs<uint32_t>(ek, ev, nent, 0, ecap, L.entry_bits, at<uint32_t>(ws, L.hist), st);
     g_launches += 3 * ((L.entry_bits + 7) / 8);
-    tile_ranges<<<grid_for((uint64_t)ecap + 1, 256), 256, 0, st>>>(ek[ecur], nent, 0, (uint32_t)L.bins,
+    tile_ranges<<<grid_for((uint64_t)ecap / 4 + 1, 256), 256, 0, st>>>(ek[ecur], nent, 0, (uint32_t)L.bins,
                                                                   at<uint32_t>(ws, L.bounds));
   }
   GMR_LAUNCHED();
@@ -730,7 +730,7 @@ int gmr_topology_build(const int32_t* faces, int64_t F, int64_t V, void* topo, s
   const int bits = std::max(1, ceil_log2((uint64_t)std::max<int64_t>(V, 1)));
   int cur = radix_sort_pairs<uint32_t>(k, v, nullptr, (uint32_t)n, (uint32_t)n, bits, hist, st);
   GMR_LAUNCHED();
-  tile_ranges<<<grid_for(n + 1, 256), 256, 0, st>>>(k[cur], nullptr, (uint32_t)n, (uint32_t)V, vstart);
+  tile_ranges<<<grid_for(n / 4 + 1, 256), 256, 0, st>>>(k[cur], nullptr, (uint32_t)n, (uint32_t)V, vstart);
   GMR_LAUNCHED();
   GMR_CUDA(cudaMemcpyAsync(slots, v[cur], n * 4, cudaMemcpyDeviceToDevice, st));
   return GMR_OK;

@@ -320,18 +320,43 @@ __global__ void __launch_bounds__(256) scan_reduce(const uint32_t* __restrict__ 
   if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
 }
 
-__global__ void __launch_bounds__(256) scan_top(uint32_t* __restrict__ bsum, int nb, DevStatus* st,
-                                               unsigned long long capacity, uint32_t* n_entries) {
-  __shared__ uint32_t sw[8];
-  unsigned long long carry = 0;
-  for (int base = 0; base < nb; base += 256) {
-    int i = base + threadIdx.x;
-    uint32_t v = i < nb ? bsum[i] : 0;
-    uint32_t tot;
-    uint32_t ex = block_exclusive_scan_256(v, sw, &tot);
-    if (i < nb) bsum[i] = (uint32_t)(carry + ex);
-    carry += tot;
+// Exclusive scan of n uint32 in place by one 1024-thread block: thread t
+// owns a contiguous run, one block scan of the run totals (64-bit carry).
+// Returns the total (thread 0 of the caller's block sees it).
+constexpr int kTopThreads = 1024;
+__device__ __forceinline__ unsigned long long scan_runs_inplace(uint32_t* __restrict__ a, int n) {
+  __shared__ unsigned long long wsum[kTopThreads / 32];
+  const int per = (n + kTopThreads - 1) / kTopThreads;
+  const int lo = min(n, (int)threadIdx.x * per), hi = min(n, lo + per);
+  unsigned long long s = 0;
+  for (int i = lo; i < hi; ++i) s += a[i];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long x = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
   }
+  if (lane == 31) wsum[warp] = x;
+  __syncthreads();
+  unsigned long long wp = 0, tot = 0;
+  for (int w = 0; w < kTopThreads / 32; ++w) {
+    const unsigned long long t = wsum[w];
+    wp += (w < warp) ? t : 0ull;
+    tot += t;
+  }
+  unsigned long long run = wp + x - s;
+  for (int i = lo; i < hi; ++i) {
+    const uint32_t v = a[i];
+    a[i] = (uint32_t)run;
+    run += v;
+  }
+  return tot;
+}
+
+__global__ void __launch_bounds__(kTopThreads) scan_top(uint32_t* __restrict__ bsum, int nb, DevStatus* st,
+                                                       unsigned long long capacity, uint32_t* n_entries) {
+  const unsigned long long carry = scan_runs_inplace(bsum, nb);
   if (threadIdx.x == 0) {
     st->entries = carry;
     const bool over = carry > capacity || carry > 0xffffffffull;
@@ -387,17 +412,8 @@ __global__ void __launch_bounds__(256) face_counts(const uint32_t* __restrict__ 
 }
 
 // single-block exclusive scan in place
-__global__ void __launch_bounds__(256) scan_inplace(uint32_t* __restrict__ a, int n) {
-  __shared__ uint32_t sw[8];
-  uint32_t carry = 0;
-  for (int base = 0; base < n; base += 256) {
-    const int i = base + threadIdx.x;
-    const uint32_t v = i < n ? a[i] : 0u;
-    uint32_t tot;
-    const uint32_t ex = block_exclusive_scan_256(v, sw, &tot);
-    if (i < n) a[i] = carry + ex;
-    carry += tot;
-  }
+__global__ void __launch_bounds__(kTopThreads) scan_inplace(uint32_t* __restrict__ a, int n) {
+  scan_runs_inplace(a, n);
 }
 
 __global__ void __launch_bounds__(256) item_offsets(const uint32_t* __restrict__ count, uint32_t F, int B,
@@ -418,19 +434,36 @@ __global__ void __launch_bounds__(256) item_offsets(const uint32_t* __restrict__
 __global__ void __launch_bounds__(256) tile_ranges(const uint32_t* __restrict__ key,
                                                   const uint32_t* n_dev, uint32_t n_host,
                                                   uint32_t num_bins, uint32_t* __restrict__ bounds) {
+  // four positions per thread (one 16-byte load; key buffers are 256-B aligned)
   const uint32_t n = n_dev ? *n_dev : n_host;
-  const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s > n) return;
-  const long long prev = s > 0 ? (long long)key[s - 1] : -1ll;
-  const long long cur = s < n ? (long long)key[s] : (long long)num_bins;
-  for (long long g = prev + 1; g <= cur && g <= (long long)num_bins; ++g) bounds[g] = s;
+  const uint32_t s0 = 4u * (blockIdx.x * blockDim.x + threadIdx.x);
+  if (s0 > n) return;
+  uint32_t k[4];
+  if (s0 + 4 <= n) {
+    const uint4 v = *reinterpret_cast<const uint4*>(key + s0);
+    k[0] = v.x; k[1] = v.y; k[2] = v.z; k[3] = v.w;
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) k[q] = (s0 + q < n) ? key[s0 + q] : num_bins;
+  }
+  // bounds[g] = first position whose key >= g: position s starts every bin in
+  // (key[s-1], key[s]] (keys past n read as num_bins)
+  uint32_t prev_plus = s0 > 0 ? key[s0 - 1] + 1u : 0u;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint32_t s = s0 + q;
+    if (s > n) break;
+    const uint32_t cur = min(k[q], num_bins);
+    for (uint32_t g = prev_plus; g <= cur; ++g) bounds[g] = s;
+    prev_plus = max(prev_plus, cur + 1u);
+  }
 }
 
 // ---------------------------------------------------------------------------
 // K3 / K4: per-tile blending over exact per-pixel coverage lists
 //
-// One CTA per (view, 16x16 tile); warp w owns tile rows 2w, 2w+1 and lane l
-// the pixel (x = l & 15, y = 2w + (l >> 4)), i.e. tile bit 32w + l.  Entries
+// One CTA per (view, 16x16 tile); warp w owns an 8x4 pixel block (tile_col /
+// tile_row below), lane l one pixel of it, i.e. coverage bit 32w + l.  Entries
 // are staged in shared memory in batches.  For each entry the loading
 // thread solves, row by row, the (padded) ellipse alpha >= 1/255 and writes a
 // 256-bit coverage mask of the tile.  A 32x32 bit transpose per warp turns
