@@ -276,6 +276,21 @@ int gmr_convert_backward(const GmrMesh* mesh, int32_t rescale, int32_t dtype,
                          const void* topology, void* scratch, size_t scratch_bytes, void* stream);
 int gmr_convert_scratch_size(int64_t num_faces, int32_t dtype, size_t* bytes);
 
+/* gmr_fit_step with every per-iteration input on the device, so that one
+ * captured CUDA graph per view replays the whole iteration: at
+ * it = *iteration (device int64), the learning rates are lr_schedule[2 it]
+ * (positions) and [2 it + 1] (colours), the losses go to history[5 it ..],
+ * the render's 64-byte status (render_status, may be null) is copied to
+ * statuses[64 it ..], and *iteration is incremented last. */
+int gmr_fit_step_scheduled(const GmrFitState* state, const GmrMeshGraph* graph, int64_t num_vertices,
+                           const float* grad_img_pos, const float* grad_img_col,
+                           const double* img_loss_sums, double inv_nc, double inv_na, double w_color,
+                           double w_silhouette, double w_edge, double w_laplacian,
+                           const double* lr_schedule, int64_t* iteration, double beta1, double beta2,
+                           double eps, int32_t optimize_colors, double* history,
+                           const void* render_status, void* statuses, void* scratch,
+                           size_t scratch_bytes, void* stream);
+
 /* ---- export and evaluation (all float64 inputs) ------- */
 
 /* export_gaussians (convert.py:497-532): per Gaussian, the 14 float32 fields

@@ -286,8 +286,12 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
     StageScope sc(kStBlendFwd, st);
     // all of the SM's unified L1/shared memory as shared memory: the
     // default carveout would cap residency below what registers allow
-    GMR_CUDA(cudaFuncSetAttribute(blend_forward<S>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                  (int)cudaSharedmemCarveoutMaxShared));
+    static bool attr_set = false;   // once per instantiation (also keeps it out of graph captures)
+    if (!attr_set) {
+      GMR_CUDA(cudaFuncSetAttribute(blend_forward<S>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                    (int)cudaSharedmemCarveoutMaxShared));
+      attr_set = true;
+    }
     blend_forward<S><<<(unsigned)L.bins, kBlendThreads, 0, st>>>(a);
     GMR_LAUNCHED();
   }
@@ -362,9 +366,13 @@ int blend_backward_launch(const Layout& L, void* ws, const GmrRaster* r, const v
   a.partial = at<S>(ws, L.partial);
   a.partial_op = kOpacity ? at<S>(ws, L.partial_op) : nullptr;
   const size_t dyn = sizeof(BwdSmem<S, kOpacity>);
-  GMR_CUDA(cudaFuncSetAttribute(blend_backward<S, kOpacity>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
-  GMR_CUDA(cudaFuncSetAttribute(blend_backward<S, kOpacity>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                (int)cudaSharedmemCarveoutMaxShared));
+  static bool attr_set = false;   // once per instantiation (also keeps it out of graph captures)
+  if (!attr_set) {
+    GMR_CUDA(cudaFuncSetAttribute(blend_backward<S, kOpacity>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+    GMR_CUDA(cudaFuncSetAttribute(blend_backward<S, kOpacity>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                  (int)cudaSharedmemCarveoutMaxShared));
+    attr_set = true;
+  }
   if (L.bins) {
     StageScope sc(kStBlendBwd, st);
     blend_backward<S, kOpacity><<<(unsigned)L.bins, kBlendThreads, dyn, st>>>(a);
@@ -616,11 +624,13 @@ int gmr_fit_scratch_size(int64_t V, int64_t E, size_t* bytes) {
   return GMR_OK;
 }
 
-int gmr_fit_step(const GmrFitState* s, const GmrMeshGraph* gr, int64_t V, const float* grad_img_pos,
-                 const float* grad_img_col, const double* img_loss_sums, double inv_nc, double inv_na,
-                 double w_color, double w_sil, double w_edge, double w_lap, double lr_pos, double lr_col,
-                 double beta1, double beta2, double eps, int32_t optimize_colors, double* history_row,
-                 void* scratch, size_t scratch_bytes, void* stream) {
+namespace {
+int fit_step_impl(const GmrFitState* s, const GmrMeshGraph* gr, int64_t V, const float* grad_img_pos,
+                  const float* grad_img_col, const double* img_loss_sums, double inv_nc, double inv_na,
+                  double w_color, double w_sil, double w_edge, double w_lap, double lr_pos, double lr_col,
+                  const double* lr_sched, int64_t* iter, double beta1, double beta2, double eps,
+                  int32_t optimize_colors, double* history_row, const void* status_src, void* statuses,
+                  void* scratch, size_t scratch_bytes, void* stream) {
   if (!s || !gr || V <= 0 || !grad_img_pos || !grad_img_col || !img_loss_sums || !history_row || !scratch)
     return fail(GMR_EINVAL, "null or empty argument");
   const int64_t E = gr->num_edges;
@@ -662,6 +672,7 @@ int gmr_fit_step(const GmrFitState* s, const GmrMeshGraph* gr, int64_t V, const 
   a.m_pos = s->m_pos; a.v_pos = s->v_pos; a.m_col = s->m_col; a.v_col = s->v_col;
   a.counts = s->step_counts; a.bad = s->flags;
   a.lr_pos = lr_pos; a.lr_col = lr_col; a.beta1 = beta1; a.beta2 = beta2; a.eps = eps;
+  a.lr_sched = lr_sched; a.iter = iter;
   a.optimize_colors = optimize_colors;
   a.reg.ve_ptr = gr->ve_ptr; a.reg.ve_slot = gr->ve_slot; a.reg.adj_ptr = gr->adj_ptr; a.reg.adj = gr->adj;
   a.reg.evec4 = evec4; a.reg.lap4 = lap4; a.reg.V = V; a.reg.w_edge = w_edge; a.reg.w_lap = w_lap;
@@ -669,9 +680,33 @@ int gmr_fit_step(const GmrFitState* s, const GmrMeshGraph* gr, int64_t V, const 
   GMR_LAUNCHED();
   fit_update<<<nbv, kTrainThreads, 0, st>>>(a, gpos, gcol);
   GMR_LAUNCHED();
-  fit_finish<<<1, 32, 0, st>>>(a, img_loss_sums, inv_nc, inv_na, w_color, w_sil, sums + 1, E, sums + 2, history_row);
+  fit_finish<<<1, 32, 0, st>>>(a, img_loss_sums, inv_nc, inv_na, w_color, w_sil, sums + 1, E, sums + 2, history_row,
+                               (const uint32_t*)status_src, (uint32_t*)statuses);
   GMR_LAUNCHED();
   return GMR_OK;
+}
+}  // namespace
+
+int gmr_fit_step(const GmrFitState* s, const GmrMeshGraph* gr, int64_t V, const float* grad_img_pos,
+                 const float* grad_img_col, const double* img_loss_sums, double inv_nc, double inv_na,
+                 double w_color, double w_sil, double w_edge, double w_lap, double lr_pos, double lr_col,
+                 double beta1, double beta2, double eps, int32_t optimize_colors, double* history_row,
+                 void* scratch, size_t scratch_bytes, void* stream) {
+  return fit_step_impl(s, gr, V, grad_img_pos, grad_img_col, img_loss_sums, inv_nc, inv_na, w_color, w_sil, w_edge,
+                       w_lap, lr_pos, lr_col, nullptr, nullptr, beta1, beta2, eps, optimize_colors, history_row,
+                       nullptr, nullptr, scratch, scratch_bytes, stream);
+}
+
+int gmr_fit_step_scheduled(const GmrFitState* s, const GmrMeshGraph* gr, int64_t V, const float* grad_img_pos,
+                           const float* grad_img_col, const double* img_loss_sums, double inv_nc, double inv_na,
+                           double w_color, double w_sil, double w_edge, double w_lap, const double* lr_schedule,
+                           int64_t* iteration, double beta1, double beta2, double eps, int32_t optimize_colors,
+                           double* history, const void* render_status, void* statuses, void* scratch,
+                           size_t scratch_bytes, void* stream) {
+  if (!lr_schedule || !iteration) return fail(GMR_EINVAL, "schedule and iteration counter are required");
+  return fit_step_impl(s, gr, V, grad_img_pos, grad_img_col, img_loss_sums, inv_nc, inv_na, w_color, w_sil, w_edge,
+                       w_lap, 0.0, 0.0, lr_schedule, iteration, beta1, beta2, eps, optimize_colors, history,
+                       render_status, statuses, scratch, scratch_bytes, stream);
 }
 
 int gmr_status(const void* ws, GmrStatus* out, void* stream) {

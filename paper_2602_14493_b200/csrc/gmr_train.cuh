@@ -148,7 +148,14 @@ struct AdamArgs {
   double lr_pos, lr_col, beta1, beta2, eps;
   int optimize_colors;
   RegArgs reg;
+  // scheduled mode (replayable): learning rates lr_sched[2 it], [2 it + 1]
+  // at it = *iter, read on the device; null = lr_pos / lr_col above
+  const double* lr_sched;
+  int64_t* iter;
 };
+
+__device__ __forceinline__ double sched_lr_pos(const AdamArgs& a) { return a.lr_sched ? a.lr_sched[2 * *a.iter] : a.lr_pos; }
+__device__ __forceinline__ double sched_lr_col(const AdamArgs& a) { return a.lr_sched ? a.lr_sched[2 * *a.iter + 1] : a.lr_col; }
 
 // pass 1: total gradients (image + regularisers) -> stash, non-finite flags
 __global__ void __launch_bounds__(kTrainThreads) fit_grads(AdamArgs a, double* __restrict__ gpos,
@@ -178,6 +185,7 @@ __global__ void __launch_bounds__(kTrainThreads) fit_update(AdamArgs a, const do
                                                            const double* __restrict__ gcol) {
   const int64_t v = (int64_t)blockIdx.x * kTrainThreads + threadIdx.x;
   if (v >= a.reg.V) return;
+  const double lr_pos = sched_lr_pos(a), lr_col = sched_lr_col(a);
   if (!a.bad[0]) {
     const double t = (double)(a.counts[0] + 1);
     const double g0 = gpos[3 * v], g1 = gpos[3 * v + 1], g2 = gpos[3 * v + 2];
@@ -191,7 +199,7 @@ __global__ void __launch_bounds__(kTrainThreads) fit_update(AdamArgs a, const do
     for (int k = 0; k < 3; ++k) {
       const double m = a.beta1 * a.m_pos[3 * v + k] + (1.0 - a.beta1) * gg[k];
       a.m_pos[3 * v + k] = m;
-      const double p = a.pos[3 * v + k] + (-a.lr_pos * (m / c1) / den);
+      const double p = a.pos[3 * v + k] + (-lr_pos * (m / c1) / den);
       a.pos[3 * v + k] = p;
       if (a.pos_f) a.pos_f[3 * v + k] = (float)p;
     }
@@ -206,7 +214,7 @@ __global__ void __launch_bounds__(kTrainThreads) fit_update(AdamArgs a, const do
       const double vv = a.beta2 * a.v_col[3 * v + k] + (1.0 - a.beta2) * g * g;
       a.m_col[3 * v + k] = m;
       a.v_col[3 * v + k] = vv;
-      const double c = fmin(fmax(a.col[3 * v + k] - a.lr_col * (m / c1) / (sqrt(vv / c2) + a.eps), 0.0), 1.0);
+      const double c = fmin(fmax(a.col[3 * v + k] - lr_col * (m / c1) / (sqrt(vv / c2) + a.eps), 0.0), 1.0);
       a.col[3 * v + k] = c;
       if (a.col_f) a.col_f[3 * v + k] = (float)c;
     }
@@ -214,10 +222,16 @@ __global__ void __launch_bounds__(kTrainThreads) fit_update(AdamArgs a, const do
 }
 
 // pass 3: step counters, flags reset, the iteration's loss report
-// history[it] = (total, color, silhouette, edge, laplacian)
+// history[it] = (total, color, silhouette, edge, laplacian); in scheduled
+// mode `history` is the [iterations][5] base, row it = *iter, the render's
+// 64-byte status is kept in statuses[it] and the counter advances last.
 __global__ void fit_finish(AdamArgs a, const double* __restrict__ img_sums, double inv_nc, double inv_na,
                            double w_color, double w_sil, const double* __restrict__ edge_sum, int64_t E,
-                           const double* __restrict__ lap_sum, double* __restrict__ history) {
+                           const double* __restrict__ lap_sum, double* __restrict__ history,
+                           const uint32_t* __restrict__ status_src, uint32_t* __restrict__ statuses) {
+  const int64_t it = a.iter ? *a.iter : 0;
+  if (status_src && statuses && threadIdx.x < 16) statuses[16 * it + threadIdx.x] = status_src[threadIdx.x];
+  __syncthreads();
   if (threadIdx.x != 0) return;
   if (!a.bad[0]) a.counts[0] += 1;
   if (a.optimize_colors && !a.bad[1]) a.counts[1] += 1;
@@ -225,11 +239,13 @@ __global__ void fit_finish(AdamArgs a, const double* __restrict__ img_sums, doub
   const double color = img_sums[0] * inv_nc, sil = img_sums[1] * inv_na;
   const double edge = E ? *edge_sum / (double)E : 0.0;
   const double lap = *lap_sum / (double)a.reg.V;
-  history[0] = w_color * color + w_sil * sil + a.reg.w_edge * edge + a.reg.w_lap * lap;
-  history[1] = color;
-  history[2] = sil;
-  history[3] = edge;
-  history[4] = lap;
+  double* h = history + 5 * it;
+  h[0] = w_color * color + w_sil * sil + a.reg.w_edge * edge + a.reg.w_lap * lap;
+  h[1] = color;
+  h[2] = sil;
+  h[3] = edge;
+  h[4] = lap;
+  if (a.iter) *a.iter = it + 1;
 }
 
 }  // namespace gmr

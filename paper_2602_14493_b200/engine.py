@@ -187,7 +187,9 @@ def render_forward_loss(pos, col, faces, cams, width, height, background, target
     """B-view forward with the colour/silhouette losses fused into the blend
     epilogue.  target_rgb [B,H,W,3] / target_mask [B,H,W] on the device in the
     render dtype.  Returns (rgb, alpha, g_rgb, g_alpha, loss_sums [2] f64 on
-    the device: sum of squared colour errors, sum of BCE terms), state)."""
+    the device: sum of squared colour errors, sum of BCE terms), state).
+    check: True = validate now (host sync), False = copy the status behind the
+    call (`check_status` later), None = leave it in the workspace."""
     lib = L.load()
     dtype = pos.dtype
     B, F = len(cams), int(faces.shape[0])
@@ -212,6 +214,11 @@ def render_forward_loss(pos, col, faces, cams, width, height, background, target
                                             _ptr(t_m), float(scale_rgb), float(scale_alpha), _ptr(rgb), _ptr(alpha),
                                             _ptr(g_rgb), _ptr(g_a), _ptr(sums), _ptr(ws), nb.value, cap, _stream()))
         st = ForwardState(ws, cap, raster, cam_arr, B, -1, -1)
+        if check is None:
+            # status stays on the device (ws[:64]); the caller validates it
+            # (graph-captured loops copy it with gmr_fit_step_scheduled)
+            st.key = key
+            return rgb, alpha, g_rgb, g_a, sums, st
         if not check:
             st.status_host = torch.empty(64, dtype=torch.uint8, pin_memory=True)
             st.status_host.copy_(ws[:64], non_blocking=True)
