@@ -91,7 +91,7 @@ inline unsigned grid_for(uint64_t n, unsigned block) { return (unsigned)std::max
 // Workspace layout (byte offsets).
 struct Layout {
   size_t status, splat, col4, rect, count, dkey[2], ditem[2], offs, entry_off, bsum, nent;
-  size_t ekey[2], eval[2], bounds, t_final, hist, partial, partial_op, face_acc, corner, aux, loss_tile;
+  size_t ekey[2], eval[2], bounds, sched, t_final, hist, partial, partial_op, face_acc, corner, aux, loss_tile;
   size_t total;
   uint64_t items, faces, bins, pixels, ecap;
   int views, tiles_x, tiles_y, tiles;
@@ -133,6 +133,7 @@ Layout plan(uint64_t faces, int views, int W, int H, uint64_t ecap, int dtype, b
   L.eval[0] = take(ecap * 4);
   L.eval[1] = take(ecap * 4);
   L.bounds = take((L.bins + 1) * 4);
+  L.sched = take(L.bins * 4);
   L.t_final = take(L.pixels * s);
   L.hist = take(std::max(radix_hist_words((uint32_t)std::min<uint64_t>(L.items, 0xffffffffu)),
                          radix_hist_words((uint32_t)std::min<uint64_t>(ecap, 0xffffffffu))) * 4);
@@ -249,10 +250,16 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
     g_launches += 3 * ((L.entry_bits + 7) / 8);
     tile_ranges<<<grid_for((uint64_t)ecap / 4 + 1, 256), 256, 0, st>>>(ek[ecur], nent, 0, (uint32_t)L.bins,
                                                                   at<uint32_t>(ws, L.bounds));
+    GMR_LAUNCHED();
+    if (L.bins) {
+      tile_schedule<<<1, kSchedThreads, 0, st>>>(at<uint32_t>(ws, L.bounds), (uint32_t)L.bins,
+                                                 at<uint32_t>(ws, L.sched));
+    }
   }
   GMR_LAUNCHED();
   BlendArgs<S> a{};
   a.bounds = at<uint32_t>(ws, L.bounds);
+  a.sched = at<uint32_t>(ws, L.sched);
   a.entry_item = ev[ecur];
   a.splat = at<Splat<S>>(ws, L.splat);
   a.col4 = at<V4<S>>(ws, L.col4);
@@ -346,6 +353,7 @@ int blend_backward_launch(const Layout& L, void* ws, const GmrRaster* r, const v
   const uint32_t ecur = (uint32_t)(((L.entry_bits + 7) / 8) & 1);
   BlendArgs<S> a{};
   a.bounds = at<uint32_t>(ws, L.bounds);
+  a.sched = at<uint32_t>(ws, L.sched);
   a.entry_item = at<uint32_t>(ws, L.eval[ecur]);
   a.splat = at<Splat<S>>(ws, L.splat);
   a.col4 = at<V4<S>>(ws, L.col4);

@@ -459,6 +459,40 @@ __global__ void __launch_bounds__(256) tile_ranges(const uint32_t* __restrict__ 
   }
 }
 
+// Blend schedule: bins ordered by decreasing entry count (bucketed), so the
+// heaviest tiles start first and the last wave holds the lightest ones.
+// The order within a bucket is arbitrary (atomics); every tile's result is
+// independent of when it runs.
+constexpr int kSchedThreads = 1024;
+__device__ __forceinline__ uint32_t sched_bucket(uint32_t cnt) { return 255u - min(cnt >> 3, 255u); }
+
+__global__ void __launch_bounds__(kSchedThreads) tile_schedule(const uint32_t* __restrict__ bounds, uint32_t bins,
+                                                               uint32_t* __restrict__ order) {
+  __shared__ uint32_t hist[256];
+  for (int i = threadIdx.x; i < 256; i += kSchedThreads) hist[i] = 0;
+  __syncthreads();
+  for (uint32_t g = threadIdx.x; g < bins; g += kSchedThreads)
+    atomicAdd(&hist[sched_bucket(bounds[g + 1] - bounds[g])], 1u);
+  __syncthreads();
+  if (threadIdx.x < 32) {   // exclusive scan of the 256 buckets by one warp
+    uint32_t v[8], s = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) { v[k] = hist[threadIdx.x * 8 + k]; s += v[k]; }
+    uint32_t x = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if ((int)threadIdx.x >= o) x += y;
+    }
+    uint32_t run = x - s;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) { hist[threadIdx.x * 8 + k] = run; run += v[k]; }
+  }
+  __syncthreads();
+  for (uint32_t g = threadIdx.x; g < bins; g += kSchedThreads)
+    order[atomicAdd(&hist[sched_bucket(bounds[g + 1] - bounds[g])], 1u)] = g;
+}
+
 // ---------------------------------------------------------------------------
 // K3 / K4: per-tile blending over exact per-pixel coverage lists
 //
@@ -503,6 +537,7 @@ template <typename S> struct BlendArgs {
   // optional 8-bit images (dataset.py:59-61 `_save_png`); rgb/alpha may then be null
   uint8_t* rgb8;           // [B,H,W,3]
   uint8_t* alpha8;         // [B,H,W]
+  const uint32_t* sched;   // launch order of the bins (tile_schedule) or null
 };
 
 // np.round(np.clip(float64(x), 0, 1) * 255).astype(uint8) (dataset.py:60-61):
@@ -751,7 +786,7 @@ struct BitWalk {
 template <typename S>
 __global__ void __launch_bounds__(kBlendThreads, 6) blend_forward(BlendArgs<S> p) {
   __shared__ StageSmem<S, kFwdBatch> sm;
-  const uint32_t g = blockIdx.x;
+  const uint32_t g = p.sched ? p.sched[blockIdx.x] : blockIdx.x;
   const uint32_t view = g / p.tiles_per_view, t = g % p.tiles_per_view;
   const int tx = (int)(t % (uint32_t)p.tiles_x), ty = (int)(t / (uint32_t)p.tiles_x);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -879,7 +914,7 @@ __global__ void __launch_bounds__(kBlendThreads, 5) blend_backward(BlendArgs<S> 
   typedef BwdSmem<S, kOpacity> Sm;
   typedef typename Sm::Rec Rec;
   Sm& sm = *reinterpret_cast<Sm*>(dyn);
-  const uint32_t g = blockIdx.x;
+  const uint32_t g = p.sched ? p.sched[blockIdx.x] : blockIdx.x;
   const uint32_t view = g / p.tiles_per_view, t = g % p.tiles_per_view;
   const int tx = (int)(t % (uint32_t)p.tiles_x), ty = (int)(t / (uint32_t)p.tiles_x);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
