@@ -1197,10 +1197,18 @@ __global__ void __launch_bounds__(128) face_views_backward(FaceBwdArgs<S> p, con
   // counts of a group of 8 views are loaded together, ahead of their use
   uint32_t off = p.entry_off[(int64_t)p.view0 * p.F + f];
   for (int v8 = 0; v8 < p.nviews; v8 += 8) {
-   uint32_t cn[8];
+   uint32_t cn[8], run = 0;
 #pragma unroll
-   for (int k = 0; k < 8; ++k)
+   for (int k = 0; k < 8; ++k) {
      cn[k] = (v8 + k < p.nviews) ? p.count[(int64_t)(p.view0 + v8 + k) * p.F + f] : 0u;
+     run += cn[k];
+   }
+   // the group's partials are one contiguous run: start pulling it into L2
+   {
+     const char* b0 = reinterpret_cast<const char*>(p.partial + (size_t)off * 8);
+     const char* b1 = reinterpret_cast<const char*>(p.partial + (size_t)(off + run) * 8);
+     for (const char* q = b0; q < b1; q += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
+   }
 #pragma unroll
    for (int k = 0; k < 8; ++k) {
     const int vv = v8 + k;
