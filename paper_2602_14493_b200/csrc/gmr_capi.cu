@@ -552,6 +552,9 @@ const char* gmr_version(void) { return "gmr-b200 0.1 (sm_100a)"; }
 int gmr_render_workspace_size(int64_t F, int32_t B, int32_t W, int32_t H, int64_t ecap, int32_t dtype,
                               size_t* bytes) {
   if (!bytes || F < 0 || B < 1 || W < 1 || H < 1 || ecap < 0) return fail(GMR_EINVAL, "bad workspace sizes");
+  if (ecap > 0xffffffffll)
+    return fail(GMR_EINVAL, "%lld tile entries: a call is limited to 2^32 - 1 (render fewer views per call)",
+                (long long)ecap);
   if ((uint64_t)F * B >= 0xffffffffull) return fail(GMR_EINVAL, "faces*views must be < 2^32");
   if (dtype != GMR_F32 && dtype != GMR_F64) return fail(GMR_EINVAL, "bad dtype");
   *bytes = plan((uint64_t)F, B, W, H, (uint64_t)ecap, dtype, true).total;
@@ -800,6 +803,8 @@ int gmr_render_backward(const GmrMesh* mesh, const GmrCamera* cams, int32_t B, c
 
 int gmr_raster_workspace_size(int64_t K, int32_t W, int32_t H, int64_t ecap, int32_t dtype, size_t* bytes) {
   if (!bytes || K < 0 || W < 1 || H < 1 || ecap < 0) return fail(GMR_EINVAL, "bad workspace sizes");
+  if (ecap > 0xffffffffll) return fail(GMR_EINVAL, "%lld tile entries: a call is limited to 2^32 - 1", (long long)ecap);
+  if (K >= 0xffffffffll) return fail(GMR_EINVAL, "splats must be < 2^32");
   if (dtype != GMR_F32 && dtype != GMR_F64) return fail(GMR_EINVAL, "bad dtype");
   *bytes = plan((uint64_t)K, 1, W, H, (uint64_t)ecap, dtype, false).total;
   return GMR_OK;

@@ -50,6 +50,9 @@ def test_argument_errors_without_gpu():
     small = nb.value
     assert cdll.gmr_render_workspace_size(100, 2, 32, 32, 100000, 0, ctypes.byref(nb)) == lib.GMR_OK
     assert nb.value > small
+    assert cdll.gmr_render_workspace_size(100, 2, 32, 32, 1 << 32, 0, ctypes.byref(nb)) == lib.GMR_EINVAL
+    assert b"2^32" in cdll.gmr_last_error()
+    assert cdll.gmr_raster_workspace_size(10, 32, 32, 1 << 33, 0, ctypes.byref(nb)) == lib.GMR_EINVAL
     r = lib.GmrRaster()
     r.width, r.height, r.dtype = 0, 8, 0
     m = lib.GmrMesh()
