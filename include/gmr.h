@@ -83,6 +83,13 @@ typedef struct {
 
 /* GmrRaster.flags: keep each item's (radius, depth) for gmr_copy_splats. */
 #define GMR_FLAG_DEBUG_AUX 1
+/* GmrRaster.flags: emit every tile of each splat's rectangle, exactly the
+ * reference's _RasterPlan lists (render.py:214-226).  By default a splat of
+ * at most 32 tiles skips the tiles its padded alpha >= 1/255 ellipse cannot
+ * reach (entries whose blend coverage would be empty): images and gradients
+ * are bit-identical either way, the tile lists are then a subsequence of the
+ * reference's. */
+#define GMR_FLAG_FULL_TILE_LISTS 2
 
 /* Result of a forward pass, read back by gmr_status (synchronises). */
 typedef struct {

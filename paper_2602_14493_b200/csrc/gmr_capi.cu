@@ -90,7 +90,7 @@ inline unsigned grid_for(uint64_t n, unsigned block) { return (unsigned)std::max
 
 // Workspace layout (byte offsets).
 struct Layout {
-  size_t status, splat, col4, rect, count, dkey[2], ditem[2], offs, entry_off, bsum, nent;
+  size_t status, splat, col4, rect, count, emask, dkey[2], ditem[2], offs, entry_off, bsum, nent;
   size_t ekey[2], eval[2], bounds, sched, t_final, hist, partial, partial_op, face_acc, corner, aux, loss_tile;
   size_t total;
   uint64_t items, faces, bins, pixels, ecap;
@@ -120,6 +120,7 @@ Layout plan(uint64_t faces, int views, int W, int H, uint64_t ecap, int dtype, b
   L.col4 = take(faces * 4 * s);
   L.rect = take(L.items * 8);
   L.count = take(L.items * 4);
+  L.emask = take(L.items * 4);
   L.dkey[0] = take(L.items * ks);
   L.dkey[1] = take(L.items * ks);
   L.ditem[0] = take(L.items * 4);
@@ -228,7 +229,8 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
   uint32_t* ek[2] = {at<uint32_t>(ws, L.ekey[0]), at<uint32_t>(ws, L.ekey[1])};
   uint32_t* ev[2] = {at<uint32_t>(ws, L.eval[0]), at<uint32_t>(ws, L.eval[1])};
   if (items) {
-    scan_emit<<<nb, 256, 0, st>>>(order, count, at<uint2>(ws, L.rect), items, bsum, (uint32_t)L.faces,
+    scan_emit<<<nb, 256, 0, st>>>(order, count, at<uint2>(ws, L.rect), at<uint32_t>(ws, L.emask), items, bsum,
+                                  (uint32_t)L.faces,
                                   L.tiles_x, (uint32_t)L.tiles, nent, ek[0], ev[0]);
     GMR_LAUNCHED();
     // face-major partial offsets (bsum and offs are free again here)
@@ -264,6 +266,7 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
   a.splat = at<Splat<S>>(ws, L.splat);
   a.col4 = at<V4<S>>(ws, L.col4);
   a.rect = at<uint2>(ws, L.rect);
+  a.emask = at<uint32_t>(ws, L.emask);
   a.entry_off = at<uint32_t>(ws, L.entry_off);
   a.items_per_view = (uint32_t)L.faces;
   a.tiles_x = L.tiles_x;
@@ -336,6 +339,8 @@ int render_forward_t(const GmrMesh* m, const GmrCamera* cams, int B, const GmrRa
     a.count = at<uint32_t>(ws, L.count);
     a.dkey = at<typename KeyOf<S>::type>(ws, L.dkey[0]);
     a.ditem = at<uint32_t>(ws, L.ditem[0]);
+    a.emask = at<uint32_t>(ws, L.emask);
+    a.cull = (r->flags & GMR_FLAG_FULL_TILE_LISTS) ? 0 : 1;
     a.aux = (r->flags & GMR_FLAG_DEBUG_AUX) ? at<S>(ws, L.aux) : nullptr;
     a.st = at<DevStatus>(ws, L.status);
     if (F) {
@@ -358,6 +363,7 @@ int blend_backward_launch(const Layout& L, void* ws, const GmrRaster* r, const v
   a.splat = at<Splat<S>>(ws, L.splat);
   a.col4 = at<V4<S>>(ws, L.col4);
   a.rect = at<uint2>(ws, L.rect);
+  a.emask = at<uint32_t>(ws, L.emask);
   a.entry_off = at<uint32_t>(ws, L.entry_off);
   a.items_per_view = (uint32_t)L.faces;
   a.tiles_x = L.tiles_x;
@@ -464,6 +470,8 @@ int rasterize_forward_t(const GmrSplats* sp, const GmrRaster* r, void* rgb, void
   a.count = at<uint32_t>(ws, L.count);
   a.dkey = at<typename KeyOf<S>::type>(ws, L.dkey[0]);
   a.ditem = at<uint32_t>(ws, L.ditem[0]);
+  a.emask = at<uint32_t>(ws, L.emask);
+  a.cull = (r->flags & GMR_FLAG_FULL_TILE_LISTS) ? 0 : 1;
   a.st = at<DevStatus>(ws, L.status);
   if (sp->count) {
     pack_splats<S><<<grid_for(sp->count, 256), 256, 0, st>>>(a);

@@ -145,6 +145,63 @@ __device__ __forceinline__ void cam_m2(const Cam<S>& cam, const S t[3], S m2[2][
   }
 }
 
+// Tiles of a splat's rectangle that its padded ellipse can reach (bit
+// (ty - ty0) * w + (tx - tx0)), for rectangles of at most 32 tiles.  Rows
+// and half-widths are solved exactly as tile_coverage does (global pixel
+// coordinates here), with 0.01 px more padding, so every tile whose blend
+// coverage mask could be non-empty is kept: dropping the others changes no
+// pixel and no gradient.  Entries of dropped tiles would be empty in both
+// blend kernels anyway (the reference's _RasterPlan lists them,
+// render.py:214-226; GMR_FLAG_FULL_TILE_LISTS keeps them).
+constexpr int kMaskTiles = 32;
+template <typename S>
+__device__ __forceinline__ uint32_t rect_tile_mask(const Splat<S>& sp, int tx0, int ty0, int tx1, int ty1) {
+  const S mx = sp.a.x, my = sp.a.y, ca = sp.a.z, cb = sp.a.w, cc = sp.b.x, ey = sp.b.z, tau = sp.b.w;
+  if (!(sp.b.y >= S(0)) || !(ca > S(0))) return 0u;
+  const int w = tx1 - tx0 + 1;
+  const S y_lo = fmax(ceil(my - ey), S(ty0 * kTile)), y_hi = fmin(floor(my + ey), S(ty1 * kTile + kTile - 1));
+  if (!(y_lo <= y_hi)) return 0u;
+  const S neg_det = cb * cb - ca * cc;
+  const S inv_a = S(1) / ca;
+  const S x_min = S(tx0 * kTile), x_max = S(tx1 * kTile + kTile - 1);
+  uint32_t m = 0;
+  for (int y = (int)y_lo; y <= (int)y_hi; ++y) {
+    const S dy = S(y) - my;
+    const S disc = dy * dy * neg_det + ca * tau;
+    if (!(disc >= S(0))) continue;
+    const S hw = sqrt_s(disc) * inv_a * S(1.0005) + S(0.02);
+    const S xc = mx - cb * dy * inv_a;
+    const S lo = fmax(ceil(xc - hw), x_min), hi = fmin(floor(xc + hw), x_max);
+    if (!(lo <= hi)) continue;
+    const int ta = ((int)lo >> 4) - tx0, tb = ((int)hi >> 4) - tx0;
+    m |= ((0xffffffffu >> (31 - (tb - ta))) << ta) << (((y >> 4) - ty0) * w);
+  }
+  return m;
+}
+
+// per-item entry count + mask: culled (mask over <= 32 tiles) or the full rect
+template <typename S>
+__device__ __forceinline__ uint32_t item_tiles(const Splat<S>& sp, int tx0, int ty0, int tx1, int ty1, bool cull,
+                                               uint32_t& mask) {
+  const uint32_t area = (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
+  if (area > (uint32_t)kMaskTiles) {
+    mask = 0xffffffffu;
+    return area;
+  }
+  mask = cull ? rect_tile_mask(sp, tx0, ty0, tx1, ty1) : (0xffffffffu >> (32 - area));
+  return (uint32_t)__popc(mask);
+}
+
+// partial slot of an entry of `item` in tile (tx, ty): its rank among the
+// item's emitted tiles (row-major over the rectangle)
+__device__ __forceinline__ uint32_t entry_rank(uint2 rc, uint32_t mask, int tx, int ty) {
+  const int tx0 = rc.x & 0xffff, ty0 = rc.x >> 16, tx1 = rc.y & 0xffff, ty1 = rc.y >> 16;
+  const int w = tx1 - tx0 + 1;
+  const uint32_t ri = (uint32_t)((ty - ty0) * w + (tx - tx0));
+  if ((uint32_t)(w * (ty1 - ty0 + 1)) > (uint32_t)kMaskTiles) return ri;
+  return (uint32_t)__popc(mask & ((1u << ri) - 1u));
+}
+
 template <typename S> struct MeshFwdArgs {
   const S* pos;
   const S* col;
@@ -159,6 +216,8 @@ template <typename S> struct MeshFwdArgs {
   uint32_t* count;
   typename KeyOf<S>::type* dkey;
   uint32_t* ditem;
+  uint32_t* emask;   // [items]: emitted tiles of the rectangle (item_tiles)
+  int cull;          // drop tiles the splat cannot reach (not GMR_FLAG_FULL_TILE_LISTS)
   S* aux;   // optional [items][2] = (radius, depth)
   DevStatus* st;
 };
@@ -194,7 +253,7 @@ __global__ void __launch_bounds__(256) mesh_to_splats(MeshFwdArgs<S> p, const __
       S t[3];
       cam_point(cam, mean, t);
       Splat<S> rec;
-      uint32_t cnt = 0;
+      uint32_t cnt = 0, emask = 0;
       uint2 rc = make_uint2(0, 0);
       typename KeyOf<S>::type key = ~(typename KeyOf<S>::type)0;
       if (t[2] > cam.near_plane && t[2] < cam.far_plane) {
@@ -219,7 +278,7 @@ __global__ void __launch_bounds__(256) mesh_to_splats(MeshFwdArgs<S> p, const __
         if (on) {
           int tx0, ty0, tx1, ty1;
           tile_rect(mx, my, r, p.tiles_x, p.tiles_y, tx0, ty0, tx1, ty1);
-          cnt = (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
+          cnt = item_tiles(rec, tx0, ty0, tx1, ty1, p.cull != 0, emask);
           rc = make_uint2((uint32_t)tx0 | ((uint32_t)ty0 << 16), (uint32_t)tx1 | ((uint32_t)ty1 << 16));
           key = order_key(t[2]);
           ++kept;
@@ -240,6 +299,7 @@ __global__ void __launch_bounds__(256) mesh_to_splats(MeshFwdArgs<S> p, const __
       p.splat[item] = rec;
       p.rect[item] = rc;
       p.count[item] = cnt;
+      p.emask[item] = emask;
       p.dkey[item] = key;
       p.ditem[item] = (uint32_t)item;
     }
@@ -266,6 +326,8 @@ template <typename S> struct PackArgs {
   uint32_t* count;
   typename KeyOf<S>::type* dkey;
   uint32_t* ditem;
+  uint32_t* emask;
+  int cull;
   DevStatus* st;
 };
 
@@ -293,14 +355,17 @@ __global__ void __launch_bounds__(256) pack_splats(PackArgs<S> p) {
   int tx0 = 0, ty0 = 0, tx1 = -1, ty1 = -1;
   if (finite_s(mx) && finite_s(my) && finite_s(r))
     tile_rect(mx, my, r, p.tiles_x, p.tiles_y, tx0, ty0, tx1, ty1);
-  const uint32_t cnt = (tx1 >= tx0 && ty1 >= ty0) ? (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1)) : 0u;
+  const bool has_rect = tx1 >= tx0 && ty1 >= ty0;
+  uint32_t emask = 0;
+  const uint32_t cnt = has_rect ? item_tiles(rec, tx0, ty0, tx1, ty1, p.cull != 0, emask) : 0u;
   p.splat[i] = rec;
   p.col4[i] = col;
   p.rect[i] = make_uint2((uint32_t)tx0 | ((uint32_t)ty0 << 16), (uint32_t)max(tx1, 0) | ((uint32_t)max(ty1, 0) << 16));
   p.count[i] = cnt;
+  p.emask[i] = emask;
   p.dkey[i] = order_key(d);
   p.ditem[i] = item;
-  if (cnt) atomicAdd(&p.st->kept, 1ull);
+  if (has_rect) atomicAdd(&p.st->kept, 1ull);
 }
 
 // ---------------------------------------------------------------------------
@@ -371,7 +436,8 @@ __global__ void __launch_bounds__(kTopThreads) scan_top(uint32_t* __restrict__ b
 // Skipped when the entries overflow.
 __global__ void __launch_bounds__(256) scan_emit(const uint32_t* __restrict__ order,
                                                 const uint32_t* __restrict__ count,
-                                                const uint2* __restrict__ rect, uint32_t n,
+                                                const uint2* __restrict__ rect,
+                                                const uint32_t* __restrict__ emask, uint32_t n,
                                                 const uint32_t* __restrict__ bsum,
                                                 uint32_t items_per_view, int tiles_x,
                                                 uint32_t tiles_per_view,
@@ -384,13 +450,26 @@ __global__ void __launch_bounds__(256) scan_emit(const uint32_t* __restrict__ or
   const uint32_t run = bsum[blockIdx.x] + block_exclusive_scan_256(c, sw, nullptr);
   if (i >= n || !c || *n_entries == 0) return;
   const uint2 rc = rect[item];
-  const int tx0 = rc.x & 0xffff, ty0 = rc.x >> 16, tx1 = rc.y & 0xffff;
+  const int tx0 = rc.x & 0xffff, ty0 = rc.x >> 16, tx1 = rc.y & 0xffff, ty1 = rc.y >> 16;
+  const int w = tx1 - tx0 + 1;
   const uint32_t vbase = (item / items_per_view) * tiles_per_view;
-  int tx = tx0, ty = ty0;
-  for (uint32_t e = 0; e < c; ++e) {
-    key[run + e] = vbase + (uint32_t)(ty * tiles_x + tx);
-    val[run + e] = item;
-    if (++tx > tx1) { tx = tx0; ++ty; }
+  if ((uint32_t)(w * (ty1 - ty0 + 1)) > (uint32_t)kMaskTiles) {
+    int tx = tx0, ty = ty0;
+    for (uint32_t e = 0; e < c; ++e) {
+      key[run + e] = vbase + (uint32_t)(ty * tiles_x + tx);
+      val[run + e] = item;
+      if (++tx > tx1) { tx = tx0; ++ty; }
+    }
+  } else {
+    // the rectangle's kept tiles, row-major (entry_rank order)
+    uint32_t m = emask[item], e = 0;
+    while (m) {
+      const int ri = __ffs(m) - 1;
+      m &= m - 1;
+      key[run + e] = vbase + (uint32_t)((ty0 + ri / w) * tiles_x + tx0 + ri % w);
+      val[run + e] = item;
+      ++e;
+    }
   }
 }
 
@@ -512,6 +591,7 @@ template <typename S> struct BlendArgs {
   const Splat<S>* splat;
   const V4<S>* col4;
   const uint2* rect;
+  const uint32_t* emask;     // emitted tiles per item (item_tiles)
   const uint32_t* entry_off;
   uint32_t items_per_view;   // F (mesh) or K (splats)
   int tiles_x;
@@ -1095,9 +1175,7 @@ __global__ void __launch_bounds__(kBlendThreads, 5) blend_backward(BlendArgs<S> 
     if (kOpacity) aop += __shfl_xor_sync(0xffffffffu, aop, 1);
     if (half == 0 && je < n) {
       const uint32_t item_j = p.entry_item[base + je];
-      const uint2 rc = p.rect[item_j];
-      const int tx0 = rc.x & 0xffff, ty0 = rc.x >> 16, tx1 = rc.y & 0xffff;
-      const uint32_t slot = p.entry_off[item_j] + (uint32_t)((ty - ty0) * (tx1 - tx0 + 1) + (tx - tx0));
+      const uint32_t slot = p.entry_off[item_j] + entry_rank(p.rect[item_j], p.emask[item_j], tx, ty);
       V4<S>* dst = reinterpret_cast<V4<S>*>(p.partial + (size_t)slot * 8);
       V4<S> lo, hi;
       lo.x = acc[0]; lo.y = acc[1]; lo.z = acc[2]; lo.w = acc[3];
@@ -1112,9 +1190,7 @@ __global__ void __launch_bounds__(kBlendThreads, 5) blend_backward(BlendArgs<S> 
   // which must hold zeros (every slot is written exactly once)
   for (uint32_t e = base + threadIdx.x; e < end; e += kBlendThreads) {
     const uint32_t item = p.entry_item[e];
-    const uint2 rc = p.rect[item];
-    const int tx0 = rc.x & 0xffff, ty0 = rc.x >> 16, tx1 = rc.y & 0xffff;
-    const uint32_t slot = p.entry_off[item] + (uint32_t)((ty - ty0) * (tx1 - tx0 + 1) + (tx - tx0));
+    const uint32_t slot = p.entry_off[item] + entry_rank(p.rect[item], p.emask[item], tx, ty);
     V4<S>* dst = reinterpret_cast<V4<S>*>(p.partial + (size_t)slot * 8);
     V4<S> z;
     z.x = z.y = z.z = z.w = S(0);

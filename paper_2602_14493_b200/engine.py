@@ -28,6 +28,12 @@ def _stream():
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
+# Extra GmrRaster flags for every call of this process.  Set to
+# L.FLAG_FULL_TILE_LISTS to get the reference's exact _RasterPlan tile lists
+# (by default splats drop the tiles they cannot reach; outputs are identical).
+DEFAULT_FLAGS = 0
+
+
 def raster_struct(width, height, background, dtype, rescale=True, flags=0) -> L.GmrRaster:
     r = L.GmrRaster()
     r.width, r.height = int(width), int(height)
@@ -35,7 +41,7 @@ def raster_struct(width, height, background, dtype, rescale=True, flags=0) -> L.
     r.background[:] = [float(x) for x in bg]
     r.dtype = _DT[dtype]
     r.rescale = 1 if rescale else 0
-    r.flags = int(flags)
+    r.flags = int(flags) | DEFAULT_FLAGS
     return r
 
 

@@ -80,11 +80,15 @@ def test_capacity_overflow_recovers(gmr):
     pos, col, faces = gmr.api._device_mesh(mesh, np.float64)
     cam = case["camera"]
     key = (len(mesh.facets), 1, 128, 128, pos.dtype)
-    ref, _, st0 = engine.render_forward(pos, col, faces, [cam], 128, 128, case["background"])
-    engine._capacity._cap[key] = 17   # far too small
-    rgb, _, st = engine.render_forward(pos, col, faces, [cam], 128, 128, case["background"])
-    assert st.entries == st0.entries == 5997 and st.capacity >= st.entries
-    assert np.array_equal(rgb.cpu().numpy(), ref.cpu().numpy())
+    from paper_2602_14493_b200 import lib
+    for flags, expect in ((lib.FLAG_FULL_TILE_LISTS, 5997), (0, None)):
+        ref, _, st0 = engine.render_forward(pos, col, faces, [cam], 128, 128, case["background"], flags=flags)
+        engine._capacity._cap[key] = 17   # far too small
+        rgb, _, st = engine.render_forward(pos, col, faces, [cam], 128, 128, case["background"], flags=flags)
+        # the reference's E (5,997 at config 1); fewer without unreachable tiles
+        assert st.entries == st0.entries == (expect or st0.entries) and st.capacity >= st.entries
+        assert expect or st.entries < 5997
+        assert np.array_equal(rgb.cpu().numpy(), ref.cpu().numpy())
 
 
 def test_nan_vertex_is_depth_culled_like_reference(gmr):

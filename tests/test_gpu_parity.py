@@ -51,10 +51,21 @@ def test_render_f64_matches_reference(gmr, name, maker):
     assert rel(gv, g["f64_grad_v"]) <= 1e-8
     assert rel(gcol, g["f64_grad_c"]) <= 1e-8
     # tile lists: bit-exact (face ids in (tile, depth, source) order + bounds)
-    from paper_2602_14493_b200 import engine
-    items, bounds = engine.copy_entries(ctx.state, len(mesh.facets), True)
+    # with the reference's full _RasterPlan lists
+    from paper_2602_14493_b200 import engine, lib
+    old = engine.DEFAULT_FLAGS
+    engine.DEFAULT_FLAGS = lib.FLAG_FULL_TILE_LISTS
+    try:
+        out_full, ctx_full = gmr.render_mesh(mesh, case["camera"], background=case["background"],
+                                             dtype=np.float64, return_ctx=True)
+        items, bounds = engine.copy_entries(ctx_full.state, len(mesh.facets), True)
+    finally:
+        engine.DEFAULT_FLAGS = old
     np.testing.assert_array_equal(items.cpu().numpy(), g["f64_entry_source"])
     np.testing.assert_array_equal(bounds.cpu().numpy(), g["f64_bounds"])
+    # dropping unreachable tiles changes nothing
+    np.testing.assert_array_equal(out_full.rgb, out.rgb)
+    np.testing.assert_array_equal(out_full.alpha, out.alpha)
 
 
 @pytest.mark.parametrize("name,maker", RENDER_CASES)
@@ -86,8 +97,9 @@ def test_binning_bit_exact_f32(gmr, name, maker):
     mesh = _mesh(case)
     pos, col, faces = gmr.api._device_mesh(mesh, np.float32)
     cam = case["camera"]
+    from paper_2602_14493_b200 import lib
     rgb, alpha, st = engine.render_forward(pos, col, faces, [cam], cam.width, cam.height,
-                                           case["background"], flags=1)
+                                           case["background"], flags=lib.FLAG_DEBUG_AUX | lib.FLAG_FULL_TILE_LISTS)
     rec, rect, cnt, aux = (x.cpu().numpy() for x in engine.copy_splats(st, len(mesh.facets), True))
     kept = np.where(cnt > 0)[0]
     mean2d = rec[kept, 0:2]
@@ -176,3 +188,36 @@ def test_fresh_scene_f64_vs_oracle(gmr):
     assert np.abs(out.rgb - rgb).max() <= 1e-10
     gv, gcol = gmr.render_backward(ctx, g_rgb, g_a)
     assert rel(gv, ogv) <= 1e-8 and rel(gcol, ogc) <= 1e-8
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_unreachable_tile_culling_is_exact(gmr, dtype):
+    """Default lists drop the tiles a splat's padded ellipse cannot reach:
+    same images and gradients bit for bit as the reference's full lists,
+    and every (tile, face) list is an order-preserving subsequence."""
+    import torch
+    from paper_2602_14493_b200 import engine, lib
+    mesh = gmr.make_geodesic_sphere(40, seed=3)
+    cams = gmr.hemisphere_cameras(3, 3.0, (200, 136))
+    tdt = torch.float64 if dtype == np.float64 else torch.float32
+    pos = torch.tensor(mesh.vertices, dtype=tdt, device="cuda")
+    col = torch.tensor(mesh.colors, dtype=tdt, device="cuda")
+    faces = torch.tensor(mesh.facets, dtype=torch.int32, device="cuda")
+    g = torch.Generator(device="cuda").manual_seed(5)
+    g_rgb = torch.randn((3, 136, 200, 3), generator=g, device="cuda", dtype=tdt)
+    g_a = torch.randn((3, 136, 200), generator=g, device="cuda", dtype=tdt)
+    res = {}
+    for name, flags in (("cull", 0), ("full", lib.FLAG_FULL_TILE_LISTS)):
+        rgb, alpha, st = engine.render_forward(pos, col, faces, cams, 200, 136, (0.1, 0.2, 0.3), flags=flags)
+        gp, gc = engine.render_backward(st, pos, col, faces, rgb, g_rgb, g_a)
+        items, bounds = engine.copy_entries(st, len(mesh.facets), True)
+        res[name] = (rgb, alpha, gp, gc, items.cpu().numpy(), bounds.cpu().numpy(), st.entries)
+    for k in range(4):
+        assert torch.equal(res["cull"][k], res["full"][k]), k
+    ic, bc, ec = res["cull"][4:]
+    iff, bf, ef = res["full"][4:]
+    assert ec < ef        # some tiles were dropped
+    for t in range(len(bf) - 1):
+        lc, lf = ic[bc[t]:bc[t + 1]], iff[bf[t]:bf[t + 1]]
+        it = iter(lf)
+        assert all(any(x == y for y in it) for x in lc), t   # subsequence
