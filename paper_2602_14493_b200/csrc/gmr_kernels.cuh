@@ -154,6 +154,14 @@ __device__ __forceinline__ void cam_m2(const Cam<S>& cam, const S t[3], S m2[2][
 // blend kernels anyway (the reference's _RasterPlan lists them,
 // render.py:214-226; GMR_FLAG_FULL_TILE_LISTS keeps them).
 constexpr int kMaskTiles = 32;
+// sqrt for the conservative tile test only: float uses the MUFU
+// approximation (relative error ~1e-7, far inside the 0.01 px extra padding)
+__device__ __forceinline__ float mask_sqrt(float x) {
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ double mask_sqrt(double x) { return sqrt(x); }
 template <typename S>
 __device__ __forceinline__ uint32_t rect_tile_mask(const Splat<S>& sp, int tx0, int ty0, int tx1, int ty1) {
   const S mx = sp.a.x, my = sp.a.y, ca = sp.a.z, cb = sp.a.w, cc = sp.b.x, ey = sp.b.z, tau = sp.b.w;
@@ -169,7 +177,7 @@ __device__ __forceinline__ uint32_t rect_tile_mask(const Splat<S>& sp, int tx0, 
     const S dy = S(y) - my;
     const S disc = dy * dy * neg_det + ca * tau;
     if (!(disc >= S(0))) continue;
-    const S hw = sqrt_s(disc) * inv_a * S(1.0005) + S(0.02);
+    const S hw = mask_sqrt(disc) * inv_a * S(1.0005) + S(0.02);
     const S xc = mx - cb * dy * inv_a;
     const S lo = fmax(ceil(xc - hw), x_min), hi = fmin(floor(xc + hw), x_max);
     if (!(lo <= hi)) continue;
@@ -179,17 +187,18 @@ __device__ __forceinline__ uint32_t rect_tile_mask(const Splat<S>& sp, int tx0, 
   return m;
 }
 
-// per-item entry count + mask: culled (mask over <= 32 tiles) or the full rect
+// per-item emitted-tile mask (bit = row-major index in the rectangle) of a
+// rectangle of `area` tiles: all bits past 32 tiles, else culled or full;
+// the entry count is item_count(mask, area)
 template <typename S>
-__device__ __forceinline__ uint32_t item_tiles(const Splat<S>& sp, int tx0, int ty0, int tx1, int ty1, bool cull,
-                                               uint32_t& mask) {
-  const uint32_t area = (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
-  if (area > (uint32_t)kMaskTiles) {
-    mask = 0xffffffffu;
-    return area;
-  }
-  mask = cull ? rect_tile_mask(sp, tx0, ty0, tx1, ty1) : (0xffffffffu >> (32 - area));
-  return (uint32_t)__popc(mask);
+__device__ __forceinline__ uint32_t item_mask(const Splat<S>& sp, int tx0, int ty0, int tx1, int ty1, uint32_t area,
+                                              bool cull) {
+  if (area > (uint32_t)kMaskTiles) return 0xffffffffu;
+  if (area == 1u || !cull) return 0xffffffffu >> (32 - area);
+  return rect_tile_mask(sp, tx0, ty0, tx1, ty1);
+}
+__device__ __forceinline__ uint32_t item_count(uint32_t mask, uint32_t area) {
+  return area > (uint32_t)kMaskTiles ? area : (uint32_t)__popc(mask);
 }
 
 // partial slot of an entry of `item` in tile (tx, ty): its rank among the
@@ -278,7 +287,9 @@ __global__ void __launch_bounds__(256) mesh_to_splats(MeshFwdArgs<S> p, const __
         if (on) {
           int tx0, ty0, tx1, ty1;
           tile_rect(mx, my, r, p.tiles_x, p.tiles_y, tx0, ty0, tx1, ty1);
-          cnt = item_tiles(rec, tx0, ty0, tx1, ty1, p.cull != 0, emask);
+          const uint32_t area = (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
+          emask = item_mask(rec, tx0, ty0, tx1, ty1, area, p.cull != 0);
+          cnt = item_count(emask, area);
           rc = make_uint2((uint32_t)tx0 | ((uint32_t)ty0 << 16), (uint32_t)tx1 | ((uint32_t)ty1 << 16));
           key = order_key(t[2]);
           ++kept;
@@ -356,8 +367,9 @@ __global__ void __launch_bounds__(256) pack_splats(PackArgs<S> p) {
   if (finite_s(mx) && finite_s(my) && finite_s(r))
     tile_rect(mx, my, r, p.tiles_x, p.tiles_y, tx0, ty0, tx1, ty1);
   const bool has_rect = tx1 >= tx0 && ty1 >= ty0;
-  uint32_t emask = 0;
-  const uint32_t cnt = has_rect ? item_tiles(rec, tx0, ty0, tx1, ty1, p.cull != 0, emask) : 0u;
+  const uint32_t area = has_rect ? (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1)) : 0u;
+  const uint32_t emask = has_rect ? item_mask(rec, tx0, ty0, tx1, ty1, area, p.cull != 0) : 0u;
+  const uint32_t cnt = has_rect ? item_count(emask, area) : 0u;
   p.splat[i] = rec;
   p.col4[i] = col;
   p.rect[i] = make_uint2((uint32_t)tx0 | ((uint32_t)ty0 << 16), (uint32_t)max(tx1, 0) | ((uint32_t)max(ty1, 0) << 16));
