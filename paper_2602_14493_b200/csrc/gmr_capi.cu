@@ -90,7 +90,7 @@ inline unsigned grid_for(uint64_t n, unsigned block) { return (unsigned)std::max
 
 // Workspace layout (byte offsets).
 struct Layout {
-  size_t status, splat, col4, rect, count, emask, dkey[2], ditem[2], offs, entry_off, bsum, nent;
+  size_t status, splat, col4, bin, count, dkey[2], ditem[2], offs, entry_off, bsum, nent;
   size_t ekey[2], eval[2], bounds, sched, t_final, hist, partial, partial_op, face_acc, corner, aux, loss_tile;
   size_t total;
   uint64_t items, faces, bins, pixels, ecap;
@@ -118,9 +118,8 @@ Layout plan(uint64_t faces, int views, int W, int H, uint64_t ecap, int dtype, b
   L.status = take(sizeof(DevStatus));
   L.splat = take(L.items * 8 * s);
   L.col4 = take(faces * 4 * s);
-  L.rect = take(L.items * 8);
+  L.bin = take(L.items * 16);
   L.count = take(L.items * 4);
-  L.emask = take(L.items * 4);
   L.dkey[0] = take(L.items * ks);
   L.dkey[1] = take(L.items * ks);
   L.ditem[0] = take(L.items * 4);
@@ -229,7 +228,7 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
   uint32_t* ek[2] = {at<uint32_t>(ws, L.ekey[0]), at<uint32_t>(ws, L.ekey[1])};
   uint32_t* ev[2] = {at<uint32_t>(ws, L.eval[0]), at<uint32_t>(ws, L.eval[1])};
   if (items) {
-    scan_emit<<<nb, 256, 0, st>>>(order, count, at<uint2>(ws, L.rect), at<uint32_t>(ws, L.emask), items, bsum,
+    scan_emit<<<nb, 256, 0, st>>>(order, at<uint4>(ws, L.bin), items, bsum,
                                   (uint32_t)L.faces,
                                   L.tiles_x, (uint32_t)L.tiles, nent, ek[0], ev[0]);
     GMR_LAUNCHED();
@@ -265,8 +264,7 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
   a.entry_item = ev[ecur];
   a.splat = at<Splat<S>>(ws, L.splat);
   a.col4 = at<V4<S>>(ws, L.col4);
-  a.rect = at<uint2>(ws, L.rect);
-  a.emask = at<uint32_t>(ws, L.emask);
+  a.bin = at<uint4>(ws, L.bin);
   a.entry_off = at<uint32_t>(ws, L.entry_off);
   a.items_per_view = (uint32_t)L.faces;
   a.tiles_x = L.tiles_x;
@@ -335,11 +333,10 @@ int render_forward_t(const GmrMesh* m, const GmrCamera* cams, int B, const GmrRa
     a.rescale = r->rescale;
     a.splat = at<Splat<S>>(ws, L.splat);
     a.col4 = at<V4<S>>(ws, L.col4);
-    a.rect = at<uint2>(ws, L.rect);
+    a.bin = at<uint4>(ws, L.bin);
     a.count = at<uint32_t>(ws, L.count);
     a.dkey = at<typename KeyOf<S>::type>(ws, L.dkey[0]);
     a.ditem = at<uint32_t>(ws, L.ditem[0]);
-    a.emask = at<uint32_t>(ws, L.emask);
     a.cull = (r->flags & GMR_FLAG_FULL_TILE_LISTS) ? 0 : 1;
     a.aux = (r->flags & GMR_FLAG_DEBUG_AUX) ? at<S>(ws, L.aux) : nullptr;
     a.st = at<DevStatus>(ws, L.status);
@@ -362,8 +359,7 @@ int blend_backward_launch(const Layout& L, void* ws, const GmrRaster* r, const v
   a.entry_item = at<uint32_t>(ws, L.eval[ecur]);
   a.splat = at<Splat<S>>(ws, L.splat);
   a.col4 = at<V4<S>>(ws, L.col4);
-  a.rect = at<uint2>(ws, L.rect);
-  a.emask = at<uint32_t>(ws, L.emask);
+  a.bin = at<uint4>(ws, L.bin);
   a.entry_off = at<uint32_t>(ws, L.entry_off);
   a.items_per_view = (uint32_t)L.faces;
   a.tiles_x = L.tiles_x;
@@ -466,11 +462,10 @@ int rasterize_forward_t(const GmrSplats* sp, const GmrRaster* r, void* rgb, void
   a.tiles_y = L.tiles_y;
   a.splat = at<Splat<S>>(ws, L.splat);
   a.col4 = at<V4<S>>(ws, L.col4);
-  a.rect = at<uint2>(ws, L.rect);
+  a.bin = at<uint4>(ws, L.bin);
   a.count = at<uint32_t>(ws, L.count);
   a.dkey = at<typename KeyOf<S>::type>(ws, L.dkey[0]);
   a.ditem = at<uint32_t>(ws, L.ditem[0]);
-  a.emask = at<uint32_t>(ws, L.emask);
   a.cull = (r->flags & GMR_FLAG_FULL_TILE_LISTS) ? 0 : 1;
   a.st = at<DevStatus>(ws, L.status);
   if (sp->count) {
@@ -875,7 +870,9 @@ int gmr_copy_splats(const void* ws, int64_t items_per_view, int32_t views, const
   cudaStream_t st = (cudaStream_t)stream;
   const size_t s = r->dtype == GMR_F64 ? 8 : 4;
   GMR_CUDA(cudaMemcpyAsync(records, (const char*)ws + L.splat, L.items * 8 * s, cudaMemcpyDeviceToDevice, st));
-  GMR_CUDA(cudaMemcpyAsync(rects, (const char*)ws + L.rect, L.items * 8, cudaMemcpyDeviceToDevice, st));
+  // rects = the first 8 bytes of each 16-byte bin record
+  if (L.items)
+    GMR_CUDA(cudaMemcpy2DAsync(rects, 8, (const char*)ws + L.bin, 16, 8, L.items, cudaMemcpyDeviceToDevice, st));
   GMR_CUDA(cudaMemcpyAsync(counts, (const char*)ws + L.count, L.items * 4, cudaMemcpyDeviceToDevice, st));
   if (aux && mesh_path)
     GMR_CUDA(cudaMemcpyAsync(aux, (const char*)ws + L.aux, L.items * 2 * s, cudaMemcpyDeviceToDevice, st));

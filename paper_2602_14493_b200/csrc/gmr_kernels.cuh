@@ -221,11 +221,10 @@ template <typename S> struct MeshFwdArgs {
   int rescale;
   Splat<S>* splat;
   V4<S>* col4;
-  uint2* rect;
-  uint32_t* count;
+  uint4* bin;        // [items]: (rect lo, rect hi, emitted-tile mask, entry count) -- one sector per gather
+  uint32_t* count;   // [items]: entry count again, for the sequential readers
   typename KeyOf<S>::type* dkey;
   uint32_t* ditem;
-  uint32_t* emask;   // [items]: emitted tiles of the rectangle (item_tiles)
   int cull;          // drop tiles the splat cannot reach (not GMR_FLAG_FULL_TILE_LISTS)
   S* aux;   // optional [items][2] = (radius, depth)
   DevStatus* st;
@@ -308,9 +307,8 @@ __global__ void __launch_bounds__(256) mesh_to_splats(MeshFwdArgs<S> p, const __
         }
       }
       p.splat[item] = rec;
-      p.rect[item] = rc;
+      p.bin[item] = make_uint4(rc.x, rc.y, emask, cnt);
       p.count[item] = cnt;
-      p.emask[item] = emask;
       p.dkey[item] = key;
       p.ditem[item] = (uint32_t)item;
     }
@@ -333,11 +331,10 @@ template <typename S> struct PackArgs {
   int tiles_x, tiles_y;
   Splat<S>* splat;
   V4<S>* col4;
-  uint2* rect;
+  uint4* bin;
   uint32_t* count;
   typename KeyOf<S>::type* dkey;
   uint32_t* ditem;
-  uint32_t* emask;
   int cull;
   DevStatus* st;
 };
@@ -372,9 +369,9 @@ __global__ void __launch_bounds__(256) pack_splats(PackArgs<S> p) {
   const uint32_t cnt = has_rect ? item_count(emask, area) : 0u;
   p.splat[i] = rec;
   p.col4[i] = col;
-  p.rect[i] = make_uint2((uint32_t)tx0 | ((uint32_t)ty0 << 16), (uint32_t)max(tx1, 0) | ((uint32_t)max(ty1, 0) << 16));
+  p.bin[i] = make_uint4((uint32_t)tx0 | ((uint32_t)ty0 << 16), (uint32_t)max(tx1, 0) | ((uint32_t)max(ty1, 0) << 16),
+                        emask, cnt);
   p.count[i] = cnt;
-  p.emask[i] = emask;
   p.dkey[i] = order_key(d);
   p.ditem[i] = item;
   if (has_rect) atomicAdd(&p.st->kept, 1ull);
@@ -447,9 +444,7 @@ __global__ void __launch_bounds__(kTopThreads) scan_top(uint32_t* __restrict__ b
 // rectangle (render.py:218-226): key = view * T + tile, value = item.
 // Skipped when the entries overflow.
 __global__ void __launch_bounds__(256) scan_emit(const uint32_t* __restrict__ order,
-                                                const uint32_t* __restrict__ count,
-                                                const uint2* __restrict__ rect,
-                                                const uint32_t* __restrict__ emask, uint32_t n,
+                                                const uint4* __restrict__ bin, uint32_t n,
                                                 const uint32_t* __restrict__ bsum,
                                                 uint32_t items_per_view, int tiles_x,
                                                 uint32_t tiles_per_view,
@@ -458,10 +453,11 @@ __global__ void __launch_bounds__(256) scan_emit(const uint32_t* __restrict__ or
   __shared__ uint32_t sw[8];
   const uint32_t i = blockIdx.x * (uint32_t)kScanTile + threadIdx.x;
   const uint32_t item = i < n ? order[i] : 0u;
-  const uint32_t c = i < n ? count[item] : 0u;
+  const uint4 bi = i < n ? bin[item] : make_uint4(0, 0, 0, 0);
+  const uint32_t c = bi.w;
   const uint32_t run = bsum[blockIdx.x] + block_exclusive_scan_256(c, sw, nullptr);
   if (i >= n || !c || *n_entries == 0) return;
-  const uint2 rc = rect[item];
+  const uint2 rc = make_uint2(bi.x, bi.y);
   const int tx0 = rc.x & 0xffff, ty0 = rc.x >> 16, tx1 = rc.y & 0xffff, ty1 = rc.y >> 16;
   const int w = tx1 - tx0 + 1;
   const uint32_t vbase = (item / items_per_view) * tiles_per_view;
@@ -474,7 +470,7 @@ __global__ void __launch_bounds__(256) scan_emit(const uint32_t* __restrict__ or
     }
   } else {
     // the rectangle's kept tiles, row-major (entry_rank order)
-    uint32_t m = emask[item], e = 0;
+    uint32_t m = bi.z, e = 0;
     while (m) {
       const int ri = __ffs(m) - 1;
       m &= m - 1;
@@ -602,8 +598,7 @@ template <typename S> struct BlendArgs {
   const uint32_t* entry_item;
   const Splat<S>* splat;
   const V4<S>* col4;
-  const uint2* rect;
-  const uint32_t* emask;     // emitted tiles per item (item_tiles)
+  const uint4* bin;          // per item: rect, emitted-tile mask, count
   const uint32_t* entry_off;
   uint32_t items_per_view;   // F (mesh) or K (splats)
   int tiles_x;
@@ -1187,7 +1182,8 @@ __global__ void __launch_bounds__(kBlendThreads, 5) blend_backward(BlendArgs<S> 
     if (kOpacity) aop += __shfl_xor_sync(0xffffffffu, aop, 1);
     if (half == 0 && je < n) {
       const uint32_t item_j = p.entry_item[base + je];
-      const uint32_t slot = p.entry_off[item_j] + entry_rank(p.rect[item_j], p.emask[item_j], tx, ty);
+      const uint4 bi = p.bin[item_j];
+      const uint32_t slot = p.entry_off[item_j] + entry_rank(make_uint2(bi.x, bi.y), bi.z, tx, ty);
       V4<S>* dst = reinterpret_cast<V4<S>*>(p.partial + (size_t)slot * 8);
       V4<S> lo, hi;
       lo.x = acc[0]; lo.y = acc[1]; lo.z = acc[2]; lo.w = acc[3];
@@ -1202,7 +1198,8 @@ __global__ void __launch_bounds__(kBlendThreads, 5) blend_backward(BlendArgs<S> 
   // which must hold zeros (every slot is written exactly once)
   for (uint32_t e = base + threadIdx.x; e < end; e += kBlendThreads) {
     const uint32_t item = p.entry_item[e];
-    const uint32_t slot = p.entry_off[item] + entry_rank(p.rect[item], p.emask[item], tx, ty);
+    const uint4 bi = p.bin[item];
+    const uint32_t slot = p.entry_off[item] + entry_rank(make_uint2(bi.x, bi.y), bi.z, tx, ty);
     V4<S>* dst = reinterpret_cast<V4<S>*>(p.partial + (size_t)slot * 8);
     V4<S> z;
     z.x = z.y = z.z = z.w = S(0);
