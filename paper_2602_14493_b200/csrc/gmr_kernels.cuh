@@ -146,11 +146,10 @@ __device__ __forceinline__ void cam_m2(const Cam<S>& cam, const S t[3], S m2[2][
 }
 
 // Tiles of a splat's rectangle that its padded ellipse can reach (bit
-// (ty - ty0) * w + (tx - tx0)), for rectangles of at most 32 tiles.  Rows
-// and half-widths are solved exactly as tile_coverage does (global pixel
-// coordinates here), with 0.01 px more padding, so every tile whose blend
-// coverage mask could be non-empty is kept: dropping the others changes no
-// pixel and no gradient.  Entries of dropped tiles would be empty in both
+// (ty - ty0) * w + (tx - tx0)), for rectangles of at most 32 tiles: a
+// superset of the tiles whose blend coverage mask (tile_coverage, same rows,
+// same padded half-widths) can be non-empty, so dropping the others changes
+// no pixel and no gradient.  Entries of dropped tiles would be empty in both
 // blend kernels anyway (the reference's _RasterPlan lists them,
 // render.py:214-226; GMR_FLAG_FULL_TILE_LISTS keeps them).
 constexpr int kMaskTiles = 32;
@@ -162,27 +161,59 @@ __device__ __forceinline__ float mask_sqrt(float x) {
   return r;
 }
 __device__ __forceinline__ double mask_sqrt(double x) { return sqrt(x); }
+__device__ __forceinline__ float mask_rcp(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ double mask_rcp(double x) { return 1.0 / x; }
 template <typename S>
 __device__ __forceinline__ uint32_t rect_tile_mask(const Splat<S>& sp, int tx0, int ty0, int tx1, int ty1) {
-  const S mx = sp.a.x, my = sp.a.y, ca = sp.a.z, cb = sp.a.w, cc = sp.b.x, ey = sp.b.z, tau = sp.b.w;
-  if (!(sp.b.y >= S(0)) || !(ca > S(0))) return 0u;
+  const S mx = sp.a.x, my = sp.a.y, ca = sp.a.z, cb = sp.a.w, cc = sp.b.x, ex = sp.b.y, ey = sp.b.z, tau = sp.b.w;
+  if (!(ex >= S(0)) || !(ca > S(0))) return 0u;   // never visible: tile_coverage marks nothing
   const int w = tx1 - tx0 + 1;
+  const int area = w * (ty1 - ty0 + 1);
+  const uint32_t full = area >= 32 ? 0xffffffffu : ((1u << area) - 1u);
+  const S neg_det = cb * cb - ca * cc;
+  if (!(neg_det < S(0)) || !(cc > S(0)) || !(tau >= S(0))) return full;   // not a proper ellipse: keep all
+  // the rows tile_coverage solves: ceil(my - ey) .. floor(my + ey)
   const S y_lo = fmax(ceil(my - ey), S(ty0 * kTile)), y_hi = fmin(floor(my + ey), S(ty1 * kTile + kTile - 1));
   if (!(y_lo <= y_hi)) return 0u;
-  const S neg_det = cb * cb - ca * cc;
-  const S inv_a = S(1) / ca;
+  const S inv_a = mask_rcp(ca);
+  // Over a band of rows, the padded spans of tile_coverage lie inside
+  // [Xmin - pad, Xmax + pad], where Xmin / Xmax are the extreme x of the
+  // tau-ellipse clipped to the band.  The clipped ellipse is convex, so its
+  // leftmost point is the ellipse's own leftmost point (row offset
+  // dys = cb sqrt(tau / (det cc))) if inside the band, else on a band edge;
+  // same for the right.  pad covers tile_coverage's 1.0005 h + 0.01, 0.01 px
+  // more, and rounding; rows whose discriminant is only negative by
+  // rounding are treated as touching.
+  const S dys = cb * mask_sqrt(tau * mask_rcp(-neg_det * cc));
+  const S pad = mask_sqrt(tau * inv_a) * S(0.0006) + S(0.03);
   const S x_min = S(tx0 * kTile), x_max = S(tx1 * kTile + kTile - 1);
   uint32_t m = 0;
-  for (int y = (int)y_lo; y <= (int)y_hi; ++y) {
-    const S dy = S(y) - my;
-    const S disc = dy * dy * neg_det + ca * tau;
-    if (!(disc >= S(0))) continue;
-    const S hw = mask_sqrt(disc) * inv_a * S(1.0005) + S(0.02);
-    const S xc = mx - cb * dy * inv_a;
-    const S lo = fmax(ceil(xc - hw), x_min), hi = fmin(floor(xc + hw), x_max);
+  for (int tr = (int)y_lo >> 4; tr <= ((int)y_hi >> 4); ++tr) {
+    const S ya = fmax(y_lo, S(tr * kTile)), yb = fmin(y_hi, S(tr * kTile + kTile - 1));
+    S xl = S(INFINITY), xr = S(-INFINITY);
+    auto probe = [&](S y, bool left, bool right) {
+      const S dy = y - my;
+      const S t1 = dy * dy * neg_det, t2 = ca * tau;
+      const S disc = t1 + t2;
+      if (!(disc >= S(-1e-5) * (fabs(t1) + fabs(t2)))) return;
+      const S h = mask_sqrt(fmax(disc, S(0))) * inv_a;
+      const S xc = mx - cb * dy * inv_a;
+      if (left) xl = fmin(xl, xc - h);
+      if (right) xr = fmax(xr, xc + h);
+    };
+    probe(ya, true, true);
+    probe(yb, true, true);
+    probe(fmin(fmax(my + dys, ya), yb), true, false);
+    probe(fmin(fmax(my - dys, ya), yb), false, true);
+    if (!(xl <= xr)) continue;                       // no row of the band meets the ellipse
+    const S lo = fmax(ceil(xl - pad), x_min), hi = fmin(floor(xr + pad), x_max);
     if (!(lo <= hi)) continue;
     const int ta = ((int)lo >> 4) - tx0, tb = ((int)hi >> 4) - tx0;
-    m |= ((0xffffffffu >> (31 - (tb - ta))) << ta) << (((y >> 4) - ty0) * w);
+    m |= ((0xffffffffu >> (31 - (tb - ta))) << ta) << ((tr - ty0) * w);
   }
   return m;
 }
