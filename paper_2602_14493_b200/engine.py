@@ -332,8 +332,30 @@ class GMRRender(torch.autograd.Function):
         return g_pos, g_col, None, None, None, None, None, None
 
 
+def _check_mesh_tensors(pos, col, faces):
+    if not (isinstance(pos, torch.Tensor) and isinstance(col, torch.Tensor) and isinstance(faces, torch.Tensor)):
+        raise TypeError("pos, col and faces must be torch tensors")
+    if pos.dtype not in _DT:
+        raise ValueError(f"pos must be float32 or float64, got {pos.dtype}")
+    if col.dtype != pos.dtype:
+        raise ValueError(f"col dtype {col.dtype} != pos dtype {pos.dtype}")
+    if faces.dtype != torch.int32:
+        raise ValueError(f"faces must be int32, got {faces.dtype}")
+    if pos.dim() != 2 or pos.shape[1] != 3 or col.shape != pos.shape:
+        raise ValueError(f"pos and col must both be [V, 3], got {tuple(pos.shape)} and {tuple(col.shape)}")
+    if faces.dim() != 2 or faces.shape[1] != 3:
+        raise ValueError(f"faces must be [F, 3], got {tuple(faces.shape)}")
+    if not (pos.is_cuda and col.device == pos.device and faces.device == pos.device):
+        raise ValueError("pos, col and faces must be on the same CUDA device")
+
+
 def render_views(pos, col, faces, cams, width, height, background=(0.0, 0.0, 0.0), rescale=True):
-    """Batched torch entry: B views of one mesh, differentiable in pos/col."""
+    """Batched torch entry: B views of one mesh, differentiable in pos/col.
+    pos, col [V,3] float32|float64 (same dtype), faces [F,3] int32, all on one
+    CUDA device.  Returns rgb [B,H,W,3], alpha [B,H,W] in pos's dtype."""
+    _check_mesh_tensors(pos, col, faces)
+    if len(cams) == 0:
+        raise ValueError("need at least one camera")
     return GMRRender.apply(pos, col, faces, list(cams), int(width), int(height),
                            tuple(np.asarray(background, dtype=np.float64).reshape(3)), bool(rescale))
 
