@@ -125,3 +125,43 @@ def test_sharded_image_loss_gpu_local_fn(gmr):
     assert s == pytest.approx(float(g["silhouette"]), rel=1e-10)
     assert rel(gp.cpu().numpy(), g["grad_v"]) <= 1e-8
     assert rel(gcol.cpu().numpy(), g["grad_c"]) <= 1e-8
+
+
+def test_unreachable_tile_culling_paths_against_oracle(gmr):
+    """Splats whose 3-sigma rectangle exceeds 32 tiles (no mask), and thin
+    diagonal splats whose rectangles have many unreachable tiles (mask path):
+    both must equal the reference semantics exactly (float64)."""
+    rng = np.random.default_rng(7)
+    W, H = 160, 120
+    k_big, k_thin = 12, 60
+    mean = np.concatenate([rng.uniform(20, 140, size=(k_big, 2)), rng.uniform(10, 150, size=(k_thin, 2))])
+    covs = []
+    for _ in range(k_big):
+        a = rng.normal(size=(2, 2))
+        covs.append(a @ a.T * 300.0 + np.eye(2) * 80.0)
+    for _ in range(k_thin):
+        th = rng.uniform(0, np.pi)
+        R = np.array([[np.cos(th), -np.sin(th)], [np.sin(th), np.cos(th)]])
+        covs.append(R @ np.diag([rng.uniform(30, 120), 0.3]) @ R.T)
+    k = k_big + k_thin
+    case = dict(mean2d=mean, cov2d=np.array(covs), depth=rng.uniform(1, 5, size=k), color=rng.random((k, 3)),
+                opacity=rng.uniform(0.05, 0.9, size=k), source=np.arange(k),
+                g_rgb=rng.normal(size=(H, W, 3)), g_alpha=rng.normal(size=(H, W)))
+    _check_splats(gmr, case, W, H)
+
+
+@pytest.mark.parametrize("W,H", [(1, 37), (53, 1), (1, 1)])
+def test_one_pixel_wide_images(gmr, W, H):
+    from paper_2602_14493_b200.camera import Camera
+    m = gmr.make_icosphere(80)
+    f = 3.0 * max(W, H)
+    cam = Camera(rotation=np.eye(3), translation=np.array([0.0, 0.0, 3.0]), fx=f, fy=f,
+                 cx=(W - 1) / 2, cy=(H - 1) / 2, width=W, height=H)
+    out, ctx = gmr.render_mesh(m, cam, background=(0.3, 0.2, 0.1), return_ctx=True)
+    r, a, octx = orc.render(m.vertices, m.facets, m.colors, cam, (0.3, 0.2, 0.1))
+    assert np.abs(out.rgb - r).max() <= 1e-10 and np.abs(out.alpha - a).max() <= 1e-10
+    rng = np.random.default_rng(0)
+    g_rgb, g_a = rng.normal(size=(H, W, 3)), rng.normal(size=(H, W))
+    gv, gc = gmr.render_backward(ctx, g_rgb, g_a)
+    ogv, ogc = orc.render_grad(octx, g_rgb, g_a)
+    assert rel(gv, ogv) <= 1e-8 and rel(gc, ogc) <= 1e-8
