@@ -902,7 +902,7 @@ struct BitWalk {
 };
 
 template <typename S>
-__global__ void __launch_bounds__(kBlendThreads, 6) blend_forward(BlendArgs<S> p) {
+__global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 4 : 6) blend_forward(BlendArgs<S> p) {
   __shared__ StageSmem<S, kFwdBatch> sm;
   const uint32_t g = p.sched ? p.sched[blockIdx.x] : blockIdx.x;
   const uint32_t view = g / p.tiles_per_view, t = g % p.tiles_per_view;
@@ -1027,7 +1027,7 @@ template <typename S, bool kOpacity> struct BwdSmem {
 //    in pixel order; the halves are combined in a fixed order.
 //  No atomics, fixed orders: the result is deterministic.
 template <typename S, bool kOpacity>
-__global__ void __launch_bounds__(kBlendThreads, 5) blend_backward(BlendArgs<S> p) {
+__global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : 5) blend_backward(BlendArgs<S> p) {
   extern __shared__ __align__(32) unsigned char dyn[];
   typedef BwdSmem<S, kOpacity> Sm;
   typedef typename Sm::Rec Rec;
