@@ -91,7 +91,7 @@ inline unsigned grid_for(uint64_t n, unsigned block) { return (unsigned)std::max
 // Workspace layout (byte offsets).
 struct Layout {
   size_t status, splat, col4, bin, count, dkey[2], ditem[2], offs, entry_off, bsum, nent;
-  size_t ekey[2], eval[2], bounds, sched, t_final, hist, partial, partial_op, face_acc, corner, aux, loss_tile;
+  size_t ekey[2], eval[2], bounds, sched, covbuf, t_final, hist, partial, partial_op, face_acc, corner, aux, loss_tile;
   size_t total;
   uint64_t items, faces, bins, pixels, ecap;
   int views, tiles_x, tiles_y, tiles;
@@ -134,6 +134,7 @@ Layout plan(uint64_t faces, int views, int W, int H, uint64_t ecap, int dtype, b
   L.eval[1] = take(ecap * 4);
   L.bounds = take((L.bins + 1) * 4);
   L.sched = take(L.bins * 4);
+  L.covbuf = take(ecap * 32);
   L.t_final = take(L.pixels * s);
   L.hist = take(std::max(radix_hist_words((uint32_t)std::min<uint64_t>(L.items, 0xffffffffu)),
                          radix_hist_words((uint32_t)std::min<uint64_t>(ecap, 0xffffffffu))) * 4);
@@ -286,6 +287,8 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
     a.g_alpha_out = (S*)la->g_alpha;
     a.loss_tile = at<double>(ws, L.loss_tile);
   }
+  // forwards that can be followed by a backward keep their coverage masks
+  a.covbuf = ia ? nullptr : at<uint32_t>(ws, L.covbuf);
   if (ia) {
     a.rgb8 = ia->rgb8;
     a.alpha8 = ia->alpha8;
@@ -356,6 +359,7 @@ int blend_backward_launch(const Layout& L, void* ws, const GmrRaster* r, const v
   BlendArgs<S> a{};
   a.bounds = at<uint32_t>(ws, L.bounds);
   a.sched = at<uint32_t>(ws, L.sched);
+  a.covbuf = at<uint32_t>(ws, L.covbuf);   // the forward's coverage masks
   a.entry_item = at<uint32_t>(ws, L.eval[ecur]);
   a.splat = at<Splat<S>>(ws, L.splat);
   a.col4 = at<V4<S>>(ws, L.col4);

@@ -652,6 +652,7 @@ template <typename S> struct BlendArgs {
   S* g_rgb_out;            // [B,H,W,3] dL/drgb (pre-scaled), read by K4
   S* g_alpha_out;          // [B,H,W]
   double* loss_tile;       // [bins][2]: sum of squared colour error, sum of BCE
+  uint32_t* covbuf;        // [entries][8] coverage words: written by the forward, read by the backward (or null)
   // optional 8-bit images (dataset.py:59-61 `_save_png`); rgb/alpha may then be null
   uint8_t* rgb8;           // [B,H,W,3]
   uint8_t* alpha8;         // [B,H,W]
@@ -922,6 +923,14 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 4 : 6) blend_f
     const int n = (int)min((uint32_t)kFwdBatch, end - base);
     stage_batch<S, kFwdBatch>(p, sm, base, n, vbase_item, x0, y0);
     __syncthreads();
+    if (p.covbuf) {   // keep the coverage masks for the backward (coalesced 32-byte rows)
+      for (int i = threadIdx.x; i < n; i += kBlendThreads) {
+        const uint32_t* w = sm.cov[i];
+        uint4* dst = reinterpret_cast<uint4*>(p.covbuf + (size_t)(base + i) * 8);
+        dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+        dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+      }
+    }
     const uint32_t nxt_e = base + kFwdBatch + threadIdx.x;
     const uint32_t nxt = nxt_e < end ? p.entry_item[nxt_e] : 0xffffffffu;
     BitWalk it;
@@ -1080,7 +1089,14 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : 5) blend_b
         sm.st.mean[i] = m;
         sm.st.q[i] = Eval<S>::prep(s.a.z, s.a.w, s.b.x, c.w);
         sm.st.col[i] = c;
-        tile_coverage(s.a, s.b, x0, y0, w);
+        if (p.covbuf) {   // the forward's masks for these entries
+          const uint4* src = reinterpret_cast<const uint4*>(p.covbuf + (size_t)(base + i) * 8);
+          const uint4 lo = src[0], hi = src[1];
+          w[0] = lo.x; w[1] = lo.y; w[2] = lo.z; w[3] = lo.w;
+          w[4] = hi.x; w[5] = hi.y; w[6] = hi.z; w[7] = hi.w;
+        } else {
+          tile_coverage(s.a, s.b, x0, y0, w);
+        }
       }
     }
     __syncthreads();
