@@ -1193,6 +1193,8 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : 5) blend_b
       }
     }
     prefetch_records(p, nxt, vbase_item);
+    if (p.covbuf && nxt != 0xffffffffu)   // and the next batch's coverage words
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(p.covbuf + (size_t)nxt_e * 8));
     __syncthreads();
     // ---- pass 2: my entry, my half of its records (pixel order) ----
     S acc[8];
