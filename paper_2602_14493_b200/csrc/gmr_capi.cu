@@ -205,7 +205,7 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
   {
     StageScope sc(kStDepthSort, st);
     cur = radix_sort_pairs<K>(dk, di, nullptr, items, items, L.depth_bits, at<uint32_t>(ws, L.hist), st);
-    g_launches += 3 * ((L.depth_bits + 7) / 8) - 1;
+    g_launches += radix_sort_launches<K>((uint32_t)items, L.depth_bits) - 1;
   }
   GMR_LAUNCHED();
   StageScope* emit_scope = new StageScope(kStEmit, st);
@@ -249,7 +249,7 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
   {
     StageScope sc(kStTileSort, st);
     ecur = radix_sort_pairs<uint32_t>(ek, ev, nent, 0, ecap, L.entry_bits, at<uint32_t>(ws, L.hist), st);
-    g_launches += 3 * ((L.entry_bits + 7) / 8);
+    g_launches += radix_sort_launches<uint32_t>(ecap, L.entry_bits);
     tile_ranges<<<grid_for((uint64_t)ecap / 4 + 1, 256), 256, 0, st>>>(ek[ecur], nent, 0, (uint32_t)L.bins,
                                                                   at<uint32_t>(ws, L.bounds));
     GMR_LAUNCHED();

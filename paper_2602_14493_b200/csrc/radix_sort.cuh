@@ -214,6 +214,144 @@ __global__ void __launch_bounds__(kSortThreads, 3) radix_downsweep(
   }
 }
 
+// ---------------------------------------------------------------------------
+// Small inputs: the whole sort in one 1024-thread block.  Each thread keeps
+// PER (key, value) pairs in registers (warp w owns items w*32*PER + r*32 +
+// lane); every digit pass ranks them stably exactly like radix_downsweep
+// (match_any, warps in order), scatters through one shared buffer and reads
+// back in the same striped order.  One launch instead of 3 per pass: small
+// meshes / images are launch-latency bound.  The result is written to the
+// buffer the multi-kernel path would use (passes & 1).
+// ---------------------------------------------------------------------------
+
+constexpr int kSmallThreads = 1024;
+constexpr int kSmallWarps = kSmallThreads / 32;
+
+template <typename K> struct SmallSortLimit { static constexpr uint32_t value = 16384; };
+template <> struct SmallSortLimit<unsigned long long> { static constexpr uint32_t value = 12288; };
+
+template <typename K>
+inline size_t small_sort_smem(uint32_t n_max) {
+  return (size_t)n_max * (sizeof(K) + 4) + (size_t)kSmallWarps * 256 * 4 + 1040 * 4;
+}
+
+template <typename K, int PER>
+__global__ void __launch_bounds__(kSmallThreads, 1) small_radix_sort(K* __restrict__ k0, uint32_t* __restrict__ v0,
+                                                                     K* __restrict__ k1, uint32_t* __restrict__ v1,
+                                                                     const uint32_t* n_dev, uint32_t n_host,
+                                                                     int bits, uint32_t n_max) {
+  extern __shared__ __align__(16) unsigned char ss_raw[];
+  K* skeys = reinterpret_cast<K*>(ss_raw);
+  uint32_t* svals = reinterpret_cast<uint32_t*>(ss_raw + (size_t)n_max * sizeof(K));
+  uint32_t(*wc)[256] = reinterpret_cast<uint32_t(*)[256]>(ss_raw + (size_t)n_max * (sizeof(K) + 4));
+  uint32_t* tot = reinterpret_cast<uint32_t*>(wc + kSmallWarps);   // [256] digit totals, [256..263] scan, [264] flag
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t n = sort_count(n_dev, n_host);
+  const uint32_t seg = (uint32_t)warp * (PER * 32);
+  K key[PER];
+  uint32_t val[PER];
+#pragma unroll
+  for (int r = 0; r < PER; ++r) {
+    const uint32_t idx = seg + r * 32 + lane;
+    key[r] = idx < n ? k0[idx] : K(0);
+    val[r] = idx < n ? v0[idx] : 0u;
+  }
+  const unsigned lt = lanemask_lt_sort();
+  const int passes = (bits + 7) / 8;
+  for (int pass = 0; pass < passes; ++pass) {
+    const int shift = 8 * pass;
+    for (int i = tid; i < kSmallWarps * 256; i += kSmallThreads) (&wc[0][0])[i] = 0;
+    __syncthreads();
+    uint16_t rank[PER];
+#pragma unroll
+    for (int r = 0; r < PER; ++r) {
+      const uint32_t idx = seg + r * 32 + lane;
+      const bool valid = idx < n;
+      const uint32_t d = valid ? ((uint32_t)(key[r] >> shift) & 255u) : 256u;
+      const unsigned peers = __match_any_sync(0xffffffffu, d);
+      const uint32_t c = valid ? wc[warp][d] : 0u;
+      rank[r] = (uint16_t)(c + __popc(peers & lt));
+      __syncwarp();
+      if (valid && (lt & peers) == 0) wc[warp][d] = c + __popc(peers);
+      __syncwarp();
+    }
+    __syncthreads();
+    // digit tid: per-warp exclusive prefixes; digit totals; exclusive scan
+    if (tid < 256) {
+      uint32_t run = 0;
+      for (int w = 0; w < kSmallWarps; ++w) {
+        const uint32_t c = wc[w][tid];
+        wc[w][tid] = run;
+        run += c;
+      }
+      tot[tid] = run;
+    }
+    __syncthreads();
+    if (tid < 32) {   // one warp scans the 256 totals (8 per lane)
+      uint32_t v[8], s8 = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) { v[k] = tot[lane * 8 + k]; s8 += v[k]; }
+      uint32_t x = s8;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      uint32_t run = x - s8;
+      bool triv = false;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) { triv |= v[k] == n; tot[lane * 8 + k] = run; run += v[k]; }
+      const bool any_triv = __any_sync(0xffffffffu, triv);
+      if (lane == 0) tot[264] = any_triv ? 1u : 0u;
+    }
+    __syncthreads();
+    if (tot[264]) continue;   // identity permutation: the registers are already in order
+#pragma unroll
+    for (int r = 0; r < PER; ++r) {
+      const uint32_t idx = seg + r * 32 + lane;
+      if (idx < n) {
+        const uint32_t d = (uint32_t)(key[r] >> shift) & 255u;
+        const uint32_t lp = tot[d] + wc[warp][d] + rank[r];
+        skeys[lp] = key[r];
+        svals[lp] = val[r];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < PER; ++r) {
+      const uint32_t idx = seg + r * 32 + lane;
+      if (idx < n) {
+        key[r] = skeys[idx];
+        val[r] = svals[idx];
+      }
+    }
+    __syncthreads();
+  }
+  K* kout = (passes & 1) ? k1 : k0;
+  uint32_t* vout = (passes & 1) ? v1 : v0;
+#pragma unroll
+  for (int r = 0; r < PER; ++r) {
+    const uint32_t idx = seg + r * 32 + lane;
+    if (idx < n) {
+      kout[idx] = key[r];
+      vout[idx] = val[r];
+    }
+  }
+}
+
+template <typename K, int PER>
+inline void launch_small_sort(K* keys[2], uint32_t* vals[2], const uint32_t* n_dev, uint32_t n_host, int bits,
+                              uint32_t n_max, cudaStream_t stream) {
+  static bool attr = false;
+  const size_t smem = small_sort_smem<K>(SmallSortLimit<K>::value);
+  if (!attr) {
+    cudaFuncSetAttribute(small_radix_sort<K, PER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  small_radix_sort<K, PER><<<1, kSmallThreads, small_sort_smem<K>(n_max), stream>>>(
+      keys[0], vals[0], keys[1], vals[1], n_dev, n_host, bits, n_max);
+}
+
 // Host-side driver: sorts [0, n) of (keys[0], vals[0]) by bits [0, bits).
 // Ping-pongs between buffer 0 and 1; returns the index (0/1) holding the
 // result.  `capacity` bounds n and sizes the grids; hist needs
@@ -224,6 +362,15 @@ inline int radix_sort_pairs(K* keys[2], uint32_t* vals[2], const uint32_t* n_dev
                             cudaStream_t stream) {
   const int nblocks = (int)((capacity + kSortTile - 1) / kSortTile);
   if (nblocks == 0 || bits <= 0) return 0;
+  if (capacity <= SmallSortLimit<K>::value) {   // one block, one launch
+    const uint32_t per = (capacity + kSmallThreads - 1) / kSmallThreads;
+    if (per <= 2) launch_small_sort<K, 2>(keys, vals, n_dev, n_host, bits, capacity, stream);
+    else if (per <= 4) launch_small_sort<K, 4>(keys, vals, n_dev, n_host, bits, capacity, stream);
+    else if (per <= 8) launch_small_sort<K, 8>(keys, vals, n_dev, n_host, bits, capacity, stream);
+    else if (per <= 12) launch_small_sort<K, 12>(keys, vals, n_dev, n_host, bits, capacity, stream);
+    else launch_small_sort<K, 16>(keys, vals, n_dev, n_host, bits, capacity, stream);
+    return ((bits + 7) / 8) & 1;
+  }
   uint32_t* totals = hist + (size_t)256 * nblocks;
   static bool attr_set = false;   // per K instantiation
   if (!attr_set) {
@@ -241,6 +388,13 @@ inline int radix_sort_pairs(K* keys[2], uint32_t* vals[2], const uint32_t* n_dev
     cur ^= 1;
   }
   return cur;
+}
+
+// kernel launches of one radix_sort_pairs call
+template <typename K>
+inline int radix_sort_launches(uint32_t capacity, int bits) {
+  if (capacity == 0 || bits <= 0) return 0;
+  return capacity <= SmallSortLimit<K>::value ? 1 : 3 * ((bits + 7) / 8);
 }
 
 inline size_t radix_hist_words(uint32_t capacity) {
