@@ -297,12 +297,10 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
     StageScope sc(kStBlendFwd, st);
     // all of the SM's unified L1/shared memory as shared memory: the
     // default carveout would cap residency below what registers allow
-    static bool attr_set = false;   // once per instantiation (also keeps it out of graph captures)
-    if (!attr_set) {
-      GMR_CUDA(cudaFuncSetAttribute(blend_forward<S>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                    (int)cudaSharedmemCarveoutMaxShared));
-      attr_set = true;
-    }
+    // once per instantiation (thread-safe static init; also keeps it out of graph captures)
+    static const cudaError_t attr_rc = cudaFuncSetAttribute(
+        blend_forward<S>, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+    GMR_CUDA(attr_rc);
     blend_forward<S><<<(unsigned)L.bins, kBlendThreads, 0, st>>>(a);
     GMR_LAUNCHED();
   }
@@ -380,13 +378,16 @@ int blend_backward_launch(const Layout& L, void* ws, const GmrRaster* r, const v
   a.partial = at<S>(ws, L.partial);
   a.partial_op = kOpacity ? at<S>(ws, L.partial_op) : nullptr;
   const size_t dyn = sizeof(BwdSmem<S, kOpacity>);
-  static bool attr_set = false;   // once per instantiation (also keeps it out of graph captures)
-  if (!attr_set) {
-    GMR_CUDA(cudaFuncSetAttribute(blend_backward<S, kOpacity>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
-    GMR_CUDA(cudaFuncSetAttribute(blend_backward<S, kOpacity>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                  (int)cudaSharedmemCarveoutMaxShared));
-    attr_set = true;
-  }
+  // once per instantiation (thread-safe static init; also keeps it out of graph captures)
+  static const cudaError_t attr_rc = [dyn] {
+    const cudaError_t e = cudaFuncSetAttribute(blend_backward<S, kOpacity>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    return e != cudaSuccess ? e
+                            : cudaFuncSetAttribute(blend_backward<S, kOpacity>,
+                                                   cudaFuncAttributePreferredSharedMemoryCarveout,
+                                                   (int)cudaSharedmemCarveoutMaxShared);
+  }();
+  GMR_CUDA(attr_rc);
   if (L.bins) {
     StageScope sc(kStBlendBwd, st);
     blend_backward<S, kOpacity><<<(unsigned)L.bins, kBlendThreads, dyn, st>>>(a);

@@ -342,12 +342,11 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_radix_sort(K* __restri
 template <typename K, int PER>
 inline void launch_small_sort(K* keys[2], uint32_t* vals[2], const uint32_t* n_dev, uint32_t n_host, int bits,
                               uint32_t n_max, cudaStream_t stream) {
-  static bool attr = false;
-  const size_t smem = small_sort_smem<K>(SmallSortLimit<K>::value);
-  if (!attr) {
-    cudaFuncSetAttribute(small_radix_sort<K, PER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  // thread-safe one-time attribute; a failure surfaces as the launch error
+  static const cudaError_t attr_rc = cudaFuncSetAttribute(
+      small_radix_sort<K, PER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      (int)small_sort_smem<K>(SmallSortLimit<K>::value));
+  (void)attr_rc;
   small_radix_sort<K, PER><<<1, kSmallThreads, small_sort_smem<K>(n_max), stream>>>(
       keys[0], vals[0], keys[1], vals[1], n_dev, n_host, bits, n_max);
 }
@@ -372,12 +371,10 @@ inline int radix_sort_pairs(K* keys[2], uint32_t* vals[2], const uint32_t* n_dev
     return ((bits + 7) / 8) & 1;
   }
   uint32_t* totals = hist + (size_t)256 * nblocks;
-  static bool attr_set = false;   // per K instantiation
-  if (!attr_set) {
-    cudaFuncSetAttribute(radix_downsweep<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sizeof(DownSmem<K>));
-    attr_set = true;
-  }
+  // thread-safe one-time attribute per K; a failure surfaces as the launch error
+  static const cudaError_t attr_rc = cudaFuncSetAttribute(
+      radix_downsweep<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DownSmem<K>));
+  (void)attr_rc;
   int cur = 0;
   for (int shift = 0; shift < bits; shift += 8) {
     radix_upsweep<K><<<nblocks, kSortThreads, 0, stream>>>(keys[cur], n_dev, n_host, shift, hist,
