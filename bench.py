@@ -159,7 +159,10 @@ def run_gmr(args, cfg):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    # the multi-rank path (NCCL init, per-step all-reduce, max over ranks);
+    # GMR_BENCH_DIST=1 exercises it even with one rank under torchrun
+    multi = world > 1 or os.environ.get("GMR_BENCH_DIST") == "1"
+    if multi:
         dist.init_process_group("nccl", device_id=dev)
     L = lib.load()
     mesh = build_mesh(cfg)
@@ -184,7 +187,7 @@ def run_gmr(args, cfg):
         # so the device never drains between steps
         rgb, alpha, st = engine.render_forward(pos, col, faces, cams, W, H, BG, check=False)
         gp, gc = engine.render_backward(st, pos, col, faces, rgb, g_rgb, g_a)
-        if world > 1:
+        if multi:
             buf = torch.cat([gp, gc], dim=1)
             dist.all_reduce(buf)
         pending.append(st)
@@ -201,7 +204,7 @@ def run_gmr(args, cfg):
     L.gmr_timing_enable(1)
     L.gmr_timing_read(None, None, 0, 1)
     n0 = L.gmr_launch_count()
-    if world > 1:
+    if multi:
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -212,7 +215,7 @@ def run_gmr(args, cfg):
     e1.record()
     torch.cuda.synchronize()
     wall1 = time.time()
-    if world > 1:
+    if multi:
         dist.barrier()
     launches = (L.gmr_launch_count() - n0) // args.steps
     ms = e0.elapsed_time(e1)
@@ -221,7 +224,7 @@ def run_gmr(args, cfg):
     scnt = (ctypes.c_int64 * 8)()
     L.gmr_timing_read(sms, scnt, 8, 1)
     L.gmr_timing_enable(0)
-    if world > 1:
+    if multi:
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
@@ -269,7 +272,7 @@ def run_gmr(args, cfg):
             upload(slots[(k + 1) % 2])            # next step's inputs, behind this forward
         torch.autograd.backward([rgb, alpha], [s["g"], s["a"]])
         gp, gc = p.grad, c.grad
-        if world > 1:
+        if multi:
             buf = torch.cat([gp, gc], dim=1)
             dist.all_reduce(buf)
             gp, gc = buf[:, :3], buf[:, 3:]
@@ -286,7 +289,7 @@ def run_gmr(args, cfg):
     for i in range(max(1, args.warmup)):
         e2e_step(prefetch=i < max(1, args.warmup) - 1)
     torch.cuda.synchronize()
-    if world > 1:
+    if multi:
         dist.barrier()
     k_e2e = max(3, args.steps // 2)
     ctr[0] = 0
@@ -299,7 +302,7 @@ def run_gmr(args, cfg):
     e1.record()
     torch.cuda.synchronize()
     ms_e2e = e0.elapsed_time(e1)
-    if world > 1:
+    if multi:
         t = torch.tensor([ms_e2e], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_e2e = float(t.item())
@@ -308,7 +311,7 @@ def run_gmr(args, cfg):
     clocks = sampler.summary() if sampler else None
 
     if rank != 0:
-        if world > 1:
+        if multi:
             dist.destroy_process_group()
         return None
 
@@ -386,7 +389,7 @@ def run_gmr(args, cfg):
         "cpu_baseline": cpu,
     }
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if multi:
         dist.destroy_process_group()
     return line
 
