@@ -908,7 +908,6 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 4 : 6) blend_f
   const uint32_t g = p.sched ? p.sched[blockIdx.x] : blockIdx.x;
   const uint32_t view = g / p.tiles_per_view, t = g % p.tiles_per_view;
   const int tx = (int)(t % (uint32_t)p.tiles_x), ty = (int)(t / (uint32_t)p.tiles_x);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int x0 = tx * kTile, y0 = ty * kTile;
   const int px = x0 + tile_col(threadIdx.x), py = y0 + tile_row(threadIdx.x);
   const bool inside = px < p.W && py < p.H;
