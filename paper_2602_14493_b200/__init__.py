@@ -26,7 +26,7 @@ def __getattr__(name):
     if name in _ENGINE:
         from . import engine
         return getattr(engine, name)
-    if name in ("api", "engine", "parallel", "metrics", "dataset", "fit"):
+    if name in ("api", "engine", "dist", "metrics", "dataset", "fit"):
         import importlib
         return importlib.import_module(f".{name}", __name__)
     raise AttributeError(name)
