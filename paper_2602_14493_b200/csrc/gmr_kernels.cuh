@@ -903,7 +903,7 @@ struct BitWalk {
 };
 
 template <typename S>
-__global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 4 : 6) blend_forward(BlendArgs<S> p) {
+__global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 4 : 7) blend_forward(BlendArgs<S> p) {
   __shared__ StageSmem<S, kFwdBatch> sm;
   const uint32_t g = p.sched ? p.sched[blockIdx.x] : blockIdx.x;
   const uint32_t view = g / p.tiles_per_view, t = g % p.tiles_per_view;
