@@ -174,3 +174,41 @@ def eval_case():
         imgs.append((a, b))
     return dict(gt_vertices=gt.vertices, gt_facets=gt.facets, pred_vertices=pv, pred_facets=pf, pred_colors=col,
                 n_samples=3000, images=imgs)
+
+
+def fullsize_case():
+    """Config 3 cut to one view (BASELINE configs[3]: geodesic sphere of
+    frequency 158 = 499,280 facets, 800x800): the scene, background and a
+    seeded upstream gradient for the full-size parity sketch."""
+    from paper_2602_14493_b200.camera import hemisphere_cameras
+    from paper_2602_14493_b200.mesh import make_geodesic_sphere
+    mesh = make_geodesic_sphere(158, seed=0)
+    cam = hemisphere_cameras(1, 3.0, (800, 800))[0]
+    rng = np.random.default_rng(11)
+    return dict(vertices=mesh.vertices, facets=mesh.facets, colors=mesh.colors, camera=cam,
+                background=(0.1, 0.1, 0.1), g_rgb=rng.standard_normal((800, 800, 3)),
+                g_alpha=rng.standard_normal((800, 800)))
+
+
+SKETCH_ROWS = 16
+
+
+def sketch(x, seed):
+    """A seeded Gaussian random projection (SKETCH_ROWS x x.size) of a
+    flattened float64 array.  ||sketch(a) - sketch(b)|| / ||sketch(b)||
+    estimates the relative L2 distance of a and b (Johnson-Lindenstrauss, a
+    few tens of percent at 16 rows), so a few KB stand in for a 36 MB
+    fixture.  Generated row by row to bound memory."""
+    x = np.asarray(x, dtype=np.float64).ravel()
+    rng = np.random.default_rng(seed)
+    return np.array([rng.standard_normal(x.size) @ x for _ in range(SKETCH_ROWS)])
+
+
+def flip_stats(rgb_a, alpha_a, rgb_b, alpha_b, gv_a, gv_b, gc_a, gc_b):
+    """Precision-spread summary of two renders of one scene: pixels whose
+    colour or alpha differ by more than 1e-4 (decision flips), the covered
+    pixel count, and the global relative L2 of both gradients."""
+    d = np.maximum(np.abs(rgb_a - rgb_b).max(-1), np.abs(alpha_a - alpha_b))
+    rel = lambda x, y: float(np.linalg.norm(x - y) / np.linalg.norm(y))
+    return dict(flips=int((d > 1e-4).sum()), covered=int((alpha_b > 0).sum()),
+                rel_gv=rel(gv_a, gv_b), rel_gc=rel(gc_a, gc_b))

@@ -196,6 +196,26 @@ def fit_prefix_case(name, iterations=5):
     print(name, hist[:, 0])
 
 
+def fullsize_case(name):
+    """Config 3, one view, through the reference in float64 and float32
+    (~70 s of CPU): random-projection sketches of the float64 outputs (the
+    GPU test pins its own float64 path to them) and the reference's own
+    float32-vs-float64 spread (the GPU test bounds its float32 spread by it)."""
+    case = gc.fullsize_case()
+    mesh = ref_mesh(case)
+    cam = ref_cam(case["camera"])
+    res = {}
+    for dt in (np.float64, np.float32):
+        o, ctx = ms.render_mesh(mesh, cam, background=case["background"], dtype=dt, return_ctx=True)
+        gv, gcol = ms.render_backward(ctx, case["g_rgb"].astype(dt), case["g_alpha"].astype(dt))
+        res[dt] = [np.asarray(a, dtype=np.float64) for a in (o.rgb, o.alpha, gv, gcol)]
+    (r64, a64, gv64, gc64), (r32, a32, gv32, gc32) = res[np.float64], res[np.float32]
+    out = {f"sketch_{n}": gc.sketch(a, i) for i, (n, a) in enumerate(zip(("rgb", "alpha", "gv", "gc"), res[np.float64]))}
+    out.update({f"ref32_{k}": v for k, v in gc.flip_stats(r32, a32, r64, a64, gv32, gv64, gc32, gc64).items()})
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+    print(name, {k: (v if np.ndim(v) == 0 else v.shape) for k, v in out.items()})
+
+
 if __name__ == "__main__":
     render_case("c1_icosphere1280_128", gc.c1_case())
     render_case("octahedron_32", gc.octahedron_case())
@@ -206,6 +226,8 @@ if __name__ == "__main__":
     convert_case("convert_random50", gc.convert_case())
     views_case("views_ico320_13")
     eval_case("eval_ico320")
+    if "--fullsize" in sys.argv:
+        fullsize_case("fullsize_c3_view0")
     if "--fit" in sys.argv:
         fit_case("fit_c5_200")
         fit_prefix_case("fit_c5_5", 5)
