@@ -246,8 +246,8 @@ def run_gmr(args, cfg):
     o_gp = [torch.empty_like(h_pos).pin_memory() for _ in range(2)]
     o_gc = [torch.empty_like(h_col).pin_memory() for _ in range(2)]
     slots = [dict(p=torch.empty_like(pos), c=torch.empty_like(col), g=torch.empty_like(g_rgb),
-                  a=torch.empty_like(g_a), up=torch.cuda.Event(), used=torch.cuda.Event(),
-                  down=torch.cuda.Event()) for _ in range(2)]
+                  a=torch.empty_like(g_a), up=torch.cuda.Event(), up_g=torch.cuda.Event(),
+                  used=torch.cuda.Event(), down=torch.cuda.Event()) for _ in range(2)]
     main, up_s, down_s = torch.cuda.current_stream(), torch.cuda.Stream(), torch.cuda.Stream()
     ctr = [0]
 
@@ -256,9 +256,10 @@ def run_gmr(args, cfg):
             up_s.wait_event(s["used"])           # the step that last read this slot is done
             s["p"].copy_(h_pos, non_blocking=True)
             s["c"].copy_(h_col, non_blocking=True)
+            s["up"].record(up_s)                 # the forward needs only the mesh ...
             s["g"].copy_(h_g, non_blocking=True)
             s["a"].copy_(h_a, non_blocking=True)
-            s["up"].record(up_s)
+            s["up_g"].record(up_s)               # ... the backward the image grads
 
     def e2e_step(prefetch=True):
         k = ctr[0]
@@ -270,6 +271,7 @@ def run_gmr(args, cfg):
         rgb, alpha = gmr.render_views(p, c, faces, cams, W, H, BG)
         if prefetch:
             upload(slots[(k + 1) % 2])            # next step's inputs, behind this forward
+        main.wait_event(s["up_g"])
         torch.autograd.backward([rgb, alpha], [s["g"], s["a"]])
         gp, gc = p.grad, c.grad
         if multi:
@@ -291,7 +293,7 @@ def run_gmr(args, cfg):
     torch.cuda.synchronize()
     if multi:
         dist.barrier()
-    k_e2e = max(3, args.steps // 2)
+    k_e2e = max(3, args.steps)
     ctr[0] = 0
     e0.record()
     up_s.wait_stream(main)
