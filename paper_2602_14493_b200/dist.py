@@ -8,9 +8,12 @@ all-reduce of the packed [grad_pos | grad_col] (V x 6) buffer plus the
 loss partial sums.  One process per GPU, `torch.distributed` with NCCL
 over NVLink/NVSwitch (gloo works for CPU tests of this logic).
 
-Single-rank vs R-rank results differ only by the fp32 summation order of
-the all-reduce (rank order is fixed, so a given world size is
-deterministic).
+Single-rank vs R-rank results differ only by the summation order of the
+all-reduce.  NCCL picks its algorithm (ring, tree, NVLS in-switch
+reduction) per size and topology, so the default SUM is not guaranteed to
+be bit-identical across runs or machines; `reproducible=True` all-gathers
+the per-rank partials and sums them in rank order instead (SURVEY 8e's
+bit-reproducible mode): the result then depends only on the world size.
 """
 
 from __future__ import annotations
@@ -28,14 +31,27 @@ def shard_range(n: int, rank: int, world: int):
 
 
 def allreduce_vertex_grads(g_pos: torch.Tensor, g_col: torch.Tensor, extra: torch.Tensor | None = None,
-                           group=None):
-    """One packed SUM all-reduce of [grad_pos | grad_col (| extra scalars)]."""
+                           group=None, reproducible: bool = False):
+    """One packed SUM all-reduce of [grad_pos | grad_col (| extra scalars)].
+
+    reproducible: all-gather the packed partials and add them in rank order
+    (R x the buffer in memory and traffic; bit-identical for a given world
+    size whatever algorithm NCCL would have chosen)."""
     parts = [g_pos.reshape(-1), g_col.reshape(-1)]
     if extra is not None:
         parts.append(extra.reshape(-1).to(g_pos.dtype))
     buf = torch.cat(parts)
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-        dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+        if reproducible:
+            world = dist.get_world_size(group)
+            gathered = torch.empty(world * buf.numel(), dtype=buf.dtype, device=buf.device)
+            dist.all_gather_into_tensor(gathered, buf, group=group)
+            gathered = gathered.view(world, buf.numel())
+            buf = gathered[0].clone()
+            for r in range(1, world):
+                buf += gathered[r]
+        else:
+            dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
     n = g_pos.numel()
     out_pos = buf[:n].view_as(g_pos)
     out_col = buf[n:2 * n].view_as(g_col)
@@ -45,7 +61,7 @@ def allreduce_vertex_grads(g_pos: torch.Tensor, g_col: torch.Tensor, extra: torc
 
 def sharded_image_loss(local_fn: Callable, cameras: Sequence, target_rgb: Sequence, target_mask: Sequence,
                        num_vertices: int, w_color: float = 1.0, w_sil: float = 1.0, group=None,
-                       device=None):
+                       device=None, reproducible: bool = False):
     """Image part of `total_loss` (losses.py:146-164) over views sharded
     across the process group.
 
@@ -70,7 +86,7 @@ def sharded_image_loss(local_fn: Callable, cameras: Sequence, target_rgb: Sequen
         gp = torch.zeros((num_vertices, 3), dtype=torch.float64, device=device)
         gc = torch.zeros((num_vertices, 3), dtype=torch.float64, device=device)
     extra = torch.tensor([cval, sval], dtype=torch.float64, device=gp.device)
-    gp, gc, extra = allreduce_vertex_grads(gp, gc, extra, group)
+    gp, gc, extra = allreduce_vertex_grads(gp, gc, extra, group, reproducible)
     return float(extra[0]) / n, float(extra[1]) / n, gp, gc
 
 

@@ -47,7 +47,7 @@ def oracle_local_fn(case):
     return fn
 
 
-def _worker(rank, world, port, ncams, q):
+def _worker(rank, world, port, ncams, q, reproducible=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -57,7 +57,7 @@ def _worker(rank, world, port, ncams, q):
         rgbs = (case["target_rgb"] * 2)[:ncams]
         masks = (case["target_mask"] * 2)[:ncams]
         c, s, gp, gcol = gdist.sharded_image_loss(oracle_local_fn(case), cams, rgbs, masks,
-                                                  len(case["vertices"]))
+                                                  len(case["vertices"]), reproducible=reproducible)
         q.put((rank, c, s, gp.numpy(), gcol.numpy()))
     finally:
         dist.destroy_process_group()
@@ -87,6 +87,42 @@ def test_two_rank_sharding_matches_single_process(ncams):
         np.testing.assert_allclose(gcc, gcol, rtol=0, atol=1e-12)
     # both ranks hold identical results (replicated optimiser input)
     np.testing.assert_array_equal(res[0][3], res[1][3])
+
+
+def test_four_rank_reproducible_sum_in_rank_order():
+    """World size 4 over 3 views (one rank holds an empty shard), the
+    reproducible mode: every rank returns exactly the rank-order sum of the
+    per-shard partials, and that sum matches the single-process result."""
+    ncams, world = 3, 4
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, ncams, q, True)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=240) for _ in procs], key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    case = gc.loss_case()
+    cams, rgbs, masks = case["cameras"][:ncams], case["target_rgb"][:ncams], case["target_mask"][:ncams]
+    fn = oracle_local_fn(case)
+    V = len(case["vertices"])
+    exp_p, exp_c = np.zeros((V, 3)), np.zeros((V, 3))
+    for r in range(world):
+        lo, hi = gdist.shard_range(ncams, r, world)
+        if hi > lo:
+            _, _, a, b = fn(cams[lo:hi], rgbs[lo:hi], masks[lo:hi], 1.0 / ncams, 1.0 / ncams)
+        else:
+            a, b = np.zeros((V, 3)), np.zeros((V, 3))
+        exp_p, exp_c = exp_p + a, exp_c + b
+    cv, sv, gv, gcol = orc.views_image_grad(case["vertices"], case["facets"], case["colors"], cams, rgbs,
+                                            masks, background=case["background"])
+    for _, c, s, gp, gcc in res:
+        np.testing.assert_array_equal(gp, exp_p)
+        np.testing.assert_array_equal(gcc, exp_c)
+        np.testing.assert_allclose(gp, gv, rtol=0, atol=1e-12)
+        assert c == pytest.approx(cv, rel=1e-12) and s == pytest.approx(sv, rel=1e-12)
 
 
 def test_shard_ranges_cover_views_once():
