@@ -90,6 +90,15 @@ typedef struct {
  * are bit-identical either way, the tile lists are then a subsequence of the
  * reference's. */
 #define GMR_FLAG_FULL_TILE_LISTS 2
+/* GmrRaster.flags: order each (view, tile) list by depth after the tile sort
+ * (one CTA per tile list, in shared memory up to 2048 entries) instead of
+ * sorting all B*F splats by depth before emission.  The lists are identical
+ * either way ((tile, depth, source), render.py:227); per-tile ordering is
+ * faster when every list is short and slower when a few lists hold most of
+ * the entries (a distant mesh).  Byte 60 of the workspace (the device
+ * status) holds the longest list of the last forward, so a caller can pick
+ * the flag from the previous call. */
+#define GMR_FLAG_TILE_DEPTH_SORT 4
 
 /* Result of a forward pass, read back by gmr_status (synchronises). */
 typedef struct {

@@ -198,18 +198,23 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
                   void* status_host = nullptr, void* status_event = nullptr) {
   typedef typename KeyOf<S>::type K;
   const uint32_t items = (uint32_t)L.items;
-  // depth order of all items (stable: ties keep item = (view, face) order)
+  // (tile, depth, source) order (render.py:227), either way:
+  //  default: stable depth sort of all items, entries emitted in depth
+  //    order, stable (view, tile) sort;
+  //  GMR_FLAG_TILE_DEPTH_SORT: entries emitted in item order, stable
+  //    (view, tile) sort, then each tile list sorted by depth on its own.
+  const bool tile_depth_sort = (r->flags & GMR_FLAG_TILE_DEPTH_SORT) != 0;
   K* dk[2] = {at<K>(ws, L.dkey[0]), at<K>(ws, L.dkey[1])};
-  uint32_t* di[2] = {at<uint32_t>(ws, L.ditem[0]), at<uint32_t>(ws, L.ditem[1])};
-  int cur;
-  {
+  const uint32_t* order = nullptr;
+  if (!tile_depth_sort) {
+    uint32_t* di[2] = {at<uint32_t>(ws, L.ditem[0]), at<uint32_t>(ws, L.ditem[1])};
     StageScope sc(kStDepthSort, st);
-    cur = radix_sort_pairs<K>(dk, di, nullptr, items, items, L.depth_bits, at<uint32_t>(ws, L.hist), st);
+    const int cur = radix_sort_pairs<K>(dk, di, nullptr, items, items, L.depth_bits, at<uint32_t>(ws, L.hist), st);
     g_launches += radix_sort_launches<K>((uint32_t)items, L.depth_bits) - 1;
+    GMR_LAUNCHED();
+    order = di[cur];
   }
-  GMR_LAUNCHED();
   StageScope* emit_scope = new StageScope(kStEmit, st);
-  const uint32_t* order = di[cur];
   const uint32_t* count = at<uint32_t>(ws, L.count);
   const int nb = (int)((items + kScanTile - 1) / kScanTile);
   uint32_t* bsum = at<uint32_t>(ws, L.bsum);
@@ -255,10 +260,22 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
     GMR_LAUNCHED();
     if (L.bins) {
       tile_schedule<<<1, kSchedThreads, 0, st>>>(at<uint32_t>(ws, L.bounds), (uint32_t)L.bins,
-                                                 at<uint32_t>(ws, L.sched));
+                                                 at<uint32_t>(ws, L.sched), dst);
+      GMR_LAUNCHED();
     }
   }
-  GMR_LAUNCHED();
+  if (L.bins && tile_depth_sort) {
+    StageScope sc(kStDepthSort, st);
+    // heaviest bins first; bins over the shared-memory cap use the partial
+    // buffer (free until the backward) as key/value scratch
+    K* gk0 = at<K>(ws, L.partial);
+    K* gk1 = gk0 + ecap;
+    uint32_t* gv1 = reinterpret_cast<uint32_t*>(gk1 + ecap);
+    bin_depth_sort<K><<<(unsigned)L.bins, kBinSortThreads, 0, st>>>(at<uint32_t>(ws, L.bounds),
+                                                                    at<uint32_t>(ws, L.sched), dk[0], ev[ecur],
+                                                                    gk0, gk1, gv1);
+    GMR_LAUNCHED();
+  }
   BlendArgs<S> a{};
   a.bounds = at<uint32_t>(ws, L.bounds);
   a.sched = at<uint32_t>(ws, L.sched);

@@ -27,6 +27,7 @@ __global__ void reset_status(DevStatus* st) {
   st->kept = 0;
   for (int i = 0; i < 6; ++i) st->bad_item[i] = 0xffffffffu;
   st->overflow = 0;
+  st->max_bin = 0;
 }
 
 __device__ __forceinline__ void flag_bad(DevStatus* st, int field, uint32_t item) {
@@ -255,7 +256,7 @@ template <typename S> struct MeshFwdArgs {
   uint4* bin;        // [items]: (rect lo, rect hi, emitted-tile mask, entry count) -- one sector per gather
   uint32_t* count;   // [items]: entry count again, for the sequential readers
   typename KeyOf<S>::type* dkey;
-  uint32_t* ditem;
+  uint32_t* ditem;   // item ids for the global depth sort
   int cull;          // drop tiles the splat cannot reach (not GMR_FLAG_FULL_TILE_LISTS)
   S* aux;   // optional [items][2] = (radius, depth)
   DevStatus* st;
@@ -365,7 +366,7 @@ template <typename S> struct PackArgs {
   uint4* bin;
   uint32_t* count;
   typename KeyOf<S>::type* dkey;
-  uint32_t* ditem;
+  uint32_t* ditem;   // item ids for the global depth sort
   int cull;
   DevStatus* st;
 };
@@ -409,17 +410,17 @@ __global__ void __launch_bounds__(256) pack_splats(PackArgs<S> p) {
 }
 
 // ---------------------------------------------------------------------------
-// K2: counts in depth order -> offsets -> entries -> (view, tile) sort -> ranges
+// K2: counts -> offsets -> entries -> (view, tile) sort -> ranges -> per-bin depth sort
 // ---------------------------------------------------------------------------
 
-constexpr int kScanTile = 256;   // one depth-sorted splat per thread
+constexpr int kScanTile = 256;   // one splat per thread
 
 __global__ void __launch_bounds__(256) scan_reduce(const uint32_t* __restrict__ order,
                                                   const uint32_t* __restrict__ count, uint32_t n,
                                                   uint32_t* __restrict__ bsum) {
   __shared__ uint32_t sw[8];
   const uint32_t i = blockIdx.x * (uint32_t)kScanTile + threadIdx.x;
-  const uint32_t s = i < n ? count[order[i]] : 0u;
+  const uint32_t s = i < n ? count[order ? order[i] : i] : 0u;
   uint32_t tot;
   block_exclusive_scan_256(s, sw, &tot);
   if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
@@ -470,10 +471,10 @@ __global__ void __launch_bounds__(kTopThreads) scan_top(uint32_t* __restrict__ b
   }
 }
 
-// Entry emission: per depth-sorted splat (one per thread; block scan + the
-// block's carry from scan_top), write its tile entries row-major over its
-// rectangle (render.py:218-226): key = view * T + tile, value = item.
-// Skipped when the entries overflow.
+// Entry emission: per splat in `order` (item order when null; one per
+// thread; block scan + the block's carry from scan_top), write its tile
+// entries row-major over its rectangle (render.py:218-226): key = view * T +
+// tile, value = item.  Skipped when the entries overflow.
 __global__ void __launch_bounds__(256) scan_emit(const uint32_t* __restrict__ order,
                                                 const uint4* __restrict__ bin, uint32_t n,
                                                 const uint32_t* __restrict__ bsum,
@@ -483,7 +484,7 @@ __global__ void __launch_bounds__(256) scan_emit(const uint32_t* __restrict__ or
                                                 uint32_t* __restrict__ key, uint32_t* __restrict__ val) {
   __shared__ uint32_t sw[8];
   const uint32_t i = blockIdx.x * (uint32_t)kScanTile + threadIdx.x;
-  const uint32_t item = i < n ? order[i] : 0u;
+  const uint32_t item = i < n ? (order ? order[i] : i) : 0u;
   const uint4 bi = i < n ? bin[item] : make_uint4(0, 0, 0, 0);
   const uint32_t c = bi.w;
   const uint32_t run = bsum[blockIdx.x] + block_exclusive_scan_256(c, sw, nullptr);
@@ -585,13 +586,22 @@ constexpr int kSchedThreads = 1024;
 __device__ __forceinline__ uint32_t sched_bucket(uint32_t cnt) { return 255u - min(cnt >> 3, 255u); }
 
 __global__ void __launch_bounds__(kSchedThreads) tile_schedule(const uint32_t* __restrict__ bounds, uint32_t bins,
-                                                               uint32_t* __restrict__ order) {
+                                                               uint32_t* __restrict__ order, DevStatus* st) {
   __shared__ uint32_t hist[256];
+  __shared__ uint32_t longest;
   for (int i = threadIdx.x; i < 256; i += kSchedThreads) hist[i] = 0;
+  if (threadIdx.x == 0) longest = 0;
   __syncthreads();
-  for (uint32_t g = threadIdx.x; g < bins; g += kSchedThreads)
-    atomicAdd(&hist[sched_bucket(bounds[g + 1] - bounds[g])], 1u);
+  uint32_t mx = 0;
+  for (uint32_t g = threadIdx.x; g < bins; g += kSchedThreads) {
+    const uint32_t c = bounds[g + 1] - bounds[g];
+    mx = max(mx, c);
+    atomicAdd(&hist[sched_bucket(c)], 1u);
+  }
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  if ((threadIdx.x & 31) == 0) atomicMax(&longest, mx);
   __syncthreads();
+  if (threadIdx.x == 0) st->max_bin = longest;
   if (threadIdx.x < 32) {   // exclusive scan of the 256 buckets by one warp
     uint32_t v[8], s = 0;
 #pragma unroll
@@ -609,6 +619,170 @@ __global__ void __launch_bounds__(kSchedThreads) tile_schedule(const uint32_t* _
   __syncthreads();
   for (uint32_t g = threadIdx.x; g < bins; g += kSchedThreads)
     order[atomicAdd(&hist[sched_bucket(bounds[g + 1] - bounds[g])], 1u)] = g;
+}
+
+// ---------------------------------------------------------------------------
+// K2'': per-bin depth order (render.py:227 lexsort by (tile, depth, source)).
+// Entries are emitted in item order and the (view, tile) radix sort is
+// stable, so every bin's list arrives in source order.  A stable LSD radix
+// sort of each bin by its depth key then yields (tile, depth, source) — the
+// order a global depth sort of all B*F items before emission gives
+// (GMR_FLAG_TILE_DEPTH_SORT; the default is that global sort).  One CTA per
+// bin.
+// The digits are those of key - (the bin's smallest key), so a bin needs
+// only as many passes as its depth range has bytes.  Bins of up to BinSortCap entries are ranked in
+// shared memory; larger ones ping-pong through global scratch (the
+// backward's partial buffer, unused until the backward) in chunks.
+// ---------------------------------------------------------------------------
+
+constexpr int kBinSortThreads = 256;   // thread t owns digit t
+constexpr int kBinSortWarps = kBinSortThreads / 32;
+template <typename K> struct BinSortCap { static constexpr int value = sizeof(K) == 4 ? 2048 : 1024; };
+
+template <typename K> struct BinSortSmem {
+  static constexpr int kCap = BinSortCap<K>::value;
+  K key[2][kCap];
+  uint32_t val[2][kCap];
+  uint32_t cnt[kBinSortWarps][256];
+  uint32_t sw[kBinSortWarps];
+  K red_min[kBinSortWarps], red_max[kBinSortWarps];
+};
+
+// One stable pass on the 8-bit digit of (key - kmin) at `shift`: src -> dst
+// (shared or global).  Chunks of up to kCap elements in order; in a chunk
+// warp w ranks a contiguous segment (match_any groups; the group leader
+// owns the warp's running digit count), so the output keeps the input order
+// within each digit.
+template <typename K>
+__device__ __forceinline__ void bin_digit_pass(const K* sk, const uint32_t* sv, K* dk, uint32_t* dv, uint32_t n,
+                                               int shift, K kmin, BinSortSmem<K>& sm) {
+  constexpr int kCap = BinSortSmem<K>::kCap;
+  constexpr int kGroups = kCap / kBinSortThreads;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned lt = lanemask_lt_sort();
+  uint32_t run = 0;   // running output offset of digit tid
+  const bool multi = n > (uint32_t)kCap;
+  if (multi) {   // digit bases over the whole bin first
+    sm.cnt[0][tid] = 0;
+    __syncthreads();
+    for (uint32_t i = tid; i < n; i += kBinSortThreads)
+      atomicAdd(&sm.cnt[0][(uint32_t)((sk[i] - kmin) >> shift) & 255u], 1u);
+    __syncthreads();
+    run = block_exclusive_scan_256(sm.cnt[0][tid], sm.sw, nullptr);
+  }
+  for (uint32_t c0 = 0; c0 < n; c0 += kCap) {
+    const uint32_t m = min((uint32_t)kCap, n - c0);
+    const uint32_t seg = ((m + kBinSortThreads - 1) / kBinSortThreads) * 32;   // per warp, multiple of 32
+#pragma unroll
+    for (int w = 0; w < kBinSortWarps; ++w) sm.cnt[w][tid] = 0;
+    __syncthreads();
+    uint32_t dr[kGroups];   // digit << 16 | rank in the warp's digit run; ~0 = none
+    const uint32_t w0 = c0 + warp * seg;
+#pragma unroll
+    for (int j = 0; j < kGroups; ++j) {
+      dr[j] = 0xffffffffu;
+      if (32u * j < seg) {   // warp-uniform
+        const uint32_t i = w0 + 32 * j + lane;
+        const bool valid = i < c0 + m;
+        const uint32_t d = valid ? (uint32_t)((sk[i] - kmin) >> shift) & 255u : 0xffffffffu;
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        const int leader = __ffs(peers) - 1;
+        uint32_t old = 0;
+        if (valid && lane == leader) {
+          old = sm.cnt[warp][d];
+          sm.cnt[warp][d] = old + (uint32_t)__popc(peers);
+        }
+        old = __shfl_sync(0xffffffffu, old, leader);
+        __syncwarp();
+        if (valid) dr[j] = (d << 16) | (old + (uint32_t)__popc(peers & lt));
+      }
+    }
+    __syncthreads();
+    uint32_t pre[kBinSortWarps], tot = 0;
+#pragma unroll
+    for (int w = 0; w < kBinSortWarps; ++w) { pre[w] = tot; tot += sm.cnt[w][tid]; }
+    if (!multi) run = block_exclusive_scan_256(tot, sm.sw, nullptr);   // synchronises
+#pragma unroll
+    for (int w = 0; w < kBinSortWarps; ++w) sm.cnt[w][tid] = run + pre[w];
+    run += tot;
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kGroups; ++j) {
+      if (dr[j] != 0xffffffffu) {
+        const uint32_t i = w0 + 32 * j + lane;
+        const uint32_t pos = sm.cnt[warp][dr[j] >> 16] + (dr[j] & 0xffffu);
+        dk[pos] = sk[i];
+        dv[pos] = sv[i];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <typename K>
+__global__ void __launch_bounds__(kBinSortThreads, 4) bin_depth_sort(const uint32_t* __restrict__ bounds,
+                                                                  const uint32_t* __restrict__ sched,
+                                                                  const K* __restrict__ dkey,
+                                                                  uint32_t* __restrict__ entry_item,
+                                                                  K* __restrict__ gk0, K* __restrict__ gk1,
+                                                                  uint32_t* __restrict__ gv1) {
+  __shared__ BinSortSmem<K> sm;
+  const uint32_t g = sched ? sched[blockIdx.x] : blockIdx.x;
+  const uint32_t s = bounds[g], n = bounds[g + 1] - s;
+  if (n < 2) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool in_smem = n <= (uint32_t)BinSortSmem<K>::kCap;
+  K* k0 = in_smem ? sm.key[0] : gk0 + s;
+  K* k1 = in_smem ? sm.key[1] : gk1 + s;
+  uint32_t* v0 = in_smem ? sm.val[0] : entry_item + s;
+  uint32_t* v1 = in_smem ? sm.val[1] : gv1 + s;
+  K kmin = ~(K)0, kmax = 0;
+  for (uint32_t i = tid; i < n; i += kBinSortThreads) {
+    const uint32_t item = entry_item[s + i];
+    const K k = dkey[item];
+    if (in_smem) {
+      sm.key[0][i] = k;
+      sm.val[0][i] = item;
+    } else {
+      k0[i] = k;
+    }
+    kmin = min(kmin, k);
+    kmax = max(kmax, k);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+    kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+  }
+  if (lane == 0) { sm.red_min[warp] = kmin; sm.red_max[warp] = kmax; }
+  __syncthreads();
+#pragma unroll
+  for (int w = 0; w < kBinSortWarps; ++w) { kmin = min(kmin, sm.red_min[w]); kmax = max(kmax, sm.red_max[w]); }
+  // digits of (key - kmin): only as many passes as the bin's key range needs
+  const K range = kmax - kmin;
+  int cur = 0;
+  if (in_smem) {   // separate call sites: shared-memory addressing (LDS/STS) here
+    for (int shift = 0; shift < (int)(8 * sizeof(K)) && (range >> shift); shift += 8) {
+      if (cur == 0) bin_digit_pass<K>(sm.key[0], sm.val[0], sm.key[1], sm.val[1], n, shift, kmin, sm);
+      else bin_digit_pass<K>(sm.key[1], sm.val[1], sm.key[0], sm.val[0], n, shift, kmin, sm);
+      cur ^= 1;
+    }
+  } else {
+    for (int shift = 0; shift < (int)(8 * sizeof(K)) && (range >> shift); shift += 8) {
+      if (cur == 0) bin_digit_pass<K>(k0, v0, k1, v1, n, shift, kmin, sm);
+      else bin_digit_pass<K>(k1, v1, k0, v0, n, shift, kmin, sm);
+      cur ^= 1;
+    }
+  }
+  // the result goes back to entry_item[s, s+n)
+  if (in_smem) {
+    if (range) {
+      const uint32_t* src = sm.val[cur];
+      for (uint32_t i = tid; i < n; i += kBinSortThreads) entry_item[s + i] = src[i];
+    }
+  } else if (cur) {
+    for (uint32_t i = tid; i < n; i += kBinSortThreads) entry_item[s + i] = v1[i];
+  }
 }
 
 // ---------------------------------------------------------------------------

@@ -73,6 +73,46 @@ class _Capacity:
 
 
 _capacity = _Capacity()
+
+
+class _TileOrder:
+    """Chooses GMR_FLAG_TILE_DEPTH_SORT per call shape from the longest tile
+    list of the previous forward of that shape (device status byte 60,
+    copied behind the call without a sync).  Per-tile depth ordering when
+    every list fits the kernel's shared-memory sort; the global depth sort
+    otherwise, and for the first call of a shape.  Both give the same lists."""
+
+    LIMIT = {torch.float32: 2048, torch.float64: 1024}
+
+    def __init__(self):
+        self._last = {}
+        self._pending = {}
+
+    def flags(self, key, dtype):
+        if not AUTO_TILE_ORDER:
+            return 0
+        p = self._pending.get(key)
+        # (no event queries while a graph is being captured)
+        if p is not None and not torch.cuda.is_current_stream_capturing() and p[1].query():
+            self._last[key] = int(p[0].view(torch.int32)[0])
+            del self._pending[key]
+        last = self._last.get(key)
+        return L.FLAG_TILE_DEPTH_SORT if last is not None and last <= self.LIMIT[dtype] else 0
+
+    def note(self, key, ws):
+        if key in self._pending or torch.cuda.is_current_stream_capturing():
+            return
+        h = torch.empty(4, dtype=torch.uint8, pin_memory=True)
+        h.copy_(ws[60:64], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self._pending[key] = (h, ev)
+
+
+_order = _TileOrder()
+# False: never add GMR_FLAG_TILE_DEPTH_SORT on our own (tests pin the mode
+# through DEFAULT_FLAGS)
+AUTO_TILE_ORDER = True
 _topologies = {}
 
 
@@ -136,6 +176,7 @@ def render_forward(pos, col, faces, cams, width, height, background, rescale=Tru
     cam_arr = L.camera_struct(cams)
     mesh = mesh_struct(pos, col, faces)
     key = (F, B, int(width), int(height), dtype)
+    raster.flags |= _order.flags(key, dtype)
     cap = _capacity.get(key, F * B)
     rgb = torch.empty((B, height, width, 3), dtype=dtype, device=pos.device)
     alpha = torch.empty((B, height, width), dtype=dtype, device=pos.device)
@@ -145,6 +186,7 @@ def render_forward(pos, col, faces, cams, width, height, background, rescale=Tru
         ws = torch.empty(nb.value, dtype=torch.uint8, device=pos.device)
         L.check(lib.gmr_render_forward(ctypes.byref(mesh), cam_arr, B, ctypes.byref(raster), _ptr(rgb),
                                        _ptr(alpha), _ptr(ws), nb.value, cap, _stream()))
+        _order.note(key, ws)
         st = ForwardState(ws, cap, raster, cam_arr, B, -1, -1)
         # the 64-byte device status, copied behind the forward (no sync)
         st.status_host = torch.empty(64, dtype=torch.uint8, pin_memory=True)
@@ -167,6 +209,7 @@ def render_forward(pos, col, faces, cams, width, height, background, rescale=Tru
         L.check(lib.gmr_render_forward_ex(ctypes.byref(mesh), cam_arr, B, ctypes.byref(raster), _ptr(rgb),
                                           _ptr(alpha), _ptr(ws), nb.value, cap, ctypes.c_void_p(status.data_ptr()),
                                           ctypes.c_void_p(ev.cuda_event), _stream()))
+        _order.note(key, ws)
         ev.synchronize()
         entries, kept, bad, overflow = _parse_status(status.numpy())
         for field in range(6):
@@ -203,6 +246,7 @@ def render_forward_loss(pos, col, faces, cams, width, height, background, target
     cam_arr = L.camera_struct(cams)
     mesh = mesh_struct(pos, col, faces)
     key = (F, B, int(width), int(height), dtype)
+    raster.flags |= _order.flags(key, dtype)
     dev = pos.device
     rgb = torch.empty((B, height, width, 3), dtype=dtype, device=dev)
     alpha = torch.empty((B, height, width), dtype=dtype, device=dev)
@@ -219,6 +263,7 @@ def render_forward_loss(pos, col, faces, cams, width, height, background, target
         L.check(lib.gmr_render_forward_loss(ctypes.byref(mesh), cam_arr, B, ctypes.byref(raster), _ptr(t_rgb),
                                             _ptr(t_m), float(scale_rgb), float(scale_alpha), _ptr(rgb), _ptr(alpha),
                                             _ptr(g_rgb), _ptr(g_a), _ptr(sums), _ptr(ws), nb.value, cap, _stream()))
+        _order.note(key, ws)
         st = ForwardState(ws, cap, raster, cam_arr, B, -1, -1)
         if check is None:
             # status stays on the device (ws[:64]); the caller validates it
@@ -252,6 +297,7 @@ def render_images_u8(pos, col, faces, cams, width, height, background, rescale=T
     cam_arr = L.camera_struct(cams)
     mesh = mesh_struct(pos, col, faces)
     key = (F, B, int(width), int(height), dtype)
+    raster.flags |= _order.flags(key, dtype)
     cap = _capacity.get(key, F * B)
     rgb8 = torch.empty((B, height, width, 3), dtype=torch.uint8, device=pos.device)
     a8 = torch.empty((B, height, width), dtype=torch.uint8, device=pos.device)
@@ -261,6 +307,7 @@ def render_images_u8(pos, col, faces, cams, width, height, background, rescale=T
         ws = torch.empty(nb.value, dtype=torch.uint8, device=pos.device)
         L.check(lib.gmr_render_images_u8(ctypes.byref(mesh), cam_arr, B, ctypes.byref(raster), _ptr(rgb8),
                                          _ptr(a8), _ptr(ws), nb.value, cap, _stream()))
+        _order.note(key, ws)
         st, code = _status_or_raise(ws, "mesh")
         if code == L.GMR_OK:
             _capacity.note(key, cap, st.entries)
@@ -378,6 +425,7 @@ def rasterize_forward(mean2d, cov2d, depth, color, opacity, width, height, backg
     raster = raster_struct(width, height, background, dtype)
     sp = _splat_struct(mean2d, cov2d, depth, color, opacity)
     key = ("splats", K, int(width), int(height), dtype)
+    raster.flags |= _order.flags(key, dtype)
     cap = _capacity.get(key, K)
     rgb = torch.empty((height, width, 3), dtype=dtype, device=mean2d.device)
     alpha = torch.empty((height, width), dtype=dtype, device=mean2d.device)
@@ -387,6 +435,7 @@ def rasterize_forward(mean2d, cov2d, depth, color, opacity, width, height, backg
         ws = torch.empty(nb.value, dtype=torch.uint8, device=mean2d.device)
         L.check(lib.gmr_rasterize_forward(ctypes.byref(sp), ctypes.byref(raster), _ptr(rgb), _ptr(alpha),
                                           _ptr(ws), nb.value, cap, _stream()))
+        _order.note(key, ws)
         st, code = _status_or_raise(ws, "splats")
         if code == L.GMR_OK:
             _capacity.note(key, cap, st.entries)

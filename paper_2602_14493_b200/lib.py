@@ -24,6 +24,7 @@ GMR_F32 = 0
 GMR_F64 = 1
 FLAG_DEBUG_AUX = 1
 FLAG_FULL_TILE_LISTS = 2
+FLAG_TILE_DEPTH_SORT = 4
 STAGES = ("convert_project", "depth_sort", "scan_emit", "tile_sort_ranges", "blend_forward",
           "blend_backward", "face_backward", "vertex_gather")
 

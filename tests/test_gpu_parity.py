@@ -221,3 +221,61 @@ def test_unreachable_tile_culling_is_exact(gmr, dtype):
         lc, lf = ic[bc[t]:bc[t + 1]], iff[bf[t]:bf[t + 1]]
         it = iter(lf)
         assert all(any(x == y for y in it) for x in lc), t   # subsequence
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("name,maker", RENDER_CASES)
+def test_tile_depth_sort_mode_is_identical(gmr, name, maker, dtype):
+    """GMR_FLAG_TILE_DEPTH_SORT (per-tile depth ordering after the tile sort)
+    and the default global depth sort give the same (tile, depth, source)
+    lists, hence bit-identical images and gradients; in f64 both equal the
+    reference's _RasterPlan lists."""
+    from paper_2602_14493_b200 import engine, lib
+    case = maker()
+    mesh = _mesh(case)
+    res = []
+    old = engine.DEFAULT_FLAGS
+    engine.AUTO_TILE_ORDER = False
+    try:
+        for mode in (0, lib.FLAG_TILE_DEPTH_SORT):
+            engine.DEFAULT_FLAGS = lib.FLAG_FULL_TILE_LISTS | mode
+            out, ctx = gmr.render_mesh(mesh, case["camera"], background=case["background"], dtype=dtype,
+                                       return_ctx=True)
+            assert ctx.state.raster.flags & lib.FLAG_TILE_DEPTH_SORT == mode
+            items, bounds = engine.copy_entries(ctx.state, len(mesh.facets), True)
+            gv, gcol = gmr.render_backward(ctx, case["g_rgb"], case["g_alpha"])
+            res.append((items.cpu().numpy(), bounds.cpu().numpy(), out.rgb, out.alpha, gv, gcol))
+    finally:
+        engine.DEFAULT_FLAGS = old
+        engine.AUTO_TILE_ORDER = True
+    for a, b in zip(res[0], res[1]):
+        np.testing.assert_array_equal(a, b)
+    if dtype == np.float64:
+        g = gc.load(name)
+        np.testing.assert_array_equal(res[1][0], g["f64_entry_source"])
+        np.testing.assert_array_equal(res[1][1], g["f64_bounds"])
+
+
+def test_tile_depth_sort_chosen_from_previous_call(gmr):
+    """The engine switches a call shape to per-tile depth ordering once a
+    previous forward of that shape reported only short tile lists, and back
+    to the global depth sort when a list outgrows the shared-memory sort."""
+    import torch
+    from paper_2602_14493_b200 import engine, lib
+    case = gc.c1_case()
+    mesh = _mesh(case)
+    engine._order._last.clear()   # forget earlier tests' calls of this shape
+    engine._order._pending.clear()
+    flags = []
+    for _ in range(3):
+        _, ctx = gmr.render_mesh(mesh, case["camera"], background=case["background"], dtype=np.float32,
+                                 return_ctx=True)
+        torch.cuda.synchronize()
+        flags.append(ctx.state.raster.flags & lib.FLAG_TILE_DEPTH_SORT)
+    assert flags[0] == 0 and flags[-1] == lib.FLAG_TILE_DEPTH_SORT
+    key = next(k for k in engine._order._last if k[0] == len(mesh.facets) and k[-1] == torch.float32)
+    engine._order._pending.clear()
+    engine._order._last[key] = 5000   # as if the last call had a 5000-entry list
+    _, ctx = gmr.render_mesh(mesh, case["camera"], background=case["background"], dtype=np.float32,
+                             return_ctx=True)
+    assert ctx.state.raster.flags & lib.FLAG_TILE_DEPTH_SORT == 0

@@ -165,3 +165,47 @@ def test_one_pixel_wide_images(gmr, W, H):
     gv, gc = gmr.render_backward(ctx, g_rgb, g_a)
     ogv, ogc = orc.render_grad(octx, g_rgb, g_a)
     assert rel(gv, ogv) <= 1e-8 and rel(gc, ogc) <= 1e-8
+
+
+@pytest.mark.parametrize("k", [700, 1500, 3000])
+def test_large_bins_depth_order(gmr, k):
+    """Thousands of splats in one 16x16 tile, depths with many ties: the
+    per-tile depth sort (GMR_FLAG_TILE_DEPTH_SORT) runs in shared memory
+    (k <= 2048 f32 / 1024 f64) or through global scratch (larger bins); the
+    default is the global depth sort.  Both must give the same lists, every
+    bin in (depth, source) order (render.py:227), and the f64
+    render/backward must match the oracle."""
+    from paper_2602_14493_b200 import api, engine
+    from paper_2602_14493_b200.camera import Camera
+    rng = np.random.default_rng(10 + k)
+    W = H = 16
+    case = _splat_scene(rng, k, 3, 13, 1.5, rng.uniform(0.004, 0.012, k), W, H)
+    case["depth"] = 1.0 + rng.integers(0, 40, k) / 10.0
+    cam = Camera(rotation=np.eye(3), translation=np.zeros(3), fx=40, fy=40, cx=W / 2, cy=H / 2, width=W, height=H)
+    sp = [gmr.Splat2D(m, c, float(d), col, float(o), int(i)) for m, c, d, col, o, i in
+          zip(case["mean2d"], case["cov2d"], case["depth"], case["color"], case["opacity"], case["source"])]
+    from paper_2602_14493_b200 import lib
+    modes = []
+    old = engine.DEFAULT_FLAGS
+    engine.AUTO_TILE_ORDER = False
+    try:
+        for dtype in (np.float32, np.float64):
+            for mode in (0, lib.FLAG_TILE_DEPTH_SORT):
+                engine.DEFAULT_FLAGS = mode
+                t, order, _, _, state = api._raster_device(sp, cam, (0.2, 0.1, 0.3), dtype)
+                assert state.raster.flags & lib.FLAG_TILE_DEPTH_SORT == mode
+                items, bounds = engine.copy_entries(state, k, False)
+                modes.append((dtype, order, items.cpu().numpy().astype(np.int64), bounds.cpu().numpy()))
+    finally:
+        engine.DEFAULT_FLAGS = old
+        engine.AUTO_TILE_ORDER = True
+    for (dtype, order, items, bounds), other in zip(modes, modes[1:] + modes[:1]):
+        if other[0] == dtype:
+            np.testing.assert_array_equal(items, other[2])
+        assert bounds[-1] == len(items) and bounds[1] - bounds[0] > 0.9 * k
+        d = np.asarray(case["depth"], dtype)[order][items]
+        for g in range(len(bounds) - 1):
+            dd, ii = d[bounds[g]:bounds[g + 1]], items[bounds[g]:bounds[g + 1]]
+            ok = (dd[1:] > dd[:-1]) | ((dd[1:] == dd[:-1]) & (ii[1:] > ii[:-1]))
+            assert ok.all(), (dtype, g)
+    _check_splats(gmr, case, W, H)
