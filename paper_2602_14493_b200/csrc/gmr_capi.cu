@@ -434,18 +434,13 @@ int render_backward_t(const GmrMesh* m, const GmrCamera* cams, int B, const GmrR
     a.splat = at<Splat<S>>(ws, L.splat);
     a.partial = at<S>(ws, L.partial);
     a.face_acc = at<double>(ws, L.face_acc);
+    // the last group also runs the conversion backward (face_acc stays in registers)
+    a.corner = (v0 + nv == B) ? at<S>(ws, L.corner) : nullptr;
     if (F) {
       StageScope sc(kStFaceBwd, st);
       face_views_backward<S><<<grid_for(F, 128), 128, 0, st>>>(a, make_cams<S>(cams, v0, nv));
       GMR_LAUNCHED();
     }
-  }
-  if (F) {
-    StageScope sc(kStFaceBwd, st);
-    face_convert_backward<S><<<grid_for(F, 128), 128, 0, st>>>((const S*)m->positions, m->faces, (int64_t)F,
-                                                               r->rescale, at<double>(ws, L.face_acc),
-                                                               at<S>(ws, L.corner));
-    GMR_LAUNCHED();
   }
   const uint32_t* vstart = (const uint32_t*)topo;
   const uint32_t* slots = vstart + align_up((V + 1) * 4) / 4;

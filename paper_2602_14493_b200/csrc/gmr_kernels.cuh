@@ -1474,7 +1474,11 @@ template <typename S> struct FaceBwdArgs {
   const Splat<S>* splat;
   const S* partial;
   double* face_acc;   // [F][12]: g_mean3 (3), g_cov3 sym (6), g_col (3), summed over views in float64
+  S* corner;          // non-null on the last view group: write per-corner grads (convert_corners), not face_acc
 };
+
+template <typename S>
+__device__ __forceinline__ void convert_corners(const FaceGeo& g, const double a[12], int rescale, S* out);
 
 template <typename S>
 __global__ void __launch_bounds__(128) face_views_backward(FaceBwdArgs<S> p, const __grid_constant__ CamBatch<S> cams) {
@@ -1575,26 +1579,19 @@ __global__ void __launch_bounds__(128) face_views_backward(FaceBwdArgs<S> p, con
     acc[11] += (double)s[7];
    }
   }
+  if (p.corner) {   // last view group: the conversion backward right here
+    convert_corners<S>(g, acc, p.rescale, p.corner + f * 18);
+  } else {
 #pragma unroll
-  for (int q = 0; q < 12; ++q) p.face_acc[f * 12 + q] = acc[q];
+    for (int q = 0; q < 12; ++q) p.face_acc[f * 12 + q] = acc[q];
+  }
 }
 
-// conversion backward per face (convert.py:393-425) -> per-corner
-// contributions corner[f][c][6] = (g_pos xyz, g_col rgb)
+// conversion backward per face (convert.py:393-425): the face's summed
+// world-space grads a[12] = (g_mean3 (3), g_cov3 sym (6), g_col (3)) ->
+// per-corner contributions out[c][6] = (g_pos xyz, g_col rgb)
 template <typename S>
-__global__ void __launch_bounds__(128) face_convert_backward(const S* __restrict__ pos,
-                                                             const int32_t* __restrict__ faces,
-                                                             int64_t F, int rescale,
-                                                             const double* __restrict__ face_acc,
-                                                             S* __restrict__ corner) {
-  const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (f >= F) return;
-  FaceGeo g;
-  int32_t idx[3];
-  load_face(pos, faces, f, rescale, g, idx);
-  double a[12];
-#pragma unroll
-  for (int q = 0; q < 12; ++q) a[q] = face_acc[f * 12 + q];
+__device__ __forceinline__ void convert_corners(const FaceGeo& g, const double a[12], int rescale, S* out) {
   // G symmetric (xx,xy,xz,yy,yz,zz); gsym = 2G
   const double G[3][3] = {{a[3], a[4], a[5]}, {a[4], a[6], a[7]}, {a[5], a[7], a[8]}};
   double ge[3][3];   // g_e1, g_e2, g_e3 (float64 like convert.py:393-425)
@@ -1640,7 +1637,6 @@ __global__ void __launch_bounds__(128) face_convert_backward(const S* __restrict
 #pragma unroll
       for (int r = 0; r < 3; ++r) ge[i][r] = 0.0;
   }
-  S* out = corner + f * 18;
 #pragma unroll
   for (int r = 0; r < 3; ++r) {
     const double third = a[r] / 3.0;
@@ -1652,6 +1648,23 @@ __global__ void __launch_bounds__(128) face_convert_backward(const S* __restrict
     out[9 + r] = gc;
     out[15 + r] = gc;
   }
+}
+
+template <typename S>
+__global__ void __launch_bounds__(128) face_convert_backward(const S* __restrict__ pos,
+                                                             const int32_t* __restrict__ faces,
+                                                             int64_t F, int rescale,
+                                                             const double* __restrict__ face_acc,
+                                                             S* __restrict__ corner) {
+  const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= F) return;
+  FaceGeo g;
+  int32_t idx[3];
+  load_face(pos, faces, f, rescale, g, idx);
+  double a[12];
+#pragma unroll
+  for (int q = 0; q < 12; ++q) a[q] = face_acc[f * 12 + q];
+  convert_corners<S>(g, a, rescale, corner + f * 18);
 }
 
 // K6: per vertex, sum its (face, corner) contributions in the reference's
