@@ -1481,7 +1481,10 @@ template <typename S>
 __device__ __forceinline__ void convert_corners(const FaceGeo& g, const double a[12], int rescale, S* out);
 
 template <typename S>
-__global__ void __launch_bounds__(128) face_views_backward(FaceBwdArgs<S> p, const __grid_constant__ CamBatch<S> cams) {
+#ifndef GMR_K5_MINB
+#define GMR_K5_MINB 6   // 80 registers: more faces in flight (latency-bound gathers)
+#endif
+__global__ void __launch_bounds__(128, GMR_K5_MINB) face_views_backward(FaceBwdArgs<S> p, const __grid_constant__ CamBatch<S> cams) {
   const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= p.F) return;
   FaceGeo g;
