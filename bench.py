@@ -123,20 +123,25 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(inside)}
 
 
-def stage_bytes(F, V, B, W, H, E, bins):
+def stage_bytes(F, V, B, W, H, E, bins, tile_depth_sort=True):
     """Algorithmic bytes per launch of each stage (fp32 values, int32 indices;
-    each array crossing the kernel boundary once)."""
+    each array crossing the kernel boundary once).
+    tile_depth_sort: the forward ordered each tile list by depth after the
+    tile sort (GMR_FLAG_TILE_DEPTH_SORT) instead of sorting all items first."""
     n = F * B
     px = W * H * B
     entry_passes = max(1, (max(1, (bins - 1).bit_length()) + 7) // 8)
+    groups = (B + 63) // 64   # view groups of face_views_backward (face_acc round trips between them)
     return {
         "convert_project": 12 * F + 24 * V + 16 * F + 52 * n,
-        "depth_sort": 4 * 20 * n,
-        "scan_emit": 36 * n + 8 * E,
+        # per-tile: entry items read + depth keys gathered + items written;
+        # global: 4 passes over (key, item) pairs of all items
+        "depth_sort": 12 * E if tile_depth_sort else 4 * 20 * n,
+        "scan_emit": (32 if tile_depth_sort else 36) * n + 8 * E,
         "tile_sort_ranges": 20 * entry_passes * E + 4 * E + 4 * bins,
         "blend_forward": 8 * bins + 52 * E + 20 * px,
         "blend_backward": 8 * bins + 96 * E + 32 * px,
-        "face_backward": 24 * F + 24 * V + 40 * n + 32 * E + 48 * F + 48 * F + 72 * F,
+        "face_backward": 24 * F + 24 * V + 40 * n + 32 * E + 96 * F * (groups - 1) + 72 * F,
         "vertex_gather": 4 * V + 12 * F + 72 * F + 24 * V,
     }
 
@@ -320,7 +325,7 @@ def run_gmr(args, cfg):
     # ---- roofline of the dominant stage ------------------------------------
     peak, peak_src = load_peaks()
     names = lib.STAGES
-    sb = stage_bytes(F, V, B, W, H, E, bins)
+    sb = stage_bytes(F, V, B, W, H, E, bins, bool(state['st'].raster.flags & lib.FLAG_TILE_DEPTH_SORT))
     stages = {}
     for i, nm in enumerate(names):
         if scnt[i]:
@@ -374,6 +379,8 @@ def run_gmr(args, cfg):
         "config": {"workload": cfg["desc"] + f", {B} views per GPU per step (hemisphere cameras r=3)",
                    "faces": F, "vertices": V, "views_per_gpu": B, "resolution": [W, H],
                    "tile_entries_per_step": E, "l2": "inputs+workspace per step > 126 MB L2 (no flush needed)",
+                   "depth_order": ("per-tile lists (GMR_FLAG_TILE_DEPTH_SORT)"
+                                   if state["st"].raster.flags & lib.FLAG_TILE_DEPTH_SORT else "global item sort"),
                    "parallelism": f"views sharded over {world} GPU(s), NCCL all-reduce of vertex grads"},
         "e2e": {"value": round(B * world * k_e2e / (ms_e2e / 1e3), 2), "unit": "views/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,

@@ -77,36 +77,53 @@ _capacity = _Capacity()
 
 class _TileOrder:
     """Chooses GMR_FLAG_TILE_DEPTH_SORT per call shape from the longest tile
-    list of the previous forward of that shape (device status byte 60,
-    copied behind the call without a sync).  Per-tile depth ordering when
-    every list fits the kernel's shared-memory sort; the global depth sort
-    otherwise, and for the first call of a shape.  Both give the same lists."""
+    list of an earlier forward of that shape (device status byte 60, copied
+    behind the call without a sync; re-read every REFRESH calls).  Per-tile
+    depth ordering when every list fits the kernel's shared-memory sort; the
+    global depth sort otherwise, and for the first call of a shape.  Both give
+    the same lists."""
 
     LIMIT = {torch.float32: 2048, torch.float64: 1024}
+    REFRESH = 64
+
+    class _Shape:
+        __slots__ = ("last", "host", "event", "pending", "calls")
+
+        def __init__(self):
+            self.last, self.host, self.event, self.pending, self.calls = None, None, None, False, 0
 
     def __init__(self):
-        self._last = {}
-        self._pending = {}
+        self._shapes = {}
 
     def flags(self, key, dtype):
         if not AUTO_TILE_ORDER:
             return 0
-        p = self._pending.get(key)
+        sh = self._shapes.get(key)
+        if sh is None:
+            return 0
         # (no event queries while a graph is being captured)
-        if p is not None and not torch.cuda.is_current_stream_capturing() and p[1].query():
-            self._last[key] = int(p[0].view(torch.int32)[0])
-            del self._pending[key]
-        last = self._last.get(key)
-        return L.FLAG_TILE_DEPTH_SORT if last is not None and last <= self.LIMIT[dtype] else 0
+        if sh.pending and not torch.cuda.is_current_stream_capturing() and sh.event.query():
+            sh.last = int(sh.host.view(torch.int32)[0])
+            sh.pending = False
+        return L.FLAG_TILE_DEPTH_SORT if sh.last is not None and sh.last <= self.LIMIT[dtype] else 0
 
     def note(self, key, ws):
-        if key in self._pending or torch.cuda.is_current_stream_capturing():
+        if not AUTO_TILE_ORDER or torch.cuda.is_current_stream_capturing():
             return
-        h = torch.empty(4, dtype=torch.uint8, pin_memory=True)
-        h.copy_(ws[60:64], non_blocking=True)
-        ev = torch.cuda.Event()
-        ev.record()
-        self._pending[key] = (h, ev)
+        sh = self._shapes.get(key)
+        if sh is None:
+            sh = self._shapes[key] = self._Shape()
+            sh.host = torch.empty(4, dtype=torch.uint8, pin_memory=True)
+            sh.event = torch.cuda.Event()
+        sh.calls += 1
+        if sh.pending or (sh.last is not None and sh.calls % self.REFRESH):
+            return
+        sh.host.copy_(ws[60:64], non_blocking=True)
+        sh.event.record()
+        sh.pending = True
+
+    def forget(self):
+        self._shapes.clear()
 
 
 _order = _TileOrder()

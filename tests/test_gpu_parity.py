@@ -264,8 +264,7 @@ def test_tile_depth_sort_chosen_from_previous_call(gmr):
     from paper_2602_14493_b200 import engine, lib
     case = gc.c1_case()
     mesh = _mesh(case)
-    engine._order._last.clear()   # forget earlier tests' calls of this shape
-    engine._order._pending.clear()
+    engine._order.forget()   # earlier tests' calls of this shape
     flags = []
     for _ in range(3):
         _, ctx = gmr.render_mesh(mesh, case["camera"], background=case["background"], dtype=np.float32,
@@ -273,9 +272,9 @@ def test_tile_depth_sort_chosen_from_previous_call(gmr):
         torch.cuda.synchronize()
         flags.append(ctx.state.raster.flags & lib.FLAG_TILE_DEPTH_SORT)
     assert flags[0] == 0 and flags[-1] == lib.FLAG_TILE_DEPTH_SORT
-    key = next(k for k in engine._order._last if k[0] == len(mesh.facets) and k[-1] == torch.float32)
-    engine._order._pending.clear()
-    engine._order._last[key] = 5000   # as if the last call had a 5000-entry list
+    key = next(k for k in engine._order._shapes if k[0] == len(mesh.facets) and k[-1] == torch.float32)
+    sh = engine._order._shapes[key]
+    sh.pending, sh.last = False, 5000   # as if the last read-back had seen a 5000-entry list
     _, ctx = gmr.render_mesh(mesh, case["camera"], background=case["background"], dtype=np.float32,
                              return_ctx=True)
     assert ctx.state.raster.flags & lib.FLAG_TILE_DEPTH_SORT == 0
