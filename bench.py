@@ -337,15 +337,16 @@ def run_gmr(args, cfg):
     achieved = sb[dom] / (dper / 1e3) / 1e9
     step_bytes = survey_bytes_per_view(F, V, E / B, (W // 16) * (H // 16), W, H) * B
     step_gbs = step_bytes / (ms / args.steps / 1e3) / 1e9
-    traffic, warp_inst = None, None
+    traffic, warp_inst, smem_wf = None, None, None
     tf = os.path.join(ROOT, "profiles", "traffic_r01.json")
     if os.path.exists(tf):
         try:
             tj = json.load(open(tf))
             traffic = tj.get(dom)
             warp_inst = (tj.get("warp_instructions") or {}).get(dom)
+            smem_wf = (tj.get("smem_wavefronts") or {}).get(dom)
         except Exception:
-            traffic, warp_inst = None, None
+            traffic, warp_inst, smem_wf = None, None, None
     # the binding roofline of the blend kernels: instruction issue (148 SMs x
     # 4 warp-instructions / clock); warp instructions per launch from the ncu
     # capture in profiles/, time from the live stage timer
@@ -357,6 +358,16 @@ def run_gmr(args, cfg):
         issue = {"bound": "issue", "kernel": dom, "achieved": round(ach / 1e12, 4), "peak": round(peak_issue / 1e12, 4),
                  "unit": "T warp-instr/s", "frac": round(ach / peak_issue, 4),
                  "warp_instructions_per_launch": int(warp_inst), "source": "ncu smsp__inst_executed.sum (profiles/)"}
+    # ... and its shared-memory pipe: one 128-byte wavefront per clock per SM
+    smem = None
+    if smem_wf:
+        mhz = (clocks or {}).get("sm_mhz") or (clocks or {}).get("sm_max_mhz") or 1965.0
+        peak_wf = 148 * float(mhz) * 1e6
+        ach = smem_wf / (dper / 1e3)
+        smem = {"bound": "shared-memory pipe", "kernel": dom, "achieved": round(ach / 1e12, 4),
+                "peak": round(peak_wf / 1e12, 4), "unit": "T wavefronts/s", "frac": round(ach / peak_wf, 4),
+                "wavefronts_per_launch": int(smem_wf),
+                "source": "ncu l1tex__data_pipe_lsu_wavefronts_mem_shared.sum (profiles/)"}
 
     # ---- CPU baseline (rank 0, N = 1, bounded sample) -----------------------
     cpu = None
@@ -390,6 +401,7 @@ def run_gmr(args, cfg):
                      "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                      "peak_source": peak_src},
         "issue_roofline": issue,
+        "smem_roofline": smem,
         "step_roofline": {"bytes_per_step": int(step_bytes), "achieved_GBs": round(step_gbs, 1),
                           "frac": round(step_gbs / peak, 4),
                           "model": "SURVEY 8d: 160F+60V+116E+24T+48WH per view"},
