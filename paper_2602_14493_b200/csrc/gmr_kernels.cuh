@@ -650,7 +650,7 @@ template <typename K> struct BinSortSmem {
 
 // One stable pass on the 8-bit digit of (key - kmin) at `shift`: src -> dst
 // (shared or global).  Chunks of up to kCap elements in order; in a chunk
-// warp w ranks a contiguous segment (match_any groups; the group leader
+// warp w ranks a contiguous segment (ballot-built digit groups; the group leader
 // owns the warp's running digit count), so the output keeps the input order
 // within each digit.
 template <typename K>
@@ -684,8 +684,8 @@ __device__ __forceinline__ void bin_digit_pass(const K* sk, const uint32_t* sv, 
       if (32u * j < seg) {   // warp-uniform
         const uint32_t i = w0 + 32 * j + lane;
         const bool valid = i < c0 + m;
-        const uint32_t d = valid ? (uint32_t)((sk[i] - kmin) >> shift) & 255u : 0xffffffffu;
-        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        const uint32_t d = valid ? (uint32_t)((sk[i] - kmin) >> shift) & 255u : 256u;
+        const unsigned peers = digit_peers_ballot(d);
         const int leader = __ffs(peers) - 1;
         uint32_t old = 0;
         if (valid && lane == leader) {

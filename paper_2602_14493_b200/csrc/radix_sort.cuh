@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+
 namespace gmr {
 
 constexpr int kSortThreads = 256;
@@ -25,6 +26,21 @@ constexpr int kSortWarps = kSortThreads / 32;
 __device__ __forceinline__ unsigned lanemask_lt_sort() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Lanes holding the same digit d (< 512) by nine ballots: they pipeline,
+// where __match_any_sync is one long-latency instruction.  Faster in the
+// barrier-bound per-list sort (bin_depth_sort), slower in the radix
+// downsweep, which is closer to issue-bound and keeps match_any.
+__device__ __forceinline__ unsigned digit_peers_ballot(uint32_t d) {
+  unsigned m = 0xffffffffu;
+#pragma unroll
+  for (int b = 0; b < 9; ++b) {
+    const bool bit = (d >> b) & 1u;
+    const unsigned bal = __ballot_sync(0xffffffffu, bit);
+    m &= bit ? bal : ~bal;
+  }
   return m;
 }
 
