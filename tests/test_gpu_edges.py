@@ -134,3 +134,47 @@ def test_backward_shape_errors_match_reference(gmr):
         gmr.convert_backward(mesh, cloud, np.zeros((7, 3)), np.zeros((8, 3, 3)), np.zeros((8, 3)))
     with pytest.raises(ValueError, match="unknown conversion path"):
         gmr.convert_mesh(mesh, path="bogus")
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_distant_mesh_long_tile_lists(gmr, dtype):
+    """A 5,120-face sphere far from the camera: every facet lands in the same
+    few tiles, so each list holds thousands of entries (beyond the per-tile
+    sort's shared memory).  The engine uses the global depth sort for the
+    first call and keeps it (the read-back list length is too long); forcing
+    the per-tile sort (global-scratch path) must give the same lists, and the
+    render must match the oracle."""
+    import torch
+    from paper_2602_14493_b200 import engine, lib
+    m = gmr.make_icosphere(5120)
+    mesh = gmr.TriangleMesh(m.vertices, m.facets, gmr.seeded_colors(m.num_vertices, 3))
+    cam = gmr.look_at((0.0, -9.0, 2.0), (0, 0, 0), **gmr.default_intrinsics(40, 40))
+    rng = np.random.default_rng(4)
+    g_rgb, g_a = rng.normal(size=(40, 40, 3)), rng.normal(size=(40, 40))
+    res = []
+    old = engine.DEFAULT_FLAGS
+    engine.AUTO_TILE_ORDER = False
+    try:
+        for mode in (0, lib.FLAG_TILE_DEPTH_SORT):
+            engine.DEFAULT_FLAGS = mode
+            out, ctx = gmr.render_mesh(mesh, cam, background=(0.1, 0.1, 0.1), dtype=dtype, return_ctx=True)
+            items, bounds = engine.copy_entries(ctx.state, len(mesh.facets), True)
+            gv, gc_ = gmr.render_backward(ctx, g_rgb, g_a)
+            res.append((items.cpu().numpy(), bounds.cpu().numpy(), out.rgb, gv, gc_))
+    finally:
+        engine.DEFAULT_FLAGS = old
+        engine.AUTO_TILE_ORDER = True
+    assert np.diff(res[0][1]).max() > 2048   # the long-list path really ran
+    for a, b in zip(res[0], res[1]):
+        np.testing.assert_array_equal(a, b)
+    r, _, octx = orc.render(mesh.vertices, mesh.facets, mesh.colors, cam, (0.1, 0.1, 0.1), True, dtype)
+    ogv = orc.render_grad(octx, g_rgb, g_a)[0]
+    itol, gtol = (1e-10, 1e-8) if dtype == np.float64 else (2e-4, 2e-3)
+    assert np.abs(res[0][2] - r).max() <= itol
+    assert rel(res[0][3], ogv) <= gtol
+    # the automatic choice: a list this long keeps the global sort
+    engine._order.forget()
+    for _ in range(3):
+        _, ctx = gmr.render_mesh(mesh, cam, background=(0.1, 0.1, 0.1), dtype=dtype, return_ctx=True)
+        torch.cuda.synchronize()
+    assert ctx.state.raster.flags & lib.FLAG_TILE_DEPTH_SORT == 0
