@@ -354,7 +354,7 @@ int render_forward_t(const GmrMesh* m, const GmrCamera* cams, int B, const GmrRa
     a.bin = at<uint4>(ws, L.bin);
     a.count = at<uint32_t>(ws, L.count);
     a.dkey = at<typename KeyOf<S>::type>(ws, L.dkey[0]);
-    a.ditem = at<uint32_t>(ws, L.ditem[0]);
+    a.ditem = (r->flags & GMR_FLAG_TILE_DEPTH_SORT) ? nullptr : at<uint32_t>(ws, L.ditem[0]);
     a.cull = (r->flags & GMR_FLAG_FULL_TILE_LISTS) ? 0 : 1;
     a.aux = (r->flags & GMR_FLAG_DEBUG_AUX) ? at<S>(ws, L.aux) : nullptr;
     a.st = at<DevStatus>(ws, L.status);
@@ -482,7 +482,7 @@ int rasterize_forward_t(const GmrSplats* sp, const GmrRaster* r, void* rgb, void
   a.bin = at<uint4>(ws, L.bin);
   a.count = at<uint32_t>(ws, L.count);
   a.dkey = at<typename KeyOf<S>::type>(ws, L.dkey[0]);
-  a.ditem = at<uint32_t>(ws, L.ditem[0]);
+  a.ditem = (r->flags & GMR_FLAG_TILE_DEPTH_SORT) ? nullptr : at<uint32_t>(ws, L.ditem[0]);
   a.cull = (r->flags & GMR_FLAG_FULL_TILE_LISTS) ? 0 : 1;
   a.st = at<DevStatus>(ws, L.status);
   if (sp->count) {

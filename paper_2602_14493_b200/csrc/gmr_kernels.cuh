@@ -256,7 +256,7 @@ template <typename S> struct MeshFwdArgs {
   uint4* bin;        // [items]: (rect lo, rect hi, emitted-tile mask, entry count) -- one sector per gather
   uint32_t* count;   // [items]: entry count again, for the sequential readers
   typename KeyOf<S>::type* dkey;
-  uint32_t* ditem;   // item ids for the global depth sort
+  uint32_t* ditem;   // item ids for the global depth sort (null: per-tile depth order)
   int cull;          // drop tiles the splat cannot reach (not GMR_FLAG_FULL_TILE_LISTS)
   S* aux;   // optional [items][2] = (radius, depth)
   DevStatus* st;
@@ -342,7 +342,7 @@ __global__ void __launch_bounds__(256) mesh_to_splats(MeshFwdArgs<S> p, const __
       p.bin[item] = make_uint4(rc.x, rc.y, emask, cnt);
       p.count[item] = cnt;
       p.dkey[item] = key;
-      p.ditem[item] = (uint32_t)item;
+      if (p.ditem) p.ditem[item] = (uint32_t)item;
     }
   }
   // warp-aggregated kept count
@@ -366,7 +366,7 @@ template <typename S> struct PackArgs {
   uint4* bin;
   uint32_t* count;
   typename KeyOf<S>::type* dkey;
-  uint32_t* ditem;   // item ids for the global depth sort
+  uint32_t* ditem;   // item ids for the global depth sort (null: per-tile depth order)
   int cull;
   DevStatus* st;
 };
@@ -405,7 +405,7 @@ __global__ void __launch_bounds__(256) pack_splats(PackArgs<S> p) {
                         emask, cnt);
   p.count[i] = cnt;
   p.dkey[i] = order_key(d);
-  p.ditem[i] = item;
+  if (p.ditem) p.ditem[i] = item;
   if (has_rect) atomicAdd(&p.st->kept, 1ull);
 }
 
