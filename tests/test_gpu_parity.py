@@ -88,18 +88,26 @@ def test_render_f32_matches_reference(gmr, name, maker):
         assert rl2 <= 1e-2
 
 
+@pytest.mark.parametrize("tile_mode", [False, True])
 @pytest.mark.parametrize("name,maker", RENDER_CASES)
-def test_binning_bit_exact_f32(gmr, name, maker):
+def test_binning_bit_exact_f32(gmr, name, maker, tile_mode):
     """Feed the kernel's own fp32 (mean2d, radius, depth) of kept splats to the
-    oracle's _RasterPlan restatement: entries and bounds must be identical."""
+    oracle's _RasterPlan restatement: entries and bounds must be identical
+    (global and per-tile depth order)."""
     from paper_2602_14493_b200 import engine
     case = maker()
     mesh = _mesh(case)
     pos, col, faces = gmr.api._device_mesh(mesh, np.float32)
     cam = case["camera"]
     from paper_2602_14493_b200 import lib
-    rgb, alpha, st = engine.render_forward(pos, col, faces, [cam], cam.width, cam.height,
-                                           case["background"], flags=lib.FLAG_DEBUG_AUX | lib.FLAG_FULL_TILE_LISTS)
+    flags = lib.FLAG_DEBUG_AUX | lib.FLAG_FULL_TILE_LISTS | (lib.FLAG_TILE_DEPTH_SORT if tile_mode else 0)
+    engine.AUTO_TILE_ORDER = False
+    try:
+        rgb, alpha, st = engine.render_forward(pos, col, faces, [cam], cam.width, cam.height,
+                                               case["background"], flags=flags)
+    finally:
+        engine.AUTO_TILE_ORDER = True
+    assert bool(st.raster.flags & lib.FLAG_TILE_DEPTH_SORT) == tile_mode
     rec, rect, cnt, aux = (x.cpu().numpy() for x in engine.copy_splats(st, len(mesh.facets), True))
     kept = np.where(cnt > 0)[0]
     mean2d = rec[kept, 0:2]
