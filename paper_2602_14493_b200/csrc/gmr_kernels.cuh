@@ -1436,16 +1436,30 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : 5) blend_b
 // projection backward per view -> accumulate over views -> conversion backward
 // ---------------------------------------------------------------------------
 
+#ifndef GMR_K5_AHEAD
+#define GMR_K5_AHEAD 4
+#endif
 template <typename S>
 __device__ __forceinline__ void sum_entries(const S* __restrict__ partial, uint32_t off, uint32_t cnt,
                                             S acc[8]) {
 #pragma unroll
   for (int q = 0; q < 8; ++q) acc[q] = S(0);
   const V4<S>* src = reinterpret_cast<const V4<S>*>(partial + (size_t)off * 8);
-  for (uint32_t e = 0; e < cnt; ++e) {
-    const V4<S> lo = src[2 * e], hi = src[2 * e + 1];
-    acc[0] += lo.x; acc[1] += lo.y; acc[2] += lo.z; acc[3] += lo.w;
-    acc[4] += hi.x; acc[5] += hi.y; acc[6] += hi.z; acc[7] += hi.w;
+  // loads of up to GMR_K5_AHEAD entries in flight, summed in entry (tile) order
+  for (uint32_t e0 = 0; e0 < cnt; e0 += GMR_K5_AHEAD) {
+    V4<S> lo[GMR_K5_AHEAD], hi[GMR_K5_AHEAD];
+#pragma unroll
+    for (int k = 0; k < GMR_K5_AHEAD; ++k)
+      if (e0 + k < cnt) {
+        lo[k] = src[2 * (e0 + k)];
+        hi[k] = src[2 * (e0 + k) + 1];
+      }
+#pragma unroll
+    for (int k = 0; k < GMR_K5_AHEAD; ++k)
+      if (e0 + k < cnt) {
+        acc[0] += lo[k].x; acc[1] += lo[k].y; acc[2] += lo[k].z; acc[3] += lo[k].w;
+        acc[4] += hi[k].x; acc[5] += hi[k].y; acc[6] += hi[k].z; acc[7] += hi[k].w;
+      }
   }
 }
 
@@ -1482,7 +1496,7 @@ __device__ __forceinline__ void convert_corners(const FaceGeo& g, const double a
 
 template <typename S>
 #ifndef GMR_K5_MINB
-#define GMR_K5_MINB 6   // 80 registers: more faces in flight (latency-bound gathers)
+#define GMR_K5_MINB 4   // 128 registers: four partial runs in flight per face (latency-bound gathers)
 #endif
 __global__ void __launch_bounds__(128, GMR_K5_MINB) face_views_backward(FaceBwdArgs<S> p, const __grid_constant__ CamBatch<S> cams) {
   const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
