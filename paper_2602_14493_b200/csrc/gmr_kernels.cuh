@@ -432,10 +432,17 @@ __global__ void __launch_bounds__(256) scan_reduce(const uint32_t* __restrict__ 
 constexpr int kTopThreads = 1024;
 __device__ __forceinline__ unsigned long long scan_runs_inplace(uint32_t* __restrict__ a, int n) {
   __shared__ unsigned long long wsum[kTopThreads / 32];
-  const int per = (n + kTopThreads - 1) / kTopThreads;
+  // runs of a multiple of 4 elements: 16-byte loads and stores (a is
+  // 16-byte aligned: workspace buffers are 256-byte aligned)
+  const int per = (((n + kTopThreads - 1) / kTopThreads) + 3) & ~3;
   const int lo = min(n, (int)threadIdx.x * per), hi = min(n, lo + per);
   unsigned long long s = 0;
-  for (int i = lo; i < hi; ++i) s += a[i];
+  int i = lo;
+  for (; i + 4 <= hi; i += 4) {
+    const uint4 v = *reinterpret_cast<const uint4*>(a + i);
+    s += (unsigned long long)v.x + v.y + v.z + v.w;
+  }
+  for (; i < hi; ++i) s += a[i];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   unsigned long long x = s;
 #pragma unroll
@@ -452,7 +459,17 @@ __device__ __forceinline__ unsigned long long scan_runs_inplace(uint32_t* __rest
     tot += t;
   }
   unsigned long long run = wp + x - s;
-  for (int i = lo; i < hi; ++i) {
+  i = lo;
+  for (; i + 4 <= hi; i += 4) {
+    const uint4 v = *reinterpret_cast<const uint4*>(a + i);
+    uint4 o;
+    o.x = (uint32_t)run; run += v.x;
+    o.y = (uint32_t)run; run += v.y;
+    o.z = (uint32_t)run; run += v.z;
+    o.w = (uint32_t)run; run += v.w;
+    *reinterpret_cast<uint4*>(a + i) = o;
+  }
+  for (; i < hi; ++i) {
     const uint32_t v = a[i];
     a[i] = (uint32_t)run;
     run += v;
