@@ -1712,15 +1712,29 @@ __global__ void __launch_bounds__(256) vertex_gather(const uint32_t* __restrict_
   if (v >= V) return;
   S gp[3] = {0, 0, 0}, gc[3] = {0, 0, 0};
   const uint32_t b = vstart[v], e = vstart[v + 1];
-  for (uint32_t k = b; k < e; ++k) {
-    const uint32_t s = slots[k];
-    const uint32_t c = (uint32_t)(s / (uint64_t)F);
-    const uint64_t f = s - (uint64_t)c * F;
-    const S* src = corner + f * 18 + c * 6;
+  const uint64_t F2 = 2 * (uint64_t)F;
+  // four contributions in flight, summed in slot (np.add.at) order
+  for (uint32_t k0 = b; k0 < e; k0 += 4) {
+    S val[4][6];
 #pragma unroll
-    for (int r = 0; r < 3; ++r) {
-      gp[r] += src[r];
-      gc[r] += src[3 + r];
+    for (int q = 0; q < 4; ++q) {
+      if (k0 + q < e) {
+        const uint64_t sl = slots[k0 + q];   // corner * F + face
+        const uint64_t c = sl >= F2 ? 2 : (sl >= (uint64_t)F ? 1 : 0);
+        const S* src = corner + (sl - c * (uint64_t)F) * 18 + c * 6;
+#pragma unroll
+        for (int r = 0; r < 6; ++r) val[q][r] = src[r];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (k0 + q < e) {
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          gp[r] += val[q][r];
+          gc[r] += val[q][3 + r];
+        }
+      }
     }
   }
 #pragma unroll
