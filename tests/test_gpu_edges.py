@@ -215,3 +215,37 @@ def test_random_scenes_tile_lists_and_images(gmr, seed):
     finally:
         engine.DEFAULT_FLAGS = old
         engine.AUTO_TILE_ORDER = True
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_scenes_f32_and_backward_vs_oracle(gmr, seed):
+    """Randomised scenes through the full fwd+bwd in both dtypes: f64 within
+    1e-10 / 1e-8 of the oracle; f32 against the oracle's own f32 path with the
+    flip-aware tolerances of test_gpu_parity (image 1e-4 except on at most
+    0.1 % of pixels, gradients 1e-3 relative when nothing flipped)."""
+    rng = np.random.default_rng(300 + seed)
+    n = int(rng.choice([4, 6, 9]))
+    mesh = gmr.make_geodesic_sphere(n, seed=seed)
+    W, H = int(rng.integers(16, 64)), int(rng.integers(16, 64))
+    d = float(rng.choice([1.6, 2.5, 4.0]))
+    u = rng.normal(size=3)
+    cam = gmr.look_at(tuple(d * u / np.linalg.norm(u)), (0, 0, 0), **gmr.default_intrinsics(W, H))
+    bg = tuple(rng.uniform(0, 1, 3))
+    g_rgb, g_a = rng.normal(size=(H, W, 3)), rng.normal(size=(H, W))
+    for dtype in (np.float64, np.float32):
+        r, a, octx = orc.render(mesh.vertices, mesh.facets, mesh.colors, cam, bg, True, dtype)
+        ogv, ogc = orc.render_grad(octx, g_rgb, g_a)
+        out, ctx = gmr.render_mesh(mesh, cam, background=bg, dtype=dtype, return_ctx=True)
+        gv, gcol = gmr.render_backward(ctx, g_rgb, g_a)
+        if dtype == np.float64:
+            assert np.abs(out.rgb - r).max() <= 1e-10 and np.abs(out.alpha - a).max() <= 1e-10
+            assert rel(gv, ogv) <= 1e-8 and rel(gcol, ogc) <= 1e-8
+        else:
+            dd = np.abs(out.rgb.astype(np.float64) - r).max(axis=2)
+            da = np.abs(out.alpha.astype(np.float64) - a)
+            bad = (dd > 1e-4) | (da > 1e-4)
+            assert bad.sum() <= max(2, 1e-3 * bad.size), (bad.sum(), dd.max())
+            if bad.sum() == 0:
+                assert rel(gv, ogv) <= 1e-3 and rel(gcol, ogc) <= 1e-3
+            else:
+                assert np.linalg.norm(gv - ogv) / np.linalg.norm(ogv) <= 1e-2
