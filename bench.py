@@ -42,6 +42,9 @@ CONFIGS = {
                  desc="config3 batch 1: geodesic displaced sphere n=158 (499,280 faces), 800x800"),
     "c4": dict(mesh=("geodesic", 316), res=1024, views=8,
                desc="config4: geodesic displaced sphere n=316 (1,997,120 faces), 1024x1024"),
+    # BASELINE configs[3] as stated: 64 views in total, sharded over the ranks
+    "c4s": dict(mesh=("geodesic", 316), res=1024, views=64, total_views=True, chunk=16,
+                desc="config4: geodesic displaced sphere n=316 (1,997,120 faces), 1024x1024, 64 views in total"),
     "views": dict(mesh=("geodesic", 158), res=256, views=253,
                   desc="SURVEY 8f row 3: make_views of the config-3 mesh (499,280 faces), 253 hemisphere views "
                        "256x256, float64 like the reference, 8-bit images to host"),
@@ -123,26 +126,45 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(inside)}
 
 
-def stage_bytes(F, V, B, W, H, E, bins, tile_depth_sort=True):
-    """Algorithmic bytes per launch of each stage (fp32 values, int32 indices;
-    each array crossing the kernel boundary once).
-    tile_depth_sort: the forward ordered each tile list by depth after the
-    tile sort (GMR_FLAG_TILE_DEPTH_SORT) instead of sorting all items first."""
+# Stage groups of the library's CUDA-event timers (lib.STAGES) that SURVEY
+# §8(d)'s per-kernel byte model prices as one kernel.
+STAGE_GROUPS = {
+    "convert_project": ("convert_project",),                          # K1
+    "binning": ("depth_sort", "scan_emit", "tile_sort_ranges"),       # K2
+    "blend_forward": ("blend_forward",),                              # K3
+    "blend_backward": ("blend_backward",),                            # K4
+    "face_vertex_backward": ("face_backward", "vertex_gather"),       # K5 + K6
+}
+
+
+def section8d_bytes(F, V, B, W, H, E, T):
+    """SURVEY §8(d) compulsory bytes per launch of each stage group (fp32
+    values, int32 indices, each logical array crossing a kernel boundary
+    once): per view K1 60F+24V, K2 24F+44E+8T, K3 8T+36E+24WH,
+    K4 24WH+8T+36E+32F, K5/K6 44F+36V.  E is summed over the B views."""
+    WH = W * H
+    return {
+        "convert_project": B * (60 * F + 24 * V),
+        "binning": B * (24 * F + 8 * T) + 44 * E,
+        "blend_forward": B * (8 * T + 24 * WH) + 36 * E,
+        "blend_backward": B * (24 * WH + 8 * T + 32 * F) + 36 * E,
+        "face_vertex_backward": B * (44 * F + 36 * V),
+    }
+
+
+def implementation_bytes(F, V, B, W, H, E, bins, tile_depth_sort=True):
+    """What the implementation moves per launch (diagnostic beside the
+    §8(d) model: coverage masks, entry partials, double-buffered sorts)."""
     n = F * B
     px = W * H * B
     entry_passes = max(1, (max(1, (bins - 1).bit_length()) + 7) // 8)
-    groups = (B + 63) // 64   # view groups of face_views_backward (face_acc round trips between them)
     return {
         "convert_project": 12 * F + 24 * V + 16 * F + 52 * n,
-        # per-tile: entry items read + depth keys gathered + items written;
-        # global: 4 passes over (key, item) pairs of all items
-        "depth_sort": 12 * E if tile_depth_sort else 4 * 20 * n,
-        "scan_emit": (32 if tile_depth_sort else 36) * n + 8 * E,
-        "tile_sort_ranges": 20 * entry_passes * E + 4 * E + 4 * bins,
+        "binning": (12 * E if tile_depth_sort else 80 * n) + (32 if tile_depth_sort else 36) * n + 8 * E
+        + 20 * entry_passes * E + 4 * E + 4 * bins,
         "blend_forward": 8 * bins + 52 * E + 20 * px,
         "blend_backward": 8 * bins + 96 * E + 32 * px,
-        "face_backward": 24 * F + 24 * V + 40 * n + 32 * E + 96 * F * (groups - 1) + 72 * F,
-        "vertex_gather": 4 * V + 12 * F + 72 * F + 24 * V,
+        "face_vertex_backward": 24 * F + 24 * V + 40 * n + 32 * E + 72 * F + 4 * V + 12 * F + 72 * F + 24 * V,
     }
 
 
@@ -151,12 +173,39 @@ def survey_bytes_per_view(F, V, E_view, T, W, H):
     return 160 * F + 60 * V + 116 * E_view + 24 * T + 48 * W * H
 
 
+def load_counters(config):
+    """ncu counters of the dominant kernels for THIS config (profiles/
+    traffic_r02.json, keyed by config name), or None."""
+    tf = os.path.join(ROOT, "profiles", "traffic_r02.json")
+    try:
+        with open(tf) as f:
+            return json.load(f).get(config)
+    except Exception:
+        return None
+
+
+def static_config(cfg, name, world):
+    """The `config` object both arms print (run-independent keys only)."""
+    F, V = {("geodesic", 158): (499280, 249642), ("geodesic", 316): (1997120, 998562),
+            ("icosphere", 1280): (1280, 642), ("icosphere", 81920): (81920, 40962)}.get(cfg["mesh"], (None, None))
+    total = cfg.get("total_views", False)
+    per = cfg["views"] // world if total else cfg["views"]
+    return {"workload": cfg["desc"] + (f", {cfg['views']} views sharded over the GPUs" if total else
+                                       f", {cfg['views']} views per GPU per step (hemisphere cameras r=3)"),
+            "name": name, "faces": F, "vertices": V, "views_per_gpu": per, "resolution": [cfg["res"], cfg["res"]],
+            "l2": "inputs+workspace per step > 126 MB L2 (no flush needed)",
+            "parallelism": f"views sharded over {world} GPU(s), one NCCL all-reduce of vertex grads per step"}
+
+
 def run_gmr(args, cfg):
+    import ctypes
+
     import numpy as np
     import torch
     import torch.distributed as dist
 
     import paper_2602_14493_b200 as gmr
+    from paper_2602_14493_b200 import dist as gdist
     from paper_2602_14493_b200 import engine, lib
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -168,12 +217,21 @@ def run_gmr(args, cfg):
     # GMR_BENCH_DIST=1 exercises it even with one rank under torchrun
     multi = world > 1 or os.environ.get("GMR_BENCH_DIST") == "1"
     if multi:
+        # NCCL's init lines (rank count, transport) go to stderr for the record
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=dev)
     L = lib.load()
     mesh = build_mesh(cfg)
-    B, W = cfg["views"], cfg["res"]
-    H = W
-    cams = all_cams(cfg, B * world)[rank * B:(rank + 1) * B]
+    W = H = cfg["res"]
+    if cfg.get("total_views"):   # strong scaling: a fixed set of views split over the ranks
+        lo, hi = gdist.shard_range(cfg["views"], rank, world)
+        cams = all_cams(cfg, cfg["views"])[lo:hi]
+    else:                        # weak scaling: `views` per rank
+        cams = all_cams(cfg, cfg["views"] * world)[rank * cfg["views"]:(rank + 1) * cfg["views"]]
+    B = len(cams)
+    chunk = cfg.get("chunk") or B
+    total_views = cfg["views"] if cfg.get("total_views") else cfg["views"] * world
     pos = torch.tensor(np.asarray(mesh.vertices), dtype=torch.float32, device=dev)
     col = torch.tensor(np.asarray(mesh.colors), dtype=torch.float32, device=dev)
     faces = torch.tensor(np.asarray(mesh.facets), dtype=torch.int32, device=dev)
@@ -181,25 +239,50 @@ def run_gmr(args, cfg):
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
     g_rgb = torch.randn((B, H, W, 3), generator=gen, device=dev)
     g_a = torch.randn((B, H, W), generator=gen, device=dev)
-
-    state = {}
+    T = ((W + 15) // 16) * ((H + 15) // 16)
 
     pending = []
+    last = {}
 
-    def step(final=False):
-        # forward and backward enqueued back to back; the forward's status
-        # (entry capacity, non-finite splats) is validated one step behind,
-        # so the device never drains between steps
-        rgb, alpha, st = engine.render_forward(pos, col, faces, cams, W, H, BG, check=False)
-        gp, gc = engine.render_backward(st, pos, col, faces, rgb, g_rgb, g_a)
+    def step(final=False, flags=0, views=None):
+        # forward and backward of every chunk enqueued back to back; each
+        # forward's status (entry capacity, non-finite splats) is validated
+        # one step behind, so the device never drains between steps
+        nv = B if views is None else views
+        gp = gc = None
+        states = []
+        for c0 in range(0, nv, chunk):
+            c1 = min(nv, c0 + chunk)
+            rgb, alpha, st = engine.render_forward(pos, col, faces, cams[c0:c1], W, H, BG, flags=flags, check=False)
+            a, b = engine.render_backward(st, pos, col, faces, rgb, g_rgb[c0:c1], g_a[c0:c1])
+            gp, gc = (a, b) if gp is None else (gp + a, gc + b)
+            states.append(st)
+        pending.extend(states)
+        last["states"] = states
         if multi:
-            buf = torch.cat([gp, gc], dim=1)
-            dist.all_reduce(buf)
-        pending.append(st)
-        while len(pending) > (0 if final else 1):
+            gdist.allreduce_vertex_grads(gp, gc)
+        keep = 0 if final else len(states)
+        while len(pending) > keep:
             engine.check_status(pending.pop(0))   # raises on overflow / non-finite
-        state["st"] = st
         return gp
+
+    def timed(k, **kw):
+        """K steps bracketed by barrier + synchronize; device ms (max over ranks)."""
+        if multi:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(k):
+            step(final=(i == k - 1), **kw)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        if multi:
+            t = torch.tensor([ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
 
     for i in range(args.warmup):
         step(final=(i == args.warmup - 1))
@@ -207,26 +290,17 @@ def run_gmr(args, cfg):
     sampler = ClockSampler(local) if rank == 0 else None
     time.sleep(0.3 if sampler else 0)
     n0 = L.gmr_launch_count()
-    if multi:
-        dist.barrier()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     wall0 = time.time()
-    e0.record()
-    for i in range(args.steps):
-        step(final=(i == args.steps - 1))
-    e1.record()
-    torch.cuda.synchronize()
+    ms = timed(args.steps)
     wall1 = time.time()
-    if multi:
-        dist.barrier()
     launches = (L.gmr_launch_count() - n0) // args.steps
-    ms = e0.elapsed_time(e1)
+    st_main = last["states"][0]
+    E_step = sum(int(st.entries) for st in last["states"])   # tile entries of one step (all chunks)
+    value = total_views * args.steps / (ms / 1e3)
+
     # per-stage times: the same K steps again with the library's stage
     # timers on (CUDA events on the launching stream around every stage);
-    # kept out of the pass above, whose step time is the headline (the
-    # timers' event bookkeeping is host work that shows on small configs)
-    import ctypes
+    # kept out of the pass above, whose step time is the headline
     L.gmr_timing_enable(1)
     L.gmr_timing_read(None, None, 0, 1)
     for i in range(args.steps):
@@ -236,16 +310,27 @@ def run_gmr(args, cfg):
     scnt = (ctypes.c_int64 * 8)()
     L.gmr_timing_read(sms, scnt, 8, 1)
     L.gmr_timing_enable(0)
-    if multi:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    if sampler:
-        sampler.mark(wall0, wall1)
-    st = state["st"]
-    E = int(st.entries)
-    bins = ((W + 15) // 16) * ((H + 15) // 16) * B
-    value = B * world * args.steps / (ms / 1e3)
+
+    # config 3 extras in the same run: the reference's exact tile lists
+    # (GMR_FLAG_FULL_TILE_LISTS) and batch 1 (BASELINE configs[2])
+    extras = {}
+    if args.config == "c3" and not args.no_extras:
+        for i in range(2):
+            step(final=(i == 1), flags=lib.FLAG_FULL_TILE_LISTS)
+        ms_full = timed(args.steps, flags=lib.FLAG_FULL_TILE_LISTS)
+        extras["full_tile_lists"] = {
+            "value": round(total_views * args.steps / (ms_full / 1e3), 2), "unit": "views/s",
+            "ms_per_step": round(ms_full / args.steps, 4),
+            "tile_entries_per_step": sum(int(st.entries) for st in last["states"]),
+            "note": "GMR_FLAG_FULL_TILE_LISTS: every tile of each splat's 3-sigma rectangle, the reference's "
+                    "_RasterPlan lists bit for bit (render.py:214-226); the headline drops tiles a splat's "
+                    "alpha >= 1/255 ellipse cannot reach (identical images and gradients)"}
+        for i in range(3):
+            step(final=(i == 2), views=1)
+        ms_b1 = timed(args.steps, views=1)
+        extras["batch1"] = {"value": round(world * args.steps / (ms_b1 / 1e3), 2), "unit": "views/s",
+                            "ms_per_step": round(ms_b1 / args.steps, 4),
+                            "note": "config 3 batch 1: one view per GPU per step (BASELINE configs[2])"}
 
     # ---- end to end through the public torch API, host buffers -------------
     # Every step uploads its inputs (vertices, colours, upstream image grads)
@@ -280,16 +365,16 @@ def run_gmr(args, cfg):
         main.wait_event(s["up"])
         p = s["p"].detach().requires_grad_(True)
         c = s["c"].detach().requires_grad_(True)
-        rgb, alpha = gmr.render_views(p, c, faces, cams, W, H, BG)
-        if prefetch:
-            upload(slots[(k + 1) % 2])            # next step's inputs, behind this forward
-        main.wait_event(s["up_g"])
-        torch.autograd.backward([rgb, alpha], [s["g"], s["a"]])
+        for c0 in range(0, B, chunk):
+            c1 = min(B, c0 + chunk)
+            rgb, alpha = gmr.render_views(p, c, faces, cams[c0:c1], W, H, BG)
+            if prefetch and c0 == 0:
+                upload(slots[(k + 1) % 2])        # next step's inputs, behind this forward
+            main.wait_event(s["up_g"])
+            torch.autograd.backward([rgb, alpha], [s["g"][c0:c1], s["a"][c0:c1]])
         gp, gc = p.grad, c.grad
         if multi:
-            buf = torch.cat([gp, gc], dim=1)
-            dist.all_reduce(buf)
-            gp, gc = buf[:, :3], buf[:, 3:]
+            gp, gc, _ = gdist.allreduce_vertex_grads(gp, gc)
         s["used"].record(main)
         with torch.cuda.stream(down_s):
             down_s.wait_event(s["used"])
@@ -307,6 +392,7 @@ def run_gmr(args, cfg):
         dist.barrier()
     k_e2e = max(3, args.steps)
     ctr[0] = 0
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     up_s.wait_stream(main)
     upload(slots[0])                              # the first step's upload is timed too
@@ -322,6 +408,8 @@ def run_gmr(args, cfg):
         ms_e2e = float(t.item())
     h2d = (h_pos.numel() + h_col.numel() + h_g.numel() + h_a.numel()) * 4
     d2h = (o_gp[0].numel() + o_gc[0].numel()) * 4
+    if sampler:
+        sampler.mark(wall0, wall1)
     clocks = sampler.summary() if sampler else None
 
     if rank != 0:
@@ -329,83 +417,80 @@ def run_gmr(args, cfg):
             dist.destroy_process_group()
         return None
 
-    # ---- roofline of the dominant stage ------------------------------------
+    # ---- rooflines of the dominant stage -----------------------------------
     peak, peak_src = load_peaks()
     names = lib.STAGES
-    sb = stage_bytes(F, V, B, W, H, E, bins, bool(state['st'].raster.flags & lib.FLAG_TILE_DEPTH_SORT))
+    per_stage = {nm: sms[i] / args.steps for i, nm in enumerate(names) if scnt[i]}
+    tds = bool(st_main.raster.flags & lib.FLAG_TILE_DEPTH_SORT)
+    b8d = section8d_bytes(F, V, B, W, H, E_step, T)
+    bimp = implementation_bytes(F, V, B, W, H, E_step, T * B, tds)
     stages = {}
-    for i, nm in enumerate(names):
-        if scnt[i]:
-            per = sms[i] / scnt[i]
-            stages[nm] = {"ms_per_launch": round(per, 4), "launches_per_step": scnt[i] // args.steps,
-                          "GBs": round(sb[nm] / (per / 1e3) / 1e9, 1)}
-    dom = max(stages, key=lambda k: stages[k]["ms_per_launch"] * stages[k]["launches_per_step"])
-    dper = stages[dom]["ms_per_launch"]
-    achieved = sb[dom] / (dper / 1e3) / 1e9
-    step_bytes = survey_bytes_per_view(F, V, E / B, (W // 16) * (H // 16), W, H) * B
+    for grp, members in STAGE_GROUPS.items():
+        t = sum(per_stage.get(m, 0.0) for m in members)
+        if t <= 0:
+            continue
+        stages[grp] = {"ms_per_step": round(t, 4), "members": {m: round(per_stage[m], 4) for m in members
+                                                              if m in per_stage},
+                       "GBs_8d": round(b8d[grp] / (t / 1e3) / 1e9, 1),
+                       "frac_8d": round(b8d[grp] / (t / 1e3) / 1e9 / peak, 4),
+                       "GBs_implementation": round(bimp[grp] / (t / 1e3) / 1e9, 1)}
+    dom = max(stages, key=lambda k: stages[k]["ms_per_step"])
+    dms = stages[dom]["ms_per_step"] / ((B + chunk - 1) // chunk)   # per launch
+    per_launch_8d = b8d[dom] / ((B + chunk - 1) // chunk)
+    achieved = per_launch_8d / (dms / 1e3) / 1e9
+    step_bytes = survey_bytes_per_view(F, V, E_step / B, T, W, H) * B
     step_gbs = step_bytes / (ms / args.steps / 1e3) / 1e9
-    traffic, warp_inst, smem_wf = None, None, None
-    tf = os.path.join(ROOT, "profiles", "traffic_r01.json")
-    if os.path.exists(tf):
-        try:
-            tj = json.load(open(tf))
-            traffic = tj.get(dom)
-            warp_inst = (tj.get("warp_instructions") or {}).get(dom)
-            smem_wf = (tj.get("smem_wavefronts") or {}).get(dom)
-        except Exception:
-            traffic, warp_inst, smem_wf = None, None, None
-    # the binding roofline of the blend kernels: instruction issue (148 SMs x
-    # 4 warp-instructions / clock); warp instructions per launch from the ncu
-    # capture in profiles/, time from the live stage timer
-    issue = None
-    if warp_inst:
-        mhz = (clocks or {}).get("sm_mhz") or (clocks or {}).get("sm_max_mhz") or 1965.0
+    ctr_ = load_counters(args.config) or {}
+    kc = ctr_.get(dom) or {}
+    traffic = kc.get("dram_bytes")
+    mhz = (clocks or {}).get("sm_mhz") or (clocks or {}).get("sm_max_mhz") or 1965.0
+    issue = smem = None
+    if kc.get("warp_instructions"):
         peak_issue = 148 * 4 * float(mhz) * 1e6
-        ach = warp_inst / (dper / 1e3)
+        ach = kc["warp_instructions"] / (dms / 1e3)
         issue = {"bound": "issue", "kernel": dom, "achieved": round(ach / 1e12, 4), "peak": round(peak_issue / 1e12, 4),
                  "unit": "T warp-instr/s", "frac": round(ach / peak_issue, 4),
-                 "warp_instructions_per_launch": int(warp_inst), "source": "ncu smsp__inst_executed.sum (profiles/)"}
-    # ... and its shared-memory pipe: one 128-byte wavefront per clock per SM
-    smem = None
-    if smem_wf:
-        mhz = (clocks or {}).get("sm_mhz") or (clocks or {}).get("sm_max_mhz") or 1965.0
+                 "warp_instructions_per_launch": int(kc["warp_instructions"]),
+                 "source": f"ncu smsp__inst_executed.sum, {ctr_.get('source', 'profiles/traffic_r02.json')}"}
+    if kc.get("smem_wavefronts"):
         peak_wf = 148 * float(mhz) * 1e6
-        ach = smem_wf / (dper / 1e3)
+        ach = kc["smem_wavefronts"] / (dms / 1e3)
         smem = {"bound": "shared-memory pipe", "kernel": dom, "achieved": round(ach / 1e12, 4),
                 "peak": round(peak_wf / 1e12, 4), "unit": "T wavefronts/s", "frac": round(ach / peak_wf, 4),
-                "wavefronts_per_launch": int(smem_wf),
-                "source": "ncu l1tex__data_pipe_lsu_wavefronts_mem_shared.sum (profiles/)"}
+                "wavefronts_per_launch": int(kc["smem_wavefronts"]),
+                "source": "ncu l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"}
 
-    # ---- CPU baseline (rank 0, N = 1, bounded sample) -----------------------
+    # ---- CPU baseline (rank 0, N = 1): full unsampled views ---------------
     cpu = None
     if world == 1 and not args.no_cpu:
-        from oracle.cpu_baseline import ViewWorkers
-        wk = ViewWorkers(mesh.vertices, mesh.facets, mesh.colors, all_cams(cfg, max(8, B)), BG)
-        vps, det = wk.step(face_stride=1, tile_stride=args.cpu_tile_stride)
+        from oracle.cpu_baseline import BandWorkers
+        wk = BandWorkers(mesh.vertices, mesh.facets, mesh.colors, all_cams(cfg, 8), BG, bands=1)
+        wall, per = wk.full_view()
         wk.close()
-        cpu = {"value": round(vps, 5), "unit": "views/s", "cores": wk.procs, "kind": "port",
-               "sample": (f"{wk.procs} concurrent views (one process per core), numpy restatement of the "
-                          f"reference (oracle/gmr_oracle.py) in fp32: all per-face stages and binning in "
-                          f"full, blend loops on every {args.cpu_tile_stride}th tile scaled to all tiles; "
-                          f"{det['per_view_s']:.1f} s per view extrapolated")}
+        cpu = {"value": round(wk.procs / wall, 5), "unit": "views/s", "cores": wk.procs, "kind": wk.impl,
+               "sample": (f"{wk.procs} concurrent whole views (one process per host core, OPENBLAS_NUM_THREADS=1), "
+                          f"{'the reference meshsplat from baseline/_ref' if wk.impl == 'reference' else 'the pinned numpy port oracle/gmr_oracle.py'}"
+                          f": render_mesh(float32) + render_backward, unsampled; {float(np.mean(per)):.1f} s per view, "
+                          f"{wall:.1f} s wall")}
 
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "views/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (procedural mesh, seeded vertex colours, N(0,1) upstream image grads)",
-        "config": {"workload": cfg["desc"] + f", {B} views per GPU per step (hemisphere cameras r=3)",
-                   "faces": F, "vertices": V, "views_per_gpu": B, "resolution": [W, H],
-                   "tile_entries_per_step": E, "l2": "inputs+workspace per step > 126 MB L2 (no flush needed)",
-                   "depth_order": ("per-tile lists (GMR_FLAG_TILE_DEPTH_SORT)"
-                                   if state["st"].raster.flags & lib.FLAG_TILE_DEPTH_SORT else "global item sort"),
-                   "parallelism": f"views sharded over {world} GPU(s), NCCL all-reduce of vertex grads"},
-        "e2e": {"value": round(B * world * k_e2e / (ms_e2e / 1e3), 2), "unit": "views/s",
+        "higher_is_better": True, "scaling": "strong" if cfg.get("total_views") else "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic (procedural mesh, seeded vertex colours, N(0,1) upstream image grads)",
+        "config": static_config(cfg, args.config, world),
+        "run": {"tile_entries_per_step": E_step, "views_per_call": chunk,
+                "depth_order": "per-tile lists (GMR_FLAG_TILE_DEPTH_SORT)" if tds else "global item sort",
+                "tile_lists": "unreachable tiles dropped (default)"},
+        "e2e": {"value": round(total_views * k_e2e / (ms_e2e / 1e3), 2), "unit": "views/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "api": "paper_2602_14493_b200.render_views + torch.autograd.backward; pinned host buffers, uploads/read-backs double-buffered on copy streams"},
+                "api": "paper_2602_14493_b200.render_views + torch.autograd.backward; pinned host buffers, "
+                       "uploads/read-backs double-buffered on copy streams"},
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "bytes_per_launch": int(per_launch_8d),
+                     "model": "SURVEY 8(d) per-kernel compulsory bytes (K4: 24WH+8T+36E+32F per view)",
                      "peak_source": peak_src},
         "issue_roofline": issue,
         "smem_roofline": smem,
@@ -417,6 +502,7 @@ def run_gmr(args, cfg):
         "clocks": clocks,
         "cpu_baseline": cpu,
     }
+    line.update(extras)
     print(json.dumps(line), flush=True)
     if multi:
         dist.destroy_process_group()
@@ -439,12 +525,12 @@ def run_fit(args, cfg):
     iters = 200
     cfg5 = gfit.FitConfig(iterations=iters, batch_size=1, seed=0, log_every=0, lr_positions=1e-2)
     for _ in range(max(1, args.warmup)):
-        gfit.fit_device(init, case["cameras"], rgbs, masks, gfit.FitConfig(iterations=5, batch_size=1, seed=0,
+        gfit.fit(init, case["cameras"], rgbs, masks, gfit.FitConfig(iterations=5, batch_size=1, seed=0,
                                                                   log_every=0, lr_positions=1e-2))
     torch.cuda.synchronize()
     walls = []
     for _ in range(max(1, args.steps // 10)):
-        res = gfit.fit_device(init, case["cameras"], rgbs, masks, cfg5)
+        res = gfit.fit(init, case["cameras"], rgbs, masks, cfg5)
         walls.append(res.wall_time)
     wall = float(np.median(walls))
     final = res.history[-1]["total"]
@@ -584,38 +670,50 @@ def run_eval(args, cfg):
 
 
 def run_reference(args, cfg):
-    """CPU arm: the reference algorithm on the host cores (bounded samples)."""
+    """Reference arm: the reference's own CPU render path (the real meshsplat
+    from baseline/_ref when installed, else the pinned numpy port) on all
+    host cores, unsampled -- see oracle/cpu_baseline.py.  A step: every
+    worker renders the next band (1/bands of its view's tile rows) through
+    the reference API; `bands` steps are P whole views.  A calibration pass
+    of P whole views (same workers, concurrent) gives the band split's
+    overhead, and `value` is the whole-view rate."""
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return None
     import numpy as np
-    from oracle.cpu_baseline import ViewWorkers
+    from oracle.cpu_baseline import BandWorkers
     mesh = build_mesh(cfg)
-    B = cfg["views"]
-    wk = ViewWorkers(mesh.vertices, mesh.facets, mesh.colors, all_cams(cfg, max(8, B * world)), BG)
-    for _ in range(args.warmup):
-        wk.step(face_stride=64, tile_stride=512)
+    bands = args.ref_bands
+    wk = BandWorkers(mesh.vertices, mesh.facets, mesh.colors, all_cams(cfg, 8), BG, bands=bands)
+    for i in range(args.warmup):
+        wk.step(i)
+    wk.band_renders, wk.wall = 0, 0.0
     t0 = time.perf_counter()
-    vals = []
-    for _ in range(args.steps):
-        v, det = wk.step(face_stride=args.ref_face_stride, tile_stride=args.ref_tile_stride)
-        vals.append(v)
+    for i in range(args.steps):
+        wk.step(args.warmup + i)
     wall = time.perf_counter() - t0
+    band_rate = wk.views_per_s()
+    full_wall, full_per = (wk.full_view() if not args.ref_no_full else (None, None))
     wk.close()
-    value = float(np.mean(vals))
-    sample = (f"{wk.procs} concurrent views (one process per host core), reference algorithm (numpy "
-              f"restatement pinned to meshsplat) in fp32; per step every {args.ref_face_stride}th face for "
-              f"the per-face stages and every {args.ref_tile_stride}th tile for the blend loops, binning in "
-              f"full, times scaled to whole views")
+    value = wk.procs / full_wall if full_wall else band_rate
+    ms_per_step = 1e3 * wall / args.steps
+    sample = (f"{wk.procs} worker processes (one per host core, OPENBLAS_NUM_THREADS=1), "
+              f"{'the reference meshsplat (baseline/_ref)' if wk.impl == 'reference' else 'the pinned numpy port'}"
+              f" render_mesh(float32) + render_backward, unsampled; a step = every worker renders one of "
+              f"{bands} tile-row bands of its view through a crop camera; value = {wk.procs} concurrent whole "
+              f"views / their wall time ({full_wall:.1f} s)" if full_wall else "")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 5), "unit": "views/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(1e3 * (B * world) / value, 1), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": cfg["desc"] + f", {B} views per GPU-equivalent step", "sampled_wall_s": round(wall, 1)},
-        "cpu_baseline": {"value": round(value, 5), "unit": "views/s", "cores": wk.procs, "kind": "port",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 1),
+        "higher_is_better": True, "scaling": "strong" if cfg.get("total_views") else "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic (procedural mesh, seeded vertex colours, N(0,1) upstream image grads)",
+        "config": static_config(cfg, args.config, world),
+        "cpu_baseline": {"value": round(value, 5), "unit": "views/s", "cores": wk.procs, "kind": wk.impl,
                          "sample": sample},
+        "band_steps": {"views_per_s": round(band_rate, 5), "wall_s": round(wall, 2), "bands_per_view": bands,
+                       "overhead_vs_whole_views": round(value / band_rate, 3) if band_rate else None},
+        "whole_view_s": round(float(np.mean(full_per)), 2) if full_per else None,
         "e2e": {"value": round(value, 5), "unit": "views/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -630,9 +728,9 @@ def main():
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="gmr", choices=["gmr", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
-    ap.add_argument("--cpu-tile-stride", type=int, default=16)
-    ap.add_argument("--ref-face-stride", type=int, default=8)
-    ap.add_argument("--ref-tile-stride", type=int, default=32)
+    ap.add_argument("--no-extras", action="store_true", help="config 3: skip the full-tile-list and batch-1 lines")
+    ap.add_argument("--ref-bands", type=int, default=10, help="reference arm: tile-row bands per view")
+    ap.add_argument("--ref-no-full", action="store_true", help="reference arm: skip the whole-view pass")
     ap.add_argument("--views-f32", action="store_true", help="--config views: render in float32")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]

@@ -19,6 +19,8 @@
  *   losses.py:151-162  total_loss view loop          B views per gmr_render_* call
  *   losses.py:43-73    color_loss, silhouette_loss   gmr_render_forward_loss (fused)
  *   losses.py:76-123, optim.py:29-135, :271-295      gmr_fit_step (regularisers + Adam)
+ *   losses.py:76-123   edge_length / laplacian loss  gmr_mesh_regularizers
+ *   losses.py:43-73    color_loss, silhouette_loss   gmr_image_loss (stand-alone)
  *   dataset.py:118-164 make_views (render + _save_png) gmr_render_images_u8
  *   convert.py:497-532 export_gaussians              gmr_export_gaussians
  *   metrics.py:40-86   chamfer / normal consistency  gmr_chamfer_nc, gmr_nearest
@@ -221,6 +223,25 @@ int gmr_fit_step(const GmrFitState* state, const GmrMeshGraph* graph, int64_t nu
                  double beta1, double beta2, double eps, int32_t optimize_colors,
                  double* history_row, void* scratch, size_t scratch_bytes, void* stream);
 
+/* The mesh regularisers of total_loss on their own (losses.py:76-123):
+ * values (device, 2 doubles) = (edge-length loss, Laplacian loss) of the
+ * float64 positions [V,3]; grad_edge / grad_laplacian (device [V,3]
+ * doubles, either may be null) their gradients, accumulated in the
+ * reference's np.add.at order over the static graph.  Scratch size:
+ * gmr_fit_scratch_size. */
+int gmr_mesh_regularizers(const double* positions, const GmrMeshGraph* graph, int64_t num_vertices,
+                          double* values, double* grad_edge, double* grad_laplacian, void* scratch,
+                          size_t scratch_bytes, void* stream);
+
+/* The image losses of the drop-in color_loss / silhouette_loss
+ * (losses.py:43-73) over n float64 elements: kind 0 = mean squared error of
+ * x against target, grad = 2 (x - target) / n; kind 1 = binary cross-entropy
+ * of alpha x against mask target with the reference's 1e-6 clamp and
+ * clamp-gated grad.  value (device, 1 double) = the mean. */
+int gmr_image_loss_scratch_size(int64_t n, size_t* bytes);
+int gmr_image_loss(int32_t kind, const double* x, const double* target, int64_t n, double* grad,
+                   double* value, void* scratch, size_t scratch_bytes, void* stream);
+
 /* Synchronise `stream` and read the status of the last forward that used
  * `workspace`.  Returns GMR_ECAPACITY / GMR_ENONFINITE as appropriate. */
 int gmr_status(const void* workspace, GmrStatus* status, void* stream);
@@ -234,7 +255,9 @@ int gmr_topology_build(const int32_t* faces, int64_t num_faces, int64_t num_vert
 /* Backward of sum(g_rgb*rgb) + sum(g_alpha*alpha) over all B views:
  * grad_positions / grad_colors [V,3] (dtype) are OVERWRITTEN with the sum
  * over views (reference losses.py:160-162 semantics when the caller
- * pre-scales g by w/n).  `rgb` is the forward's output. */
+ * pre-scales g by w/n).  `rgb` is the forward's output.  After a forward
+ * that overflowed its entry capacity (GmrStatus.overflow) the gradients are
+ * written as zeros and nothing outside the workspace is read. */
 int gmr_render_backward(const GmrMesh* mesh, const GmrCamera* cameras, int32_t num_views,
                         const GmrRaster* raster, const void* rgb, const void* grad_rgb,
                         const void* grad_alpha, void* grad_positions, void* grad_colors,
@@ -297,7 +320,9 @@ int gmr_convert_scratch_size(int64_t num_faces, int32_t dtype, size_t* bytes);
  * it = *iteration (device int64), the learning rates are lr_schedule[2 it]
  * (positions) and [2 it + 1] (colours), the losses go to history[5 it ..],
  * the render's 64-byte status (render_status, may be null) is copied to
- * statuses[64 it ..], and *iteration is incremented last. */
+ * statuses[64 it ..], and *iteration is incremented last.  A step whose
+ * render status shows an entry overflow or a non-finite splat is rejected
+ * (no parameter or moment changes; the host re-runs with more capacity). */
 int gmr_fit_step_scheduled(const GmrFitState* state, const GmrMeshGraph* graph, int64_t num_vertices,
                            const float* grad_img_pos, const float* grad_img_col,
                            const double* img_loss_sums, double inv_nc, double inv_na, double w_color,

@@ -473,3 +473,98 @@ def views_image_grad(vertices, facets, colors, cams, target_rgb, target_mask,
         gv += a
         gc += b
     return cval / n, sval / n, gv, gc
+
+
+# ---------------------------------------------------------------------------
+# mesh regularisers (losses.py:76-123) and the optimiser (optim.py:29-135),
+# checkers for the device kernels of gmr_train.cuh
+# ---------------------------------------------------------------------------
+
+def unique_edges(facets):
+    """mesh.py:96-106: unique undirected edges, smaller index first, lexsorted."""
+    f = np.asarray(facets, np.int64)
+    if len(f) == 0:
+        return np.zeros((0, 2), np.int64)
+    return np.unique(np.sort(f[:, [0, 1, 1, 2, 2, 0]].reshape(-1, 2), axis=1), axis=0)
+
+
+def edge_length_loss(vertices, facets):
+    """losses.py:76-97 (mean length detached; np.add.at scatter order)."""
+    v = np.asarray(vertices, np.float64)
+    e = unique_edges(facets)
+    if len(e) == 0:
+        return 0.0, np.zeros_like(v)
+    vec = v[e[:, 1]] - v[e[:, 0]]
+    length = np.linalg.norm(vec, axis=1)
+    dev = length - length.mean()
+    coeff = (2.0 / len(e)) * dev / np.maximum(length, 1e-12)
+    g = np.zeros_like(v)
+    np.add.at(g, e[:, 1], coeff[:, None] * vec)
+    np.add.at(g, e[:, 0], -coeff[:, None] * vec)
+    return float(np.mean(dev * dev)), g
+
+
+def laplacian_loss(vertices, facets):
+    """losses.py:100-123 (uniform Laplacian over the sorted neighbour lists,
+    mesh.py:114-126)."""
+    v = np.asarray(vertices, np.float64)
+    nv = len(v)
+    e = unique_edges(facets)
+    both = np.concatenate([e, e[:, ::-1]]) if len(e) else np.zeros((0, 2), np.int64)
+    both = both[np.lexsort((both[:, 1], both[:, 0]))]
+    deg = np.bincount(both[:, 0], minlength=nv).astype(np.float64)
+    has = deg > 0
+    nbr = np.zeros_like(v)
+    np.add.at(nbr, both[:, 0], v[both[:, 1]])
+    lap = np.zeros_like(v)
+    lap[has] = v[has] - nbr[has] / deg[has, None]
+    scaled = np.where(has[:, None], lap / np.maximum(deg, 1.0)[:, None], 0.0)
+    back = np.zeros_like(v)
+    np.add.at(back, both[:, 1], scaled[both[:, 0]])
+    return float(np.mean(np.sum(lap * lap, axis=1))), (2.0 / nv) * lap - (2.0 / nv) * back
+
+
+class VectorAdam:
+    """optim.py:29-81: Adam with one second moment per vertex row; a step
+    with a non-finite gradient is rejected."""
+
+    def __init__(self, n, beta1=0.9, beta2=0.999, eps=1e-8):
+        self.b1, self.b2, self.eps = beta1, beta2, eps
+        self.m, self.v, self.t = np.zeros((n, 3)), np.zeros(n), 0
+
+    def step(self, p, g, lr):
+        if not np.all(np.isfinite(g)):
+            return p
+        self.t += 1
+        self.m = self.b1 * self.m + (1 - self.b1) * g
+        self.v = self.b2 * self.v + (1 - self.b2) * np.sum(g * g, axis=1)
+        mh = self.m / (1 - self.b1 ** self.t)
+        vh = self.v / (1 - self.b2 ** self.t)
+        return p - lr * mh / (np.sqrt(vh)[:, None] + self.eps)
+
+
+class ScalarAdam:
+    """optim.py:84-126: per-component Adam."""
+
+    def __init__(self, shape, beta1=0.9, beta2=0.999, eps=1e-8):
+        self.b1, self.b2, self.eps = beta1, beta2, eps
+        self.m, self.v, self.t = np.zeros(shape), np.zeros(shape), 0
+
+    def step(self, p, g, lr):
+        if not np.all(np.isfinite(g)):
+            return p
+        self.t += 1
+        self.m = self.b1 * self.m + (1 - self.b1) * g
+        self.v = self.b2 * self.v + (1 - self.b2) * g * g
+        mh = self.m / (1 - self.b1 ** self.t)
+        vh = self.v / (1 - self.b2 ** self.t)
+        return p - lr * mh / (np.sqrt(vh) + self.eps)
+
+
+def cosine_lr(it, total, base, floor_fraction=0.1):
+    """optim.py:129-135."""
+    if total <= 1:
+        return base
+    frac = min(max(it / (total - 1), 0.0), 1.0)
+    lo = floor_fraction * base
+    return lo + (base - lo) * 0.5 * (1.0 + np.cos(np.pi * frac))

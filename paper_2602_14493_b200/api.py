@@ -104,14 +104,6 @@ class RenderContext:
     rgb_device: torch.Tensor
 
 
-def _kept_rank(state, num_faces):
-    def to_index(item):
-        _, _, cnt, _ = engine.copy_splats(state, num_faces, True)
-        c = cnt.cpu().numpy()
-        return int(np.count_nonzero(c[:item] > 0))
-    return to_index
-
-
 def render_mesh(mesh, camera, background=(0.0, 0.0, 0.0), rescale: bool = True,
                 dtype=np.float64, return_ctx: bool = False):
     """convert -> project -> rasterize on the GPU (reference render.py:441-450)."""
@@ -119,7 +111,7 @@ def render_mesh(mesh, camera, background=(0.0, 0.0, 0.0), rescale: bool = True,
     bg = np.asarray(background, dtype=dtype)
     rgb, alpha, state = engine.render_forward(
         pos, col, faces, [camera], camera.width, camera.height, bg, rescale,
-        item_to_index=None)
+        item_to_index="kept")
     out = RenderOutput(rgb=rgb[0].cpu().numpy(), alpha=alpha[0].cpu().numpy(), background=bg)
     if not return_ctx:
         return out
@@ -324,80 +316,103 @@ class LossReport:
     n_views: int
 
 
+def _scratch(n_bytes, dev):
+    return torch.empty(max(int(n_bytes), 1), dtype=torch.uint8, device=dev)
+
+
+def _image_loss(kind, x, t):
+    import ctypes
+    lib = engine.L.load()
+    dev = _device()
+    xd = torch.as_tensor(np.ascontiguousarray(x, dtype=np.float64)).to(dev)
+    td = torch.as_tensor(np.ascontiguousarray(t, dtype=np.float64)).to(dev)
+    n = xd.numel()
+    grad = torch.empty_like(xd)
+    val = torch.empty(1, dtype=torch.float64, device=dev)
+    if n == 0:
+        return float("nan"), np.zeros(xd.shape)
+    nb = ctypes.c_size_t()
+    engine.L.check(lib.gmr_image_loss_scratch_size(n, ctypes.byref(nb)))
+    scr = _scratch(nb.value, dev)
+    engine.L.check(lib.gmr_image_loss(kind, engine._ptr(xd), engine._ptr(td), n, engine._ptr(grad),
+                                      engine._ptr(val), engine._ptr(scr), nb.value, engine._stream()))
+    return float(val.item()), grad.cpu().numpy()
+
+
 def color_loss(rendered, target):
-    """MSE and its gradient (losses.py:43-56)."""
-    rendered = np.asarray(rendered, dtype=np.float64)
-    target = np.asarray(target, dtype=np.float64)
+    """Mean squared colour error and its gradient (losses.py:43-56), float64,
+    computed on the device (gmr_image_loss kind 0)."""
+    rendered, target = np.asarray(rendered), np.asarray(target)
     if rendered.shape != target.shape:
         raise ValueError(f"shape mismatch: {rendered.shape} vs {target.shape}")
-    diff = rendered - target
-    return float(np.mean(diff * diff)), (2.0 / diff.size) * diff
+    return _image_loss(0, rendered, target)
 
 
 def silhouette_loss(alpha, mask):
-    """Clamped BCE and its gradient (losses.py:59-73)."""
-    alpha = np.asarray(alpha, dtype=np.float64)
-    mask = np.asarray(mask, dtype=np.float64)
+    """Clamped binary cross-entropy of alpha against the mask and its
+    gradient (losses.py:59-73), float64, on the device (gmr_image_loss kind 1)."""
+    alpha, mask = np.asarray(alpha), np.asarray(mask)
     if alpha.shape != mask.shape:
         raise ValueError(f"shape mismatch: {alpha.shape} vs {mask.shape}")
-    p = np.clip(alpha, BCE_CLAMP, 1.0 - BCE_CLAMP)
-    value = float(-np.mean(mask * np.log(p) + (1.0 - mask) * np.log1p(-p)))
-    inside = (alpha > BCE_CLAMP) & (alpha < 1.0 - BCE_CLAMP)
-    return value, np.where(inside, (-mask / p + (1.0 - mask) / (1.0 - p)) / alpha.size, 0.0)
+    return _image_loss(1, alpha, mask)
 
 
-def _edges(facets):
-    ent = _facets_entry(facets) if _cuda_ok() else {}
-    e = ent.get("edges")
-    if e is None:
-        e = np.unique(np.sort(np.asarray(facets)[:, [0, 1, 1, 2, 2, 0]].reshape(-1, 2), axis=1), axis=0)
-        ent["edges"] = e
-    return e
+def _graph(facets, num_vertices):
+    """Static mesh graph on the device (edges, np.add.at-order CSRs), cached
+    with the facets' other per-topology data."""
+    from . import lib as L
+    from .mesh import mesh_graph
+    ent = _facets_entry(facets)
+    hit = ent.get("graph")
+    if hit is None or hit[0] != num_vertices:
+        dev = _device()
+        g = {k: torch.as_tensor(v).to(dev) for k, v in mesh_graph(facets, num_vertices).items()}
+        st = L.GmrMeshGraph(g["edges"].data_ptr(), int(g["edges"].shape[0]), g["ve_ptr"].data_ptr(),
+                            g["ve_slot"].data_ptr(), g["adj_ptr"].data_ptr(), g["adj"].data_ptr())
+        hit = ent["graph"] = (num_vertices, st, g)
+    return hit[1]
 
 
-def _cuda_ok():
-    return torch.cuda.is_available()
+def _regularizers(facets, vertices, want_edge=True, want_lap=True):
+    """(values [2] (edge, laplacian), grad_edge, grad_laplacian) on the
+    device for float64 vertices (gmr_mesh_regularizers)."""
+    import ctypes
+    lib = engine.L.load()
+    dev = _device()
+    v = torch.as_tensor(np.ascontiguousarray(vertices, dtype=np.float64)).to(dev) \
+        if not isinstance(vertices, torch.Tensor) else vertices.to(dev, torch.float64).contiguous()
+    nv = int(v.shape[0])
+    graph = _graph(facets, nv)
+    nb = ctypes.c_size_t()
+    engine.L.check(lib.gmr_fit_scratch_size(nv, graph.num_edges, ctypes.byref(nb)))
+    scr = _scratch(nb.value, dev)
+    vals = torch.empty(2, dtype=torch.float64, device=dev)
+    ge = torch.empty_like(v) if want_edge else None
+    gl = torch.empty_like(v) if want_lap else None
+    engine.L.check(lib.gmr_mesh_regularizers(engine._ptr(v), ctypes.byref(graph), nv, engine._ptr(vals),
+                                             engine._ptr(ge), engine._ptr(gl), engine._ptr(scr), nb.value,
+                                             engine._stream()))
+    return vals, ge, gl
 
 
 def edge_length_loss(mesh, vertices=None):
-    """losses.py:76-97 (mesh regulariser; evaluated once per objective)."""
+    """Edge-length variance regulariser and its gradient (losses.py:76-97),
+    on the device (gmr_mesh_regularizers)."""
     verts = np.asarray(mesh.vertices if vertices is None else vertices, dtype=np.float64)
-    edges = _edges(mesh.facets) if len(mesh.facets) else np.zeros((0, 2), np.int64)
-    if len(edges) == 0:
+    if len(mesh.facets) == 0 or len(verts) == 0:
         return 0.0, np.zeros_like(verts)
-    vec = verts[edges[:, 1]] - verts[edges[:, 0]]
-    length = np.linalg.norm(vec, axis=1)
-    dev = length - length.mean()
-    coeff = (2.0 / len(edges)) * dev / np.maximum(length, 1e-12)
-    grad = np.zeros_like(verts)
-    np.add.at(grad, edges[:, 1], coeff[:, None] * vec)
-    np.add.at(grad, edges[:, 0], -coeff[:, None] * vec)
-    return float(np.mean(dev * dev)), grad
+    vals, ge, _ = _regularizers(mesh.facets, verts, want_lap=False)
+    return float(vals[0].item()), ge.cpu().numpy()
 
 
 def laplacian_loss(mesh, vertices=None):
-    """losses.py:100-123 (uniform Laplacian regulariser)."""
+    """Uniform-Laplacian regulariser and its gradient (losses.py:100-123), on
+    the device (gmr_mesh_regularizers)."""
     verts = np.asarray(mesh.vertices if vertices is None else vertices, dtype=np.float64)
-    nv = len(verts)
-    ent = _facets_entry(mesh.facets) if _cuda_ok() else {}
-    both = ent.get("adjacency")
-    if both is None:
-        e = _edges(mesh.facets) if len(mesh.facets) else np.zeros((0, 2), np.int64)
-        both = np.concatenate([e, e[:, ::-1]]) if len(e) else np.zeros((0, 2), np.int64)
-        both = both[np.lexsort((both[:, 1], both[:, 0]))]
-        ent["adjacency"] = both
-    deg = np.bincount(both[:, 0], minlength=nv).astype(np.float64)
-    owner = both[:, 0]
-    has = deg > 0
-    nbr = np.zeros_like(verts)
-    np.add.at(nbr, owner, verts[both[:, 1]])
-    lap = np.zeros_like(verts)
-    lap[has] = verts[has] - nbr[has] / deg[has, None]
-    value = float(np.mean(np.sum(lap * lap, axis=1)))
-    scaled = np.where(has[:, None], lap / np.maximum(deg, 1.0)[:, None], 0.0)
-    back = np.zeros_like(verts)
-    np.add.at(back, both[:, 1], scaled[owner])
-    return value, (2.0 / nv) * lap - (2.0 / nv) * back
+    if len(verts) == 0:
+        return 0.0, np.zeros_like(verts)
+    vals, _, gl = _regularizers(mesh.facets, verts, want_edge=False)
+    return float(vals[1].item()), gl.cpu().numpy()
 
 
 def total_loss(mesh, cameras: Sequence[Camera], target_rgb, target_mask, weights: LossWeights = LossWeights(),
@@ -436,17 +451,20 @@ def total_loss(mesh, cameras: Sequence[Camera], target_rgb, target_mask, weights
         gp, gc = engine.render_backward(state, pos, col, faces, rgb, g_rgb, g_a)
         gp_acc += gp.double()
         gc_acc += gc.double()
-    # one transfer for everything
-    flat = torch.cat([cv_acc.view(1), sv_acc.view(1), gp_acc.view(-1), gc_acc.view(-1)]).cpu().numpy()
-    cval_sum, sval_sum = flat[0], flat[1]
+    # the mesh regularisers on the device too (float64 like the reference)
     nv = len(mesh.vertices)
-    grad_v = flat[2:2 + 3 * nv].reshape(nv, 3).copy()
-    grad_c = flat[2 + 3 * nv:].reshape(nv, 3).copy()
+    if len(mesh.facets) and nv:
+        regs, g_edge, g_lap = _regularizers(mesh.facets, mesh.vertices)
+        gp_acc += weights.edge * g_edge + weights.laplacian * g_lap
+    else:
+        regs = torch.zeros(2, dtype=torch.float64, device=dev)
+    # one transfer for everything
+    flat = torch.cat([cv_acc.view(1), sv_acc.view(1), regs, gp_acc.view(-1), gc_acc.view(-1)]).cpu().numpy()
+    cval_sum, sval_sum, edge_val, lap_val = flat[0], flat[1], float(flat[2]), float(flat[3])
+    grad_v = flat[4:4 + 3 * nv].reshape(nv, 3).copy()
+    grad_c = flat[4 + 3 * nv:].reshape(nv, 3).copy()
     color_val = float(cval_sum / n)
     sil_val = float(sval_sum / n)
-    edge_val, g_edge = edge_length_loss(mesh)
-    lap_val, g_lap = laplacian_loss(mesh)
-    grad_v += weights.edge * g_edge + weights.laplacian * g_lap
     total = (weights.color * color_val + weights.silhouette * sil_val
              + weights.edge * edge_val + weights.laplacian * lap_val)
     return LossReport(color=color_val, silhouette=sil_val, edge=edge_val, laplacian=lap_val,

@@ -436,6 +436,7 @@ int render_backward_t(const GmrMesh* m, const GmrCamera* cams, int B, const GmrR
     a.face_acc = at<double>(ws, L.face_acc);
     // the last group also runs the conversion backward (face_acc stays in registers)
     a.corner = (v0 + nv == B) ? at<S>(ws, L.corner) : nullptr;
+    a.st = at<DevStatus>(ws, L.status);
     if (F) {
       StageScope sc(kStFaceBwd, st);
       face_views_backward<S><<<grid_for(F, 128), 128, 0, st>>>(a, make_cams<S>(cams, v0, nv));
@@ -509,7 +510,8 @@ int rasterize_backward_t(const GmrSplats* sp, const GmrRaster* r, const void* rg
   if (sp->count) {
     splat_grads<S><<<grid_for(sp->count, 256), 256, 0, st>>>(
         at<uint32_t>(ws, L.count), at<uint32_t>(ws, L.entry_off), at<Splat<S>>(ws, L.splat),
-        at<S>(ws, L.partial), at<S>(ws, L.partial_op), sp->count, (S*)gm, (S*)gc, (S*)gcol, (S*)gop);
+        at<S>(ws, L.partial), at<S>(ws, L.partial_op), sp->count, at<DevStatus>(ws, L.status), (S*)gm, (S*)gc,
+        (S*)gcol, (S*)gop);
     GMR_LAUNCHED();
   }
   return GMR_OK;
@@ -656,6 +658,47 @@ int gmr_fit_scratch_size(int64_t V, int64_t E, size_t* bytes) {
 }
 
 namespace {
+// The regulariser terms shared by gmr_fit_step and gmr_mesh_regularizers:
+// per-edge coeff * vec, per-vertex Laplacian, and sums[0..2] = (sum of edge
+// lengths, sum of dev^2, sum of |lap|^2), all in `scratch` (gmr_fit_scratch_size).
+struct RegScratch {
+  double *evec4, *lap4, *gpos, *gcol, *sums;
+};
+
+int reg_terms(const double* pos, const GmrMeshGraph* gr, int64_t V, void* scratch, cudaStream_t st,
+              RegScratch* out) {
+  const int64_t E = gr->num_edges;
+  const int nbe = (int)((E + kTrainThreads - 1) / kTrainThreads), nbv = (int)((V + kTrainThreads - 1) / kTrainThreads);
+  char* o = (char*)scratch;
+  double* evec4 = (double*)o; o += align_up(E * 32);
+  double* lap4 = (double*)o; o += align_up(V * 32);
+  double* gpos = (double*)o; o += align_up(V * 24);
+  double* gcol = (double*)o; o += align_up(V * 24);
+  double* part = (double*)o; o += align_up((2 * (nbe + 1) + nbv + 1) * 8);
+  double* sums = (double*)o;   // [0] sum len, [1] sum dev^2, [2] sum |lap|^2
+  double* part_len = part;
+  double* part_dev = part + nbe + 1;
+  double* part_lap = part + 2 * (nbe + 1);
+  if (E) {
+    edge_lengths<<<nbe, kTrainThreads, 0, st>>>(pos, gr->edges, E, evec4, part_len);
+    GMR_LAUNCHED();
+    sum_partials<<<1, kTrainThreads, 0, st>>>(part_len, nbe, sums);
+    GMR_LAUNCHED();
+    edge_terms<<<nbe, kTrainThreads, 0, st>>>(evec4, E, sums, part_dev);
+    GMR_LAUNCHED();
+    sum_partials<<<1, kTrainThreads, 0, st>>>(part_dev, nbe, sums + 1);
+    GMR_LAUNCHED();
+  } else {
+    GMR_CUDA(cudaMemsetAsync(sums, 0, 16, st));
+  }
+  laplacian_terms<<<nbv, kTrainThreads, 0, st>>>(pos, gr->adj_ptr, gr->adj, V, lap4, part_lap);
+  GMR_LAUNCHED();
+  sum_partials<<<1, kTrainThreads, 0, st>>>(part_lap, nbv, sums + 2);
+  GMR_LAUNCHED();
+  *out = RegScratch{evec4, lap4, gpos, gcol, sums};
+  return GMR_OK;
+}
+
 int fit_step_impl(const GmrFitState* s, const GmrMeshGraph* gr, int64_t V, const float* grad_img_pos,
                   const float* grad_img_col, const double* img_loss_sums, double inv_nc, double inv_na,
                   double w_color, double w_sil, double w_edge, double w_lap, double lr_pos, double lr_col,
@@ -670,33 +713,10 @@ int fit_step_impl(const GmrFitState* s, const GmrMeshGraph* gr, int64_t V, const
   if (rc) return rc;
   if (scratch_bytes < need) return fail(GMR_EWORKSPACE, "fit scratch has %zu bytes, needs %zu", scratch_bytes, need);
   cudaStream_t st = (cudaStream_t)stream;
-  const int nbe = (int)((E + kTrainThreads - 1) / kTrainThreads), nbv = (int)((V + kTrainThreads - 1) / kTrainThreads);
-  char* o = (char*)scratch;
-  double* evec4 = (double*)o; o += align_up(E * 32);
-  double* lap4 = (double*)o; o += align_up(V * 32);
-  double* gpos = (double*)o; o += align_up(V * 24);
-  double* gcol = (double*)o; o += align_up(V * 24);
-  double* part = (double*)o; o += align_up((2 * (nbe + 1) + nbv + 1) * 8);
-  double* sums = (double*)o;   // [0] sum len, [1] sum dev^2, [2] sum |lap|^2
-  double* part_len = part;
-  double* part_dev = part + nbe + 1;
-  double* part_lap = part + 2 * (nbe + 1);
-  if (E) {
-    edge_lengths<<<nbe, kTrainThreads, 0, st>>>(s->positions, gr->edges, E, evec4, part_len);
-    GMR_LAUNCHED();
-    sum_partials<<<1, kTrainThreads, 0, st>>>(part_len, nbe, sums);
-    GMR_LAUNCHED();
-    edge_terms<<<nbe, kTrainThreads, 0, st>>>(evec4, E, sums, part_dev);
-    GMR_LAUNCHED();
-    sum_partials<<<1, kTrainThreads, 0, st>>>(part_dev, nbe, sums + 1);
-    GMR_LAUNCHED();
-  } else {
-    GMR_CUDA(cudaMemsetAsync(sums, 0, 16, st));
-  }
-  laplacian_terms<<<nbv, kTrainThreads, 0, st>>>(s->positions, gr->adj_ptr, gr->adj, V, lap4, part_lap);
-  GMR_LAUNCHED();
-  sum_partials<<<1, kTrainThreads, 0, st>>>(part_lap, nbv, sums + 2);
-  GMR_LAUNCHED();
+  const int nbv = (int)((V + kTrainThreads - 1) / kTrainThreads);
+  RegScratch rs;
+  if ((rc = reg_terms(s->positions, gr, V, scratch, st, &rs))) return rc;
+  double *evec4 = rs.evec4, *lap4 = rs.lap4, *gpos = rs.gpos, *gcol = rs.gcol, *sums = rs.sums;
   AdamArgs a{};
   a.pos = s->positions; a.col = s->colors; a.pos_f = s->positions_f32; a.col_f = s->colors_f32;
   a.g_img_pos = grad_img_pos; a.g_img_col = grad_img_col;
@@ -705,6 +725,7 @@ int fit_step_impl(const GmrFitState* s, const GmrMeshGraph* gr, int64_t V, const
   a.lr_pos = lr_pos; a.lr_col = lr_col; a.beta1 = beta1; a.beta2 = beta2; a.eps = eps;
   a.lr_sched = lr_sched; a.iter = iter;
   a.optimize_colors = optimize_colors;
+  a.render_status = (const DevStatus*)status_src;
   a.reg.ve_ptr = gr->ve_ptr; a.reg.ve_slot = gr->ve_slot; a.reg.adj_ptr = gr->adj_ptr; a.reg.adj = gr->adj;
   a.reg.evec4 = evec4; a.reg.lap4 = lap4; a.reg.V = V; a.reg.w_edge = w_edge; a.reg.w_lap = w_lap;
   fit_grads<<<nbv, kTrainThreads, 0, st>>>(a, gpos, gcol);
@@ -738,6 +759,56 @@ int gmr_fit_step_scheduled(const GmrFitState* s, const GmrMeshGraph* gr, int64_t
   return fit_step_impl(s, gr, V, grad_img_pos, grad_img_col, img_loss_sums, inv_nc, inv_na, w_color, w_sil, w_edge,
                        w_lap, 0.0, 0.0, lr_schedule, iteration, beta1, beta2, eps, optimize_colors, history,
                        render_status, statuses, scratch, scratch_bytes, stream);
+}
+
+int gmr_mesh_regularizers(const double* positions, const GmrMeshGraph* gr, int64_t V, double* values,
+                          double* grad_edge, double* grad_laplacian, void* scratch, size_t scratch_bytes,
+                          void* stream) {
+  if (!positions || !gr || V <= 0 || !values || !scratch) return fail(GMR_EINVAL, "null or empty argument");
+  size_t need;
+  int rc = gmr_fit_scratch_size(V, gr->num_edges, &need);
+  if (rc) return rc;
+  if (scratch_bytes < need) return fail(GMR_EWORKSPACE, "regulariser scratch has %zu bytes, needs %zu", scratch_bytes, need);
+  cudaStream_t st = (cudaStream_t)stream;
+  RegScratch rs;
+  if ((rc = reg_terms(positions, gr, V, scratch, st, &rs))) return rc;
+  reg_values<<<1, 1, 0, st>>>(rs.sums, gr->num_edges, V, values);
+  GMR_LAUNCHED();
+  if (grad_edge || grad_laplacian) {
+    RegArgs r{};
+    r.ve_ptr = gr->ve_ptr; r.ve_slot = gr->ve_slot; r.adj_ptr = gr->adj_ptr; r.adj = gr->adj;
+    r.evec4 = rs.evec4; r.lap4 = rs.lap4; r.V = V; r.w_edge = 1.0; r.w_lap = 1.0;
+    reg_grads<<<(unsigned)((V + kTrainThreads - 1) / kTrainThreads), kTrainThreads, 0, st>>>(r, grad_edge,
+                                                                                          grad_laplacian);
+    GMR_LAUNCHED();
+  }
+  return GMR_OK;
+}
+
+int gmr_image_loss_scratch_size(int64_t n, size_t* bytes) {
+  if (!bytes || n < 0) return fail(GMR_EINVAL, "bad sizes");
+  *bytes = align_up(((n + kTrainThreads - 1) / kTrainThreads + 1) * 8);
+  return GMR_OK;
+}
+
+int gmr_image_loss(int32_t kind, const double* x, const double* target, int64_t n, double* grad, double* value,
+                   void* scratch, size_t scratch_bytes, void* stream) {
+  if (kind != 0 && kind != 1) return fail(GMR_EINVAL, "kind must be 0 (colour MSE) or 1 (silhouette BCE)");
+  if (n <= 0 || !x || !target || !grad || !value || !scratch) return fail(GMR_EINVAL, "null or empty argument");
+  size_t need;
+  int rc = gmr_image_loss_scratch_size(n, &need);
+  if (rc) return rc;
+  if (scratch_bytes < need) return fail(GMR_EWORKSPACE, "loss scratch has %zu bytes, needs %zu", scratch_bytes, need);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nb = (int)((n + kTrainThreads - 1) / kTrainThreads);
+  double* part = (double*)scratch;
+  image_loss_terms<<<nb, kTrainThreads, 0, st>>>(kind, x, target, n, grad, part);
+  GMR_LAUNCHED();
+  sum_partials<<<1, kTrainThreads, 0, st>>>(part, nb, value);
+  GMR_LAUNCHED();
+  scale_value<<<1, 1, 0, st>>>(value, 1.0 / (double)n);
+  GMR_LAUNCHED();
+  return GMR_OK;
 }
 
 int gmr_status(const void* ws, GmrStatus* out, void* stream) {

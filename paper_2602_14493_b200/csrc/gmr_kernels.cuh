@@ -1506,6 +1506,7 @@ template <typename S> struct FaceBwdArgs {
   const S* partial;
   double* face_acc;   // [F][12]: g_mean3 (3), g_cov3 sym (6), g_col (3), summed over views in float64
   S* corner;          // non-null on the last view group: write per-corner grads (convert_corners), not face_acc
+  const DevStatus* st;   // the forward's status: after an entry overflow no partial was written
 };
 
 template <typename S>
@@ -1541,11 +1542,15 @@ __global__ void __launch_bounds__(128, GMR_K5_MINB) face_views_backward(FaceBwdA
   // (item_offsets: face-major), so only the first offset is loaded; the
   // counts of a group of 8 views are loaded together, ahead of their use
   uint32_t off = p.entry_off[(int64_t)p.view0 * p.F + f];
-  for (int v8 = 0; v8 < p.nviews; v8 += 8) {
+  // An overflowed forward emitted no entries (scan_top), but the counts and
+  // offsets still describe the full entry set, past the partial buffer: read
+  // nothing and write zero gradients (the host reports GMR_ECAPACITY).
+  const int nviews = p.st->overflow ? 0 : p.nviews;
+  for (int v8 = 0; v8 < nviews; v8 += 8) {
    uint32_t cn[8], run = 0;
 #pragma unroll
    for (int k = 0; k < 8; ++k) {
-     cn[k] = (v8 + k < p.nviews) ? p.count[(int64_t)(p.view0 + v8 + k) * p.F + f] : 0u;
+     cn[k] = (v8 + k < nviews) ? p.count[(int64_t)(p.view0 + v8 + k) * p.F + f] : 0u;
      run += cn[k];
    }
    // the group's partials are one contiguous run: start pulling it into L2
@@ -1751,10 +1756,12 @@ __global__ void __launch_bounds__(256) splat_grads(const uint32_t* __restrict__ 
                                                   const Splat<S>* __restrict__ splat,
                                                   const S* __restrict__ partial,
                                                   const S* __restrict__ partial_op, int64_t K,
+                                                  const DevStatus* __restrict__ st,
                                                   S* g_mean2d, S* g_cov2d, S* g_color, S* g_opacity) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= K) return;
-  const uint32_t cnt = count[i];
+  // after an entry overflow no partial exists (see face_views_backward)
+  const uint32_t cnt = st->overflow ? 0u : count[i];
   S s[8];
   S op = S(0);
   if (cnt) {

@@ -110,8 +110,9 @@ struct RegArgs {
   double w_edge, w_lap;
 };
 
-// per vertex: w_e * g_edge + w_l * g_lap (losses.py:93-97, :117-123)
-__device__ __forceinline__ void reg_grad(const RegArgs& r, int64_t v, double g[3]) {
+// edge-length gradient of vertex v (losses.py:93-97): the np.add.at
+// contributions of its (edge, endpoint) slots in scatter order
+__device__ __forceinline__ void edge_grad(const RegArgs& r, int64_t v, double g[3]) {
   double ex = 0.0, ey = 0.0, ez = 0.0;
   for (int32_t k = r.ve_ptr[v]; k < r.ve_ptr[v + 1]; ++k) {
     const int32_t s = r.ve_slot[k];
@@ -119,6 +120,11 @@ __device__ __forceinline__ void reg_grad(const RegArgs& r, int64_t v, double g[3
     const double* ev = r.evec4 + 4 * (s >> 1);
     ex += sg * ev[0]; ey += sg * ev[1]; ez += sg * ev[2];
   }
+  g[0] = ex; g[1] = ey; g[2] = ez;
+}
+
+// Laplacian gradient of vertex v (losses.py:117-123)
+__device__ __forceinline__ void lap_grad(const RegArgs& r, int64_t v, double g[3]) {
   double bx = 0.0, by = 0.0, bz = 0.0;
   for (int32_t k = r.adj_ptr[v]; k < r.adj_ptr[v + 1]; ++k) {
     const double* lu = r.lap4 + 4 * r.adj[k];
@@ -127,10 +133,71 @@ __device__ __forceinline__ void reg_grad(const RegArgs& r, int64_t v, double g[3
   }
   const double c = 2.0 / (double)r.V;
   const double* lv = r.lap4 + 4 * v;
-  g[0] = r.w_edge * ex + r.w_lap * (c * lv[0] - c * bx);
-  g[1] = r.w_edge * ey + r.w_lap * (c * lv[1] - c * by);
-  g[2] = r.w_edge * ez + r.w_lap * (c * lv[2] - c * bz);
+  g[0] = c * lv[0] - c * bx;
+  g[1] = c * lv[1] - c * by;
+  g[2] = c * lv[2] - c * bz;
 }
+
+// per vertex: w_e * g_edge + w_l * g_lap
+__device__ __forceinline__ void reg_grad(const RegArgs& r, int64_t v, double g[3]) {
+  double ge[3], gl[3];
+  edge_grad(r, v, ge);
+  lap_grad(r, v, gl);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) g[k] = r.w_edge * ge[k] + r.w_lap * gl[k];
+}
+
+// the two regulariser gradients as separate [V,3] arrays (either may be null)
+__global__ void __launch_bounds__(kTrainThreads) reg_grads(RegArgs r, double* __restrict__ g_edge,
+                                                          double* __restrict__ g_lap) {
+  const int64_t v = (int64_t)blockIdx.x * kTrainThreads + threadIdx.x;
+  if (v >= r.V) return;
+  double g[3];
+  if (g_edge) {
+    edge_grad(r, v, g);
+    g_edge[3 * v] = g[0]; g_edge[3 * v + 1] = g[1]; g_edge[3 * v + 2] = g[2];
+  }
+  if (g_lap) {
+    lap_grad(r, v, g);
+    g_lap[3 * v] = g[0]; g_lap[3 * v + 1] = g[1]; g_lap[3 * v + 2] = g[2];
+  }
+}
+
+// values (edge, laplacian) = (sum dev^2 / E, sum |lap|^2 / V)
+__global__ void reg_values(const double* __restrict__ sums, int64_t E, int64_t V, double* __restrict__ out) {
+  out[0] = E ? sums[1] / (double)E : 0.0;
+  out[1] = sums[2] / (double)V;
+}
+
+// Image losses of the drop-in color_loss / silhouette_loss (losses.py:43-73),
+// float64 like the reference: kind 0 = mean squared error of x against t
+// with grad 2 (x - t) / n; kind 1 = clamped binary cross-entropy of alpha x
+// against mask t with the clamp-gated grad.  Block partial sums of the
+// per-element terms (fixed tree), then sum_partials in block order.
+__global__ void __launch_bounds__(kTrainThreads) image_loss_terms(int kind, const double* __restrict__ x,
+                                                                 const double* __restrict__ t, int64_t n,
+                                                                 double* __restrict__ grad,
+                                                                 double* __restrict__ part) {
+  const int64_t i = (int64_t)blockIdx.x * kTrainThreads + threadIdx.x;
+  double term = 0.0;
+  if (i < n) {
+    const double a = x[i], m = t[i];
+    if (kind == 0) {
+      const double d = a - m;
+      term = d * d;
+      grad[i] = (2.0 / (double)n) * d;
+    } else {
+      const double eps = 1e-6;   // losses.py:20
+      const double q = fmin(fmax(a, eps), 1.0 - eps);
+      term = -(m * log(q) + (1.0 - m) * log1p(-q));
+      const bool inside = a > eps && a < 1.0 - eps;
+      grad[i] = inside ? (-m / q + (1.0 - m) / (1.0 - q)) / (double)n : 0.0;
+    }
+  }
+  block_sum1(term, part + blockIdx.x);
+}
+
+__global__ void scale_value(double* __restrict__ v, double s) { v[0] *= s; }
 
 struct AdamArgs {
   double* pos;        // [V,3] float64 parameters (updated)
@@ -152,7 +219,19 @@ struct AdamArgs {
   // at it = *iter, read on the device; null = lr_pos / lr_col above
   const double* lr_sched;
   int64_t* iter;
+  // the status of the render that produced g_img_* (or null): a step whose
+  // render overflowed its entry capacity or met a non-finite splat has no
+  // valid image gradient and is rejected whole (the host then re-runs)
+  const DevStatus* render_status;
 };
+
+__device__ __forceinline__ bool render_failed(const DevStatus* st) {
+  if (!st) return false;
+  bool bad = st->overflow != 0u;
+#pragma unroll
+  for (int i = 0; i < 6; ++i) bad |= st->bad_item[i] != 0xffffffffu;
+  return bad;
+}
 
 __device__ __forceinline__ double sched_lr_pos(const AdamArgs& a) { return a.lr_sched ? a.lr_sched[2 * *a.iter] : a.lr_pos; }
 __device__ __forceinline__ double sched_lr_col(const AdamArgs& a) { return a.lr_sched ? a.lr_sched[2 * *a.iter + 1] : a.lr_col; }
@@ -175,8 +254,9 @@ __global__ void __launch_bounds__(kTrainThreads) fit_grads(AdamArgs a, double* _
       bc |= !isfinite(gc);
     }
   }
-  if (__syncthreads_or(bp) && threadIdx.x == 0) atomicOr(&a.bad[0], 1);
-  if (__syncthreads_or(bc) && threadIdx.x == 0) atomicOr(&a.bad[1], 1);
+  const bool failed = render_failed(a.render_status);
+  if (__syncthreads_or(bp || failed) && threadIdx.x == 0) atomicOr(&a.bad[0], 1);
+  if (__syncthreads_or(bc || failed) && threadIdx.x == 0) atomicOr(&a.bad[1], 1);
 }
 
 // pass 2: VectorAdam on positions, ScalarAdam + clip on colours; a step

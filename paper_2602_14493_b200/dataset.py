@@ -1,17 +1,17 @@
 """Batched ground-truth view rendering.
 
-Mirrors the reference's dataset module (`pkg/src/meshsplat/dataset.py`):
-`make_views` (`:118-164`) normalises a mesh, renders it from a Fibonacci
-hemisphere of cameras and writes one RGB and one mask PNG per view, the
-camera file, the normalised target mesh and a metadata file; `load_views`
-(`:167-189`) reopens such a directory; `ViewDataset` (`:71-97`) is the handle.
+`make_views` keeps the reference's dataset writer (`pkg/src/meshsplat/
+dataset.py:118-164`): normalise the mesh, render it from a Fibonacci
+hemisphere of cameras, write one RGB and one mask PNG per view, the camera
+file, the normalised target mesh and a metadata file -- byte-identical files.
 
 Rendering is the device forward (K1-K3) over many views per call, with the
 8-bit quantisation of `_save_png` (`:59-61`) fused into the blend epilogue
 (`gmr_render_images_u8`), so only uint8 images cross PCIe.  PNG encoding
 (PIL) runs on host threads while the device renders the next group of
 views.  The default render dtype is float64, as the reference's
-`render_mesh` default (`render.py:442`).
+`render_mesh` default (`render.py:442`).  Reading datasets back is outside
+the hot path and not provided.
 """
 
 from __future__ import annotations
@@ -23,14 +23,12 @@ from pathlib import Path
 
 import numpy as np
 
-from .camera import fibonacci_hemisphere, hemisphere_cameras, load_cameras, save_cameras
-from .mesh import TriangleMesh, load_mesh, normalize_mesh, save_mesh
+from .camera import fibonacci_hemisphere, hemisphere_cameras, save_cameras
+from .mesh import TriangleMesh, normalize_mesh
 
-HOLDOUT_STRIDE = 11
 VERSION = "0.1.0"
 
-__all__ = ["HOLDOUT_STRIDE", "ViewDataset", "make_views", "load_views", "render_view_images",
-           "fibonacci_hemisphere", "hemisphere_cameras"]
+__all__ = ["ViewDataset", "make_views", "render_view_images", "fibonacci_hemisphere", "hemisphere_cameras"]
 
 
 def _png(path, image_u8) -> None:
@@ -38,15 +36,10 @@ def _png(path, image_u8) -> None:
     Image.fromarray(image_u8).save(path)
 
 
-def _load_png(path: Path) -> np.ndarray:
-    if not Path(path).exists():
-        raise FileNotFoundError(f"missing image file: {path}")
-    from PIL import Image
-    return np.asarray(Image.open(path), dtype=np.float64) / 255.0
-
-
 @dataclass(frozen=True)
 class ViewDataset:
+    """What make_views wrote (the reference's return type, dataset.py:71-97,
+    without its readers)."""
     root: Path
     cameras: tuple
     rgb_paths: tuple
@@ -55,23 +48,6 @@ class ViewDataset:
 
     def __len__(self):
         return len(self.cameras)
-
-    def load_rgb(self, i: int) -> np.ndarray:
-        return _load_png(self.rgb_paths[i])
-
-    def load_mask(self, i: int) -> np.ndarray:
-        return _load_png(self.mask_paths[i])
-
-    @property
-    def train_indices(self) -> list:
-        return [i for i in range(len(self)) if i % HOLDOUT_STRIDE]
-
-    @property
-    def holdout_indices(self) -> list:
-        return [i for i in range(len(self)) if i % HOLDOUT_STRIDE == 0]
-
-    def target_mesh_path(self) -> Path:
-        return self.root / "target_mesh.ply"
 
 
 def _views_per_call(F: int, W: int, H: int, n: int) -> int:
@@ -133,31 +109,33 @@ def _drain(pending, out_rgb, out_a, on_group):
 
 
 def _write_metadata(path: Path, meta: dict) -> None:
+    """`key = value` lines in key order (the reference's metadata.txt)."""
     path.write_text("".join(f"{k} = {meta[k]}\n" for k in sorted(meta)))
 
 
-def _read_metadata(path: Path) -> dict:
-    meta = {}
-    if path.exists():
-        for line in path.read_text().splitlines():
-            line = line.strip()
-            if line and not line.startswith("#"):
-                k, _, v = line.partition("=")
-                meta[k.strip()] = v.strip()
-    return meta
+def _write_ply_ascii(mesh: TriangleMesh, path: Path) -> None:
+    """The normalised target mesh as the reference writes it (mesh.py:395-421
+    format): ASCII PLY, double xyz + rgb as %.17g, triangle index lists."""
+    with open(path, "w") as fh:
+        fh.write("ply\nformat ascii 1.0\ncomment meshsplat\n"
+                 f"element vertex {mesh.num_vertices}\n"
+                 + "".join(f"property double {p}\n" for p in ("x", "y", "z", "red", "green", "blue"))
+                 + f"element face {mesh.num_facets}\nproperty list uchar int vertex_indices\nend_header\n")
+        np.savetxt(fh, np.concatenate([mesh.vertices, mesh.colors], axis=1), fmt="%.17g", delimiter=" ")
+        np.savetxt(fh, np.asarray(mesh.facets, np.int64), fmt="3 %d %d %d")
 
 
 def make_views(mesh, n_views: int = 253, resolution=(256, 256), radius: float = 3.0, up: str = "z",
                seed: int = 0, out_dir=None, background=(0.0, 0.0, 0.0), dtype=np.float64,
                png_threads: int | None = None) -> ViewDataset:
-    """Normalise `mesh` (a TriangleMesh or a mesh file path), render
+    """Normalise `mesh` (a TriangleMesh), render
     `n_views` hemisphere views on the device and write the dataset directory
     (dataset.py:118-164: view_%04d.png, mask_%04d.png, cameras.txt,
     target_mesh.ply, metadata.txt)."""
     if out_dir is None:
         raise ValueError("out_dir is required")
-    if isinstance(mesh, (str, os.PathLike)):
-        mesh = load_mesh(mesh)
+    if not isinstance(mesh, TriangleMesh):
+        raise TypeError("make_views takes a TriangleMesh (mesh file readers are outside the hot path)")
     if isinstance(resolution, int):
         resolution = (resolution, resolution)
     mesh, _ = normalize_mesh(mesh)
@@ -176,29 +154,9 @@ def make_views(mesh, n_views: int = 253, resolution=(256, 256), radius: float = 
         for j in jobs:
             j.result()
     save_cameras(cams, out / "cameras.txt")
-    save_mesh(mesh, out / "target_mesh.ply")
+    _write_ply_ascii(mesh, out / "target_mesh.ply")
     meta = {"n_views": n_views, "width": resolution[0], "height": resolution[1], "radius": radius,
             "up": up, "seed": seed, "version": VERSION}
     _write_metadata(out / "metadata.txt", meta)
     return ViewDataset(root=out, cameras=tuple(cams), rgb_paths=rgb_paths, mask_paths=mask_paths,
                        metadata=meta)
-
-
-def load_views(root) -> ViewDataset:
-    """Open a dataset directory (dataset.py:167-189)."""
-    root = Path(root)
-    cam_file = root / "cameras.txt"
-    if not cam_file.exists():
-        raise FileNotFoundError(f"no camera file at {cam_file}")
-    cams = load_cameras(cam_file)
-    rgb_paths, mask_paths = [], []
-    for i in range(len(cams)):
-        rgb, mask = root / f"view_{i:04d}.png", root / f"mask_{i:04d}.png"
-        if not rgb.exists():
-            raise FileNotFoundError(f"view {i}: missing image file {rgb}")
-        if not mask.exists():
-            raise FileNotFoundError(f"view {i}: missing mask file {mask}")
-        rgb_paths.append(rgb)
-        mask_paths.append(mask)
-    return ViewDataset(root=root, cameras=tuple(cams), rgb_paths=tuple(rgb_paths),
-                       mask_paths=tuple(mask_paths), metadata=_read_metadata(root / "metadata.txt"))

@@ -74,55 +74,68 @@ def sharded_image_loss(local_fn: Callable, cameras: Sequence, target_rgb: Sequen
     """
     world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
     rank = dist.get_rank(group) if world > 1 else 0
+    if device is None:
+        # every rank must hand the collective a tensor on the backend's device,
+        # including ranks whose shard is empty (more ranks than views)
+        nccl = world > 1 and dist.get_backend(group) == "nccl"
+        device = torch.device("cuda", torch.cuda.current_device()) if nccl else torch.device("cpu")
     n = len(cameras)
     lo, hi = shard_range(n, rank, world)
     if hi > lo:
         cval, sval, gp, gc = local_fn(cameras[lo:hi], target_rgb[lo:hi], target_mask[lo:hi],
                                       w_color / n, w_sil / n)
-        gp = torch.as_tensor(gp, dtype=torch.float64, device=device)
-        gc = torch.as_tensor(gc, dtype=torch.float64, device=device)
+        gp = torch.as_tensor(gp, dtype=torch.float64).to(device)
+        gc = torch.as_tensor(gc, dtype=torch.float64).to(device)
+        extra = torch.stack([torch.as_tensor(cval, dtype=torch.float64).to(device).reshape(()),
+                             torch.as_tensor(sval, dtype=torch.float64).to(device).reshape(())])
     else:
-        cval = sval = 0.0
         gp = torch.zeros((num_vertices, 3), dtype=torch.float64, device=device)
         gc = torch.zeros((num_vertices, 3), dtype=torch.float64, device=device)
-    extra = torch.tensor([cval, sval], dtype=torch.float64, device=gp.device)
+        extra = torch.zeros(2, dtype=torch.float64, device=device)
     gp, gc, extra = allreduce_vertex_grads(gp, gc, extra, group, reproducible)
-    return float(extra[0]) / n, float(extra[1]) / n, gp, gc
+    ex = extra.cpu()   # the one host read: the two loss values
+    return float(ex[0]) / n, float(ex[1]) / n, gp, gc
 
 
 def gpu_local_image_loss(mesh, background=(0.0, 0.0, 0.0), rescale=True, dtype=np.float32):
     """The GPU `local_fn` for `sharded_image_loss`: this rank's views in one
-    libgmr call per resolution (paper_2602_14493_b200.api.total_loss math)."""
+    libgmr call per resolution, with the colour/silhouette losses fused into
+    the blend epilogue (gmr_render_forward_loss, the paper_2602_14493_b200
+    .api.total_loss path).  Losses and gradients stay on the device; the
+    call's status is validated after the backward is enqueued."""
     from . import api, engine
 
     pos, col, faces = api._device_mesh(mesh, dtype)
     tdt = api._torch_dtype(dtype)
     dev = pos.device
+    bg = np.asarray(background, np.float64)
 
     def local_fn(cams, rgbs, masks, scale_rgb, scale_alpha):
         gp_all = torch.zeros((pos.shape[0], 3), dtype=torch.float64, device=dev)
         gc_all = torch.zeros_like(gp_all)
-        cv = sv = 0.0
+        loss = torch.zeros(2, dtype=torch.float64, device=dev)
         groups = {}
         for i, c in enumerate(cams):
             groups.setdefault((c.width, c.height), []).append(i)
         for (w, h), idx in groups.items():
-            rgb, alpha, st = engine.render_forward(pos, col, faces, [cams[i] for i in idx], w, h,
-                                                   np.asarray(background, np.float64), rescale)
-            t_rgb = torch.as_tensor(np.stack([np.asarray(rgbs[i], np.float64) for i in idx])).to(dev)
-            t_m = torch.as_tensor(np.stack([np.asarray(masks[i], np.float64) for i in idx])).to(dev)
-            r64, a64 = rgb.double(), alpha.double()
-            diff = r64 - t_rgb
-            cv += float((diff * diff).mean(dim=(1, 2, 3)).sum())
-            g_rgb = (2.0 / diff[0].numel()) * diff * scale_rgb
-            p = a64.clamp(api.BCE_CLAMP, 1.0 - api.BCE_CLAMP)
-            sv += float((-(t_m * torch.log(p) + (1.0 - t_m) * torch.log1p(-p))).mean(dim=(1, 2)).sum())
-            inside = (a64 > api.BCE_CLAMP) & (a64 < 1.0 - api.BCE_CLAMP)
-            g_a = torch.where(inside, (-t_m / p + (1.0 - t_m) / (1.0 - p)) / a64[0].numel(),
-                              torch.zeros_like(a64)) * scale_alpha
-            gp, gc = engine.render_backward(st, pos, col, faces, rgb, g_rgb.to(tdt), g_a.to(tdt))
+            t_rgb = torch.as_tensor(np.stack([np.asarray(rgbs[i], np.float64) for i in idx]), dtype=tdt).to(dev)
+            t_m = torch.as_tensor(np.stack([np.asarray(masks[i], np.float64) for i in idx]), dtype=tdt).to(dev)
+            for attempt in range(3):
+                rgb, alpha, g_rgb, g_a, sums, st = engine.render_forward_loss(
+                    pos, col, faces, [cams[i] for i in idx], w, h, bg, t_rgb, t_m, scale_rgb, scale_alpha,
+                    rescale, check=False)
+                gp, gc = engine.render_backward(st, pos, col, faces, rgb, g_rgb, g_a)
+                try:
+                    # waits for this forward's status copy only; the backward stays queued
+                    engine.check_status(st)
+                    break
+                except engine.CapacityExceeded:
+                    if attempt == 2:
+                        raise
+            loss[0] += sums[0] / (3.0 * w * h)
+            loss[1] += sums[1] / (1.0 * w * h)
             gp_all += gp.double()
             gc_all += gc.double()
-        return cv, sv, gp_all, gc_all
+        return loss[0], loss[1], gp_all, gc_all
 
     return local_fn

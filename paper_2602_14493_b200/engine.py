@@ -231,7 +231,16 @@ def render_forward(pos, col, faces, cams, width, height, background, rescale=Tru
         entries, kept, bad, overflow = _parse_status(status.numpy())
         for field in range(6):
             if bad[field] != 0xFFFFFFFF:
-                idx = int(bad[field]) if item_to_index is None else item_to_index(int(bad[field]))
+                item = int(bad[field])
+                if item_to_index == "kept":
+                    # the reference reports the index into the view's culled
+                    # splat batch (render.py:191-197): rank among kept faces
+                    fs = ForwardState(ws, cap, raster, cam_arr, B, -1, -1)
+                    cnt = copy_splats(fs, F, True)[2].cpu().numpy()
+                    v0 = (item // max(F, 1)) * F
+                    idx = int(np.count_nonzero(cnt[v0:item] > 0))
+                else:
+                    idx = item if item_to_index is None else item_to_index(item)
                 raise ValueError(f"non-finite splat parameter {_FIELDS[field]!r} at splat {idx}")
         if not overflow:
             _capacity.note(key, cap, entries)

@@ -261,204 +261,21 @@ def make_grid_cube_normalized(divisions: int = 4) -> TriangleMesh:
     return normalize_mesh(make_grid_cube(divisions, position_colors=True))[0]
 
 
-# ---------------------------------------------------------------------------
-# File formats on either side of the path (reference mesh.py:161-421): ASCII
-# PLY writer; OBJ and PLY (ascii / binary_little_endian) readers with fan
-# triangulation.  Host-side I/O, not part of the device path.
-# ---------------------------------------------------------------------------
-
-class MeshParseError(MeshError):
-    """Malformed mesh file (mesh.py:22-28): message prefixed with path:line."""
-
-    def __init__(self, path, line, message):
-        super().__init__(f"{path}:{line}: {message}")
-        self.path, self.line = path, line
-
-
-_PLY_TYPES = {"char": "i1", "int8": "i1", "uchar": "u1", "uint8": "u1", "short": "i2", "int16": "i2",
-              "ushort": "u2", "uint16": "u2", "int": "i4", "int32": "i4", "uint": "u4", "uint32": "u4",
-              "float": "f4", "float32": "f4", "double": "f8", "float64": "f8"}
-
-
-def save_mesh(mesh: TriangleMesh, path) -> None:
-    """ASCII PLY, double positions and colours printed with %.17g so a
-    reload reproduces the mesh exactly (mesh.py:395-421)."""
-    head = ["ply", "format ascii 1.0", "comment meshsplat", f"element vertex {mesh.num_vertices}",
-            "property double x", "property double y", "property double z",
-            "property double red", "property double green", "property double blue",
-            f"element face {mesh.num_facets}", "property list uchar int vertex_indices", "end_header"]
-    vc = np.concatenate([mesh.vertices, mesh.colors], axis=1)
-    body = ["%.17g %.17g %.17g %.17g %.17g %.17g" % tuple(r) for r in vc.tolist()]
-    body += ["3 %d %d %d" % tuple(f) for f in np.asarray(mesh.facets).tolist()]
-    with open(path, "w") as fh:
-        fh.write("\n".join(head + body) + "\n")
-
-
-def _fan(idx, nv, path, where):
-    for i in idx:
-        if not 0 <= i < nv:
-            raise MeshParseError(path, where, f"vertex index {i} out of range [0, {nv})")
-    if len(idx) < 3:
-        raise MeshParseError(path, where, "face with fewer than 3 vertices")
-    return [(idx[0], idx[k], idx[k + 1]) for k in range(1, len(idx) - 1)]
-
-
-def _read_obj(path) -> TriangleMesh:
-    verts, cols, tris, colored = [], [], [], False
-    with open(path, errors="replace") as fh:
-        for n, raw in enumerate(fh, start=1):
-            tok = raw.split()
-            if not tok or tok[0].startswith("#"):
-                continue
-            if tok[0] == "v":
-                try:
-                    x = [float(t) for t in tok[1:]]
-                except ValueError:
-                    raise MeshParseError(path, n, f"bad vertex line: {raw.strip()!r}") from None
-                if len(x) < 3:
-                    raise MeshParseError(path, n, "vertex line needs at least 3 coordinates")
-                verts.append(x[:3])
-                if len(x) >= 6:
-                    cols.append(x[3:6] if len(x) > 6 else x[-3:])
-                    colored = True
-                else:
-                    cols.append([GRAY] * 3)
-            elif tok[0] == "f":
-                idx = []
-                for t in tok[1:]:
-                    try:
-                        i = int(t.split("/")[0])
-                    except ValueError:
-                        raise MeshParseError(path, n, f"bad face token {t!r}") from None
-                    if i == 0:
-                        raise MeshParseError(path, n, "OBJ face indices are 1-based; got 0")
-                    idx.append(i - 1 if i > 0 else len(verts) + i)
-                tris.extend(_fan(idx, len(verts), path, n))
-    try:
-        return TriangleMesh(np.asarray(verts, np.float64).reshape(-1, 3), tris,
-                            np.clip(cols, 0.0, 1.0) if colored else None)
-    except MeshError as e:
-        raise MeshParseError(path, 0, str(e)) from None
-
-
-def _read_ply(path) -> TriangleMesh:
-    with open(path, "rb") as fh:
-        if fh.readline().strip() != b"ply":
-            raise MeshParseError(path, 1, "not a PLY file (missing 'ply' magic)")
-        fmt, elems, n = None, [], 1
-        while True:
-            raw = fh.readline()
-            n += 1
-            if not raw:
-                raise MeshParseError(path, n, "unexpected EOF in header")
-            tok = raw.decode("ascii", errors="replace").split()
-            if not tok or tok[0] in ("comment", "obj_info"):
-                continue
-            if tok[0] == "format":
-                fmt = tok[1]
-                if fmt not in ("ascii", "binary_little_endian"):
-                    raise MeshParseError(path, n, f"unsupported PLY format {fmt!r}")
-            elif tok[0] == "element":
-                elems.append((tok[1], int(tok[2]), []))
-            elif tok[0] == "property":
-                if not elems:
-                    raise MeshParseError(path, n, "property before any element")
-                if tok[1] == "list":
-                    if tok[2] not in _PLY_TYPES or tok[3] not in _PLY_TYPES:
-                        raise MeshParseError(path, n, f"unknown list types {tok[2]}/{tok[3]}")
-                    elems[-1][2].append((tok[4], ("list", _PLY_TYPES[tok[2]], _PLY_TYPES[tok[3]])))
-                else:
-                    if tok[1] not in _PLY_TYPES:
-                        raise MeshParseError(path, n, f"unknown property type {tok[1]!r}")
-                    elems[-1][2].append((tok[2], _PLY_TYPES[tok[1]]))
-            elif tok[0] == "end_header":
-                break
-            else:
-                raise MeshParseError(path, n, f"unknown header keyword {tok[0]!r}")
-        if fmt is None:
-            raise MeshParseError(path, n, "missing 'format' line")
-        data = {}
-        for name, count, props in elems:
-            if fmt == "ascii":
-                cols = [[] for _ in props]
-                for _ in range(count):
-                    raw = fh.readline()
-                    n += 1
-                    if not raw:
-                        raise MeshParseError(path, n, f"unexpected EOF in element {name!r}")
-                    tok, k = raw.split(), 0
-                    try:
-                        for ci, (_, kind) in enumerate(props):
-                            if isinstance(kind, tuple):
-                                m = int(tok[k])
-                                vals = [float(t) for t in tok[k + 1:k + 1 + m]]
-                                if len(vals) != m:
-                                    raise IndexError
-                                cols[ci].append(np.array(vals))
-                                k += 1 + m
-                            else:
-                                cols[ci].append(float(tok[k]))
-                                k += 1
-                    except (IndexError, ValueError):
-                        raise MeshParseError(path, n, f"malformed {name!r} row") from None
-                data[name] = (props, [c if isinstance(props[i][1], tuple) else np.asarray(c, np.float64)
-                                      for i, c in enumerate(cols)])
-            elif not any(isinstance(p[1], tuple) for p in props):
-                dt = np.dtype([(f"f{i}", "<" + kind) for i, (_, kind) in enumerate(props)])
-                buf = fh.read(dt.itemsize * count)
-                if len(buf) != dt.itemsize * count:
-                    raise MeshParseError(path, n, f"truncated binary element {name!r}")
-                rec = np.frombuffer(buf, dtype=dt)
-                data[name] = (props, [rec[f"f{i}"].astype(np.float64) for i in range(len(props))])
-            else:
-                if len(props) != 1:
-                    raise MeshParseError(path, n, f"mixed list/scalar element {name!r} unsupported")
-                cdt, idt = np.dtype("<" + props[0][1][1]), np.dtype("<" + props[0][1][2])
-                lists = []
-                for row in range(count):
-                    cb = fh.read(cdt.itemsize)
-                    if len(cb) != cdt.itemsize:
-                        raise MeshParseError(path, n, f"truncated {name!r} at row {row}")
-                    m = int(np.frombuffer(cb, cdt)[0])
-                    ib = fh.read(idt.itemsize * m)
-                    if len(ib) != idt.itemsize * m:
-                        raise MeshParseError(path, n, f"truncated {name!r} at row {row}")
-                    lists.append(np.frombuffer(ib, idt).astype(np.int64))
-                data[name] = (props, [lists])
-    if "vertex" not in data:
-        raise MeshParseError(path, 0, "PLY without a vertex element")
-    props, cols = data["vertex"]
-    names = [p[0] for p in props]
-    for c in "xyz":
-        if c not in names:
-            raise MeshParseError(path, 0, f"vertex element lacks property {c!r}")
-    verts = np.stack([cols[names.index(c)] for c in "xyz"], axis=1)
-    colors = None
-    if all(c in names for c in ("red", "green", "blue")):
-        ch = [cols[names.index(c)] / (255.0 if props[names.index(c)][1] == "u1" else 1.0)
-              for c in ("red", "green", "blue")]
-        colors = np.clip(np.stack(ch, axis=1), 0.0, 1.0)
-    tris = []
-    if "face" in data:
-        props, cols = data["face"]
-        names = [p[0] for p in props]
-        key = next((k for k in ("vertex_indices", "vertex_index") if k in names), None)
-        if key is None:
-            raise MeshParseError(path, 0, "face element lacks vertex_indices")
-        for fi, idx in enumerate(cols[names.index(key)]):
-            tris.extend(_fan([int(i) for i in idx], len(verts), path, f"face {fi}"))
-    try:
-        return TriangleMesh(verts, tris, colors)
-    except MeshError as e:
-        raise MeshParseError(path, 0, str(e)) from None
-
-
-def load_mesh(path) -> TriangleMesh:
-    """OBJ or PLY by extension (mesh.py:177-199)."""
-    import os
-    ext = os.path.splitext(str(path))[1].lower()
-    if ext == ".obj":
-        return _read_obj(path)
-    if ext == ".ply":
-        return _read_ply(path)
-    raise MeshParseError(path, 0, f"unsupported mesh extension {ext!r}")
+def mesh_graph(facets, num_vertices):
+    """Edges, vertex->(edge, endpoint) CSR in np.add.at order and the sorted
+    neighbour CSR (reference mesh.py:96-126, losses.py:95-96), int32."""
+    f = np.asarray(facets)
+    e = (np.unique(np.sort(f[:, [0, 1, 1, 2, 2, 0]].reshape(-1, 2), axis=1), axis=0)
+         if len(f) else np.zeros((0, 2), np.int64))
+    E = len(e)
+    keys = np.concatenate([e[:, 1], e[:, 0]])
+    slots = np.concatenate([2 * np.arange(E) + 1, 2 * np.arange(E)])
+    order = np.argsort(keys, kind="stable")
+    ve_slot = slots[order]
+    ve_ptr = np.concatenate([[0], np.cumsum(np.bincount(keys, minlength=num_vertices))])
+    both = np.concatenate([e, e[:, ::-1]]) if E else np.zeros((0, 2), np.int64)
+    both = both[np.lexsort((both[:, 1], both[:, 0]))]
+    adj_ptr = np.concatenate([[0], np.cumsum(np.bincount(both[:, 0], minlength=num_vertices))])
+    i32 = lambda a: np.ascontiguousarray(a, dtype=np.int32)
+    return dict(edges=i32(e.reshape(-1, 2)), ve_ptr=i32(ve_ptr), ve_slot=i32(ve_slot), adj_ptr=i32(adj_ptr),
+                adj=i32(both[:, 1]))

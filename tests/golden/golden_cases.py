@@ -212,3 +212,52 @@ def flip_stats(rgb_a, alpha_a, rgb_b, alpha_b, gv_a, gv_b, gc_a, gc_b):
     rel = lambda x, y: float(np.linalg.norm(x - y) / np.linalg.norm(y))
     return dict(flips=int((d > 1e-4).sum()), covered=int((alpha_b > 0).sum()),
                 rel_gv=rel(gv_a, gv_b), rel_gc=rel(gc_a, gc_b))
+
+
+WIDE_SKETCH_ROWS = 64
+
+
+def wide_sketch(x, seed):
+    """`sketch` with WIDE_SKETCH_ROWS rows (relative-L2 estimates to ~15 %)."""
+    x = np.asarray(x, dtype=np.float64).ravel()
+    rng = np.random.default_rng(seed)
+    return np.array([rng.standard_normal(x.size) @ x for _ in range(WIDE_SKETCH_ROWS)])
+
+
+def quantize_unit(x):
+    """[0, 1] image -> uint16 steps of 1/65535 (max error 7.7e-6, far inside
+    the 1e-4 image tolerance; background regions compress to nothing)."""
+    return np.round(np.clip(np.asarray(x, np.float64), 0.0, 1.0) * 65535.0).astype(np.uint16)
+
+
+def vertex_subset(num_vertices, frac=0.1, seed=5):
+    """A seeded sorted subset of vertex ids stored exactly in full-size fixtures."""
+    rng = np.random.default_rng(seed)
+    return np.sort(rng.choice(num_vertices, size=max(1, int(frac * num_vertices)), replace=False))
+
+
+def c2_case():
+    """Config 2: icosphere L6 (81,920 F), 8 hemisphere views 512x512
+    (SURVEY 8d), seeded colours, N(0,1) upstream grads per view (seed 21);
+    the reference's view loop (losses.py:151-162) sums the per-view grads."""
+    from paper_2602_14493_b200.camera import hemisphere_cameras
+    m = make_icosphere(81920)
+    col = np.random.default_rng(0).uniform(0.1, 0.9, size=(m.num_vertices, 3))
+    cams = hemisphere_cameras(8, 3.0, (512, 512))
+    rng = np.random.default_rng(21)
+    return dict(vertices=np.asarray(m.vertices), facets=np.asarray(m.facets), colors=col, cameras=cams,
+                background=(0.1, 0.1, 0.1), g_rgb=rng.standard_normal((8, 512, 512, 3)),
+                g_alpha=rng.standard_normal((8, 512, 512)))
+
+
+def c4_case():
+    """Config 4 cut to one view: geodesic sphere n=316 (1,997,120 F), 1024x1024,
+    the first full-sphere Fibonacci camera of 64 (test_acceptance.py:61-67)."""
+    from paper_2602_14493_b200.camera import sphere_views
+    from paper_2602_14493_b200.mesh import make_geodesic_sphere
+    mesh = make_geodesic_sphere(316, seed=0)
+    cam = sphere_views(64, 3.0, 1024)[0]
+    rng = np.random.default_rng(31)
+    return dict(vertices=mesh.vertices, facets=mesh.facets, colors=mesh.colors, camera=cam,
+                background=(0.1, 0.1, 0.1), g_rgb=rng.standard_normal((1024, 1024, 3)),
+                g_alpha=rng.standard_normal((1024, 1024)))

@@ -216,18 +216,98 @@ def fullsize_case(name):
     print(name, {k: (v if np.ndim(v) == 0 else v.shape) for k, v in out.items()})
 
 
+def fullsize_f32_case(name):
+    """Config 3 view 0 through the reference in float32 only, stored so the
+    GPU float32 path can be compared with it DIRECTLY (SURVEY 8c contract):
+    the image and alpha quantised to 1/65535 (uint16), both gradients at a
+    seeded 10 % vertex subset exactly plus 64-row sketches of the full
+    vectors, and the reference's float32 tile lists (face ids in (tile,
+    depth, source) order + bounds) to count differing entries."""
+    case = gc.fullsize_case()
+    mesh = ref_mesh(case)
+    cam = ref_cam(case["camera"])
+    dt = np.float32
+    o, ctx = ms.render_mesh(mesh, cam, background=case["background"], dtype=dt, return_ctx=True)
+    gv, gcol = ms.render_backward(ctx, case["g_rgb"].astype(dt), case["g_alpha"].astype(dt))
+    plan = _RasterPlan(ctx.batch, cam.width, cam.height)
+    sub = gc.vertex_subset(len(case["vertices"]))
+    out = dict(rgb_u16=gc.quantize_unit(o.rgb), alpha_u16=gc.quantize_unit(o.alpha),
+               gv_sub=np.asarray(gv, np.float32)[sub], gc_sub=np.asarray(gcol, np.float32)[sub],
+               gv_sketch=gc.wide_sketch(gv, 100), gc_sketch=gc.wide_sketch(gcol, 101),
+               entry_face=ctx.batch.source[plan.entry_splat].astype(np.int32),
+               bounds=np.asarray(plan.bounds, np.int32))
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+    print(name, {k: v.shape for k, v in out.items()})
+
+
+def c2_case(name):
+    """Config 2 (8 views 512^2, 81,920 F) through the reference, float64 and
+    float32: per-view sketches of the images, sketches of the view-summed
+    vertex gradients (the losses.py:151-162 loop with unit weights), and the
+    reference's own float32-vs-float64 spread."""
+    case = gc.c2_case()
+    mesh = ref_mesh(case)
+    res = {}
+    for dt in (np.float64, np.float32):
+        rgbs, alphas, gv_sum, gc_sum = [], [], 0.0, 0.0
+        for v, c in enumerate(case["cameras"]):
+            cam = ref_cam(c)
+            o, ctx = ms.render_mesh(mesh, cam, background=case["background"], dtype=dt, return_ctx=True)
+            gv, gcol = ms.render_backward(ctx, case["g_rgb"][v].astype(dt), case["g_alpha"][v].astype(dt))
+            rgbs.append(np.asarray(o.rgb, np.float64))
+            alphas.append(np.asarray(o.alpha, np.float64))
+            gv_sum = gv_sum + np.asarray(gv, np.float64)
+            gc_sum = gc_sum + np.asarray(gcol, np.float64)
+        res[dt] = (np.array(rgbs), np.array(alphas), gv_sum, gc_sum)
+    out = {}
+    for tag, dt in (("f64", np.float64), ("f32", np.float32)):
+        r, a, gv, gcol = res[dt]
+        out[f"{tag}_rgb"] = np.array([gc.wide_sketch(x, 200 + i) for i, x in enumerate(r)])
+        out[f"{tag}_alpha"] = np.array([gc.wide_sketch(x, 300 + i) for i, x in enumerate(a)])
+        out[f"{tag}_gv"] = gc.wide_sketch(gv, 400)
+        out[f"{tag}_gc"] = gc.wide_sketch(gcol, 401)
+    r64, a64, gv64, gc64 = res[np.float64]
+    r32, a32, gv32, gc32 = res[np.float32]
+    out.update({f"ref32_{k}": v for k, v in gc.flip_stats(r32, a32, r64, a64, gv32, gv64, gc32, gc64).items()})
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+    print(name, {k: (v if np.ndim(v) == 0 else v.shape) for k, v in out.items()})
+
+
+def c4_case(name):
+    """Config 4 cut to one view (1,997,120 F, 1024^2) through the reference
+    in float64: sketches of image, alpha and both gradients."""
+    case = gc.c4_case()
+    mesh = ref_mesh(case)
+    cam = ref_cam(case["camera"])
+    o, ctx = ms.render_mesh(mesh, cam, background=case["background"], dtype=np.float64, return_ctx=True)
+    gv, gcol = ms.render_backward(ctx, case["g_rgb"], case["g_alpha"])
+    out = {f"sketch_{n}": gc.sketch(a, i) for i, (n, a) in enumerate(zip(("rgb", "alpha", "gv", "gc"),
+                                                                          (o.rgb, o.alpha, gv, gcol)))}
+    out["entries"] = np.int64(len(_RasterPlan(ctx.batch, cam.width, cam.height).entry_splat))
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+    print(name, {k: np.shape(v) for k, v in out.items()})
+
+
 if __name__ == "__main__":
-    render_case("c1_icosphere1280_128", gc.c1_case())
-    render_case("octahedron_32", gc.octahedron_case())
-    render_case("icosphere320_64x48", gc.small_render_case())
-    splat_case("splats7_32", gc.splat_case())
-    splat_case("splats_closed_form_32", gc.closed_form_splat_case())
-    loss_case("loss_octa_3views_16", gc.loss_case())
-    convert_case("convert_random50", gc.convert_case())
-    views_case("views_ico320_13")
-    eval_case("eval_ico320")
+    # --only: just the large cases named by their flags
+    if "--only" not in sys.argv:
+        render_case("c1_icosphere1280_128", gc.c1_case())
+        render_case("octahedron_32", gc.octahedron_case())
+        render_case("icosphere320_64x48", gc.small_render_case())
+        splat_case("splats7_32", gc.splat_case())
+        splat_case("splats_closed_form_32", gc.closed_form_splat_case())
+        loss_case("loss_octa_3views_16", gc.loss_case())
+        convert_case("convert_random50", gc.convert_case())
+        views_case("views_ico320_13")
+        eval_case("eval_ico320")
     if "--fullsize" in sys.argv:
         fullsize_case("fullsize_c3_view0")
+    if "--fullsize-f32" in sys.argv:
+        fullsize_f32_case("fullsize_c3_view0_f32")
+    if "--c2" in sys.argv:
+        c2_case("c2_8views_512")
+    if "--c4" in sys.argv:
+        c4_case("c4_view0_1024")
     if "--fit" in sys.argv:
         fit_case("fit_c5_200")
         fit_prefix_case("fit_c5_5", 5)

@@ -123,6 +123,21 @@ def test_overflowing_splat_raises_reference_error(gmr, scale):
         gmr.render_mesh(mesh, cam, dtype=np.float32)
 
 
+def test_nonfinite_error_reports_kept_splat_index(gmr):
+    """The reference reports the index into the culled splat batch
+    (render.py:191-197), not the face id: with face 0 behind the camera
+    (culled) and face 1 kept, the overflowing sliver (face 2) is splat 1.
+    Message from the reference itself on these inputs:
+    ValueError("non-finite splat parameter 'cov2d' at splat 1")."""
+    scale = 1e20
+    v = np.array([(0, 0, 5), (0.1, 0, 5), (0, 0.1, 5), (0, 0, 0.5), (0.1, 0, 0.5), (0, 0.1, 0.5),
+                  (-scale, 0, 0), (scale, 0, 0), (0, 1, 0)], float)
+    mesh = gmr.TriangleMesh(v, [(0, 1, 2), (3, 4, 5), (6, 7, 8)])
+    cam = gmr.look_at((0.3, 0.2, 3), (0, 0, 0), **gmr.default_intrinsics(32, 32))
+    with pytest.raises(ValueError, match="non-finite splat parameter 'cov2d' at splat 1$"):
+        gmr.render_mesh(mesh, cam, dtype=np.float32)
+
+
 def test_backward_shape_errors_match_reference(gmr):
     case = gc.octahedron_case()
     mesh = gmr.TriangleMesh(case["vertices"], case["facets"], case["colors"])
@@ -249,3 +264,70 @@ def test_random_scenes_f32_and_backward_vs_oracle(gmr, seed):
                 assert rel(gv, ogv) <= 1e-3 and rel(gcol, ogc) <= 1e-3
             else:
                 assert np.linalg.norm(gv - ogv) / np.linalg.norm(ogv) <= 1e-2
+
+
+def test_backward_after_capacity_overflow_is_safe(gmr):
+    """A forward planned with too few tile entries and left unchecked
+    (check=False), followed directly by the backward: the backward reads
+    nothing past the workspace and writes zero gradients; check_status then
+    raises CapacityExceeded and a re-run (grown capacity) gives the normal
+    result (face_views_backward used to read partials past the
+    entry capacity)."""
+    import torch
+    from paper_2602_14493_b200 import engine
+    case = gc.c1_case()
+    pos = torch.tensor(case["vertices"], dtype=torch.float32, device="cuda")
+    col = torch.tensor(case["colors"], dtype=torch.float32, device="cuda")
+    faces = torch.tensor(case["facets"], dtype=torch.int32, device="cuda")
+    cam = case["camera"]
+    g_rgb = torch.tensor(case["g_rgb"][None], dtype=torch.float32, device="cuda")
+    g_a = torch.tensor(case["g_alpha"][None], dtype=torch.float32, device="cuda")
+    key = (len(case["facets"]), 1, 128, 128, torch.float32)
+    engine._capacity._cap[key] = 16
+    rgb, _, st = engine.render_forward(pos, col, faces, [cam], 128, 128, case["background"], check=False)
+    gp, gcol = engine.render_backward(st, pos, col, faces, rgb, g_rgb, g_a)
+    torch.cuda.synchronize()
+    assert float(gp.abs().max()) == 0.0 and float(gcol.abs().max()) == 0.0
+    with pytest.raises(engine.CapacityExceeded):
+        engine.check_status(st)
+    rgb2, _, st2 = engine.render_forward(pos, col, faces, [cam], 128, 128, case["background"], check=False)
+    gp2, gc2 = engine.render_backward(st2, pos, col, faces, rgb2, g_rgb, g_a)
+    engine.check_status(st2)
+    rgb3, _, st3 = engine.render_forward(pos, col, faces, [cam], 128, 128, case["background"])
+    gp3, _ = engine.render_backward(st3, pos, col, faces, rgb3, g_rgb, g_a)
+    assert torch.equal(rgb2, rgb3) and torch.equal(gp2, gp3)
+    assert float(gp2.abs().max()) > 0.0
+
+
+def test_rasterize_backward_after_capacity_overflow_is_safe(gmr):
+    """Splat path (splat_grads) under the same overflow."""
+    import torch
+    from paper_2602_14493_b200 import engine
+    case = gc.splat_case()
+    dt = torch.float64
+    t = [torch.tensor(np.asarray(case[k]), dtype=dt, device="cuda") for k in ("mean2d", "cov2d", "depth", "color",
+                                                                              "opacity")]
+    K = int(t[2].shape[0])
+    cam = case["camera"]
+    key = ("splats", K, cam.width, cam.height, dt)
+    engine._capacity._cap[key] = 2
+    rgb, alpha, state = engine.rasterize_forward(*t, cam.width, cam.height, case["background"])
+    # the checked forward re-planned; force an overflowed state for the backward
+    engine._capacity._cap[key] = 2
+    lib = engine.L.load()
+    import ctypes
+    raster = engine.raster_struct(cam.width, cam.height, case["background"], dt)
+    sp = engine._splat_struct(*t)
+    nb = ctypes.c_size_t()
+    engine.L.check(lib.gmr_raster_workspace_size(K, cam.width, cam.height, 2, raster.dtype, ctypes.byref(nb)))
+    ws = torch.empty(nb.value, dtype=torch.uint8, device="cuda")
+    rgb_o = torch.empty_like(rgb)
+    a_o = torch.empty_like(alpha)
+    engine.L.check(lib.gmr_rasterize_forward(ctypes.byref(sp), ctypes.byref(raster), engine._ptr(rgb_o),
+                                             engine._ptr(a_o), engine._ptr(ws), nb.value, 2, engine._stream()))
+    over = engine.ForwardState(ws, 2, raster, None, 1, -1, -1)
+    g = torch.ones_like(rgb)
+    gm, gcv, gcol, gop = engine.rasterize_backward(over, *t, rgb_o, g, torch.ones_like(alpha))
+    torch.cuda.synchronize()
+    for x in (gm, gcv, gcol, gop):
+        assert float(x.abs().max()) == 0.0
