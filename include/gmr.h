@@ -12,8 +12,8 @@
  *   render.py:453-467  render_backward               gmr_render_backward (+ gmr_topology_build)
  *   render.py:272-291  rasterize                     gmr_rasterize_forward
  *   render.py:294-361  rasterize_backward            gmr_rasterize_backward
- *   render.py:103-145  project_cloud                 fused into gmr_render_forward (K1)
- *   render.py:364-402  project_cloud_backward        fused into gmr_render_backward (K5)
+ *   render.py:103-145  project_cloud                 fused into gmr_render_forward (K1); gmr_project
+ *   render.py:364-402  project_cloud_backward        fused into gmr_render_backward (K5); gmr_project_backward
  *   convert.py:313-368 convert_mesh (embed route)    gmr_convert
  *   convert.py:371-437 convert_backward              gmr_convert_backward
  *   losses.py:151-162  total_loss view loop          B views per gmr_render_* call
@@ -263,6 +263,25 @@ int gmr_render_backward(const GmrMesh* mesh, const GmrCamera* cameras, int32_t n
                         const void* grad_alpha, void* grad_positions, void* grad_colors,
                         const void* topology, void* workspace, size_t workspace_bytes,
                         int64_t entry_capacity, void* stream);
+
+/* ---- projection stage (project_cloud / project_cloud_backward) --------- */
+
+/* project_cloud (render.py:103-145) for one camera: K Gaussians (means
+ * [K,3], cov3d [K,3,3], dtype) -> per Gaussian t_cam [K,3] and depth [K]
+ * always; for Gaussians inside the depth window also mean2d [K,2], cov2d
+ * [K,2,2] (+0.3 px^2 dilation), conic [K,3] and radius [K]; kept [K] = 1
+ * where the Gaussian passes the depth window and the 3-sigma screen box
+ * (the caller compacts the kept ones in cloud order, as the reference's
+ * SplatBatch). */
+int gmr_project(const void* means, const void* cov3d, int64_t K, const GmrCamera* camera, int32_t width,
+                int32_t height, int32_t dtype, void* mean2d, void* cov2d, void* conic, void* depth, void* radius,
+                void* t_cam, uint8_t* kept, void* stream);
+/* project_cloud_backward (render.py:364-402): for K kept Gaussians (t_cam
+ * [K,3] of the forward, cov3d [K,3,3]) and upstream g_mean2d [K,2], g_cov2d
+ * [K,2,2] (general, not necessarily symmetric) -> g_mean3d [K,3], g_cov3d
+ * [K,3,3]. */
+int gmr_project_backward(const void* t_cam, const void* cov3d, int64_t K, const GmrCamera* camera, int32_t dtype,
+                         const void* g_mean2d, const void* g_cov2d, void* g_mean3d, void* g_cov3d, void* stream);
 
 /* ---- splat path (rasterize / rasterize_backward stage functions) ------ */
 

@@ -10,7 +10,8 @@ from .camera import (Camera, CameraError, default_intrinsics, fibonacci_hemisphe
                      hemisphere_cameras, look_at, sphere_views)
 from .mesh import MeshError, TriangleMesh, make_geodesic_sphere, make_icosphere, seeded_colors
 
-_API = ("RenderOutput", "RenderContext", "Splat2D", "GaussianCloud", "LossWeights", "LossReport",
+_API = ("RenderOutput", "RenderContext", "Splat2D", "SplatBatch", "GaussianCloud", "LossWeights", "LossReport",
+        "project_cloud", "project_cloud_backward",
         "render_mesh", "render_backward", "rasterize", "rasterize_backward", "convert_mesh",
         "convert_backward", "total_loss", "color_loss", "silhouette_loss", "edge_length_loss",
         "laplacian_loss", "export_gaussians", "ALPHA_CLAMP", "CONTRIB_FLOOR", "TRANSMITTANCE_STOP", "DILATION", "TILE")

@@ -249,6 +249,71 @@ def convert_mesh(mesh, path: str = "embed", rescale: bool = True) -> GaussianClo
                          opacities=np.ones(m), degenerate=degen.cpu().numpy(), path="embed", rescale=rescale)
 
 
+@dataclass
+class SplatBatch:
+    """Kept splats of one camera, in cloud order (render.py:52-73)."""
+    mean2d: np.ndarray
+    cov2d: np.ndarray
+    conic: np.ndarray
+    depth: np.ndarray
+    color: np.ndarray
+    opacity: np.ndarray
+    source: np.ndarray
+    t_cam: np.ndarray
+    radius: np.ndarray
+
+    def __len__(self):
+        return len(self.depth)
+
+
+def project_cloud(cloud, camera: Camera, dtype=np.float64) -> SplatBatch:
+    """EWA projection with depth-window and 3-sigma screen culling
+    (render.py:103-145), on the device (gmr_project)."""
+    import ctypes
+    lib = engine.L.load()
+    tdt = _torch_dtype(dtype)
+    dev = _device()
+    k = len(cloud.means)
+    means = torch.as_tensor(np.ascontiguousarray(np.asarray(cloud.means, np.float64).reshape(k, 3)), dtype=tdt).to(dev)
+    cov = torch.as_tensor(np.ascontiguousarray(np.asarray(cloud.cov3d, np.float64).reshape(k, 3, 3)), dtype=tdt).to(dev)
+    out = {n: torch.zeros(shape, dtype=tdt, device=dev) for n, shape in
+           (("mean2d", (k, 2)), ("cov2d", (k, 2, 2)), ("conic", (k, 3)), ("depth", (k,)), ("radius", (k,)),
+            ("t_cam", (k, 3)))}
+    kept = torch.zeros(k, dtype=torch.uint8, device=dev)
+    cam = engine.L.camera_struct([camera])
+    engine.L.check(lib.gmr_project(engine._ptr(means), engine._ptr(cov), k, cam, camera.width, camera.height,
+                                   engine._DT[tdt], *(engine._ptr(out[n]) for n in
+                                                      ("mean2d", "cov2d", "conic", "depth", "radius", "t_cam")),
+                                   engine._ptr(kept), engine._stream()))
+    idx = np.where(kept.cpu().numpy() > 0)[0]
+    host = {n: v.cpu().numpy()[idx] for n, v in out.items()}
+    np_dt = np.dtype(dtype)
+    return SplatBatch(color=np.asarray(cloud.colors)[idx].astype(np_dt),
+                      opacity=np.asarray(cloud.opacities)[idx].astype(np_dt), source=idx.astype(np.int64), **host)
+
+
+def project_cloud_backward(batch: SplatBatch, cloud, camera: Camera, g_mean2d, g_cov2d):
+    """Screen-space gradients of the kept splats -> (g_mean3d, g_cov3d)
+    aligned with the batch (render.py:364-402), on the device
+    (gmr_project_backward)."""
+    lib = engine.L.load()
+    np_dt = np.asarray(batch.mean2d).dtype
+    tdt = _torch_dtype(np_dt)
+    dev = _device()
+    k = len(batch)
+    t = lambda x, shape: torch.as_tensor(np.ascontiguousarray(np.asarray(x, np.float64).reshape(shape)),
+                                         dtype=tdt).to(dev)
+    tc = t(batch.t_cam, (k, 3))
+    cov = t(np.asarray(cloud.cov3d)[np.asarray(batch.source, np.int64)], (k, 3, 3))
+    gm, gc = t(g_mean2d, (k, 2)), t(g_cov2d, (k, 2, 2))
+    g3 = torch.zeros((k, 3), dtype=tdt, device=dev)
+    gcov = torch.zeros((k, 3, 3), dtype=tdt, device=dev)
+    engine.L.check(lib.gmr_project_backward(engine._ptr(tc), engine._ptr(cov), k, engine.L.camera_struct([camera]),
+                                            engine._DT[tdt], engine._ptr(gm), engine._ptr(gc), engine._ptr(g3),
+                                            engine._ptr(gcov), engine._stream()))
+    return g3.cpu().numpy(), gcov.cpu().numpy()
+
+
 EXPORT_PROPS = ("x", "y", "z", "f_dc_0", "f_dc_1", "f_dc_2", "opacity", "scale_0", "scale_1", "scale_2",
                 "rot_0", "rot_1", "rot_2", "rot_3")
 

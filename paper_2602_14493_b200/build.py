@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libgmr.so")
 SOURCES = ["gmr_capi.cu"]
-DEPS = ["gmr_capi.cu", "gmr_kernels.cuh", "gmr_common.cuh", "radix_sort.cuh", "gmr_train.cuh", "gmr_eval.cuh"]
+DEPS = ["gmr_capi.cu", "gmr_kernels.cuh", "gmr_common.cuh", "radix_sort.cuh", "gmr_train.cuh", "gmr_eval.cuh", "gmr_stage.cuh"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-warn-spills"]
 

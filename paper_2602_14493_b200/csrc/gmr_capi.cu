@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "gmr_kernels.cuh"
+#include "gmr_stage.cuh"
 #include "gmr_train.cuh"
 #include "gmr_eval.cuh"
 
@@ -888,6 +889,50 @@ int gmr_render_backward(const GmrMesh* mesh, const GmrCamera* cams, int32_t B, c
   if (r->dtype == GMR_F64)
     return render_backward_t<double>(mesh, cams, B, r, rgb, g_rgb, g_alpha, g_pos, g_col, topo, ws, L, st);
   return render_backward_t<float>(mesh, cams, B, r, rgb, g_rgb, g_alpha, g_pos, g_col, topo, ws, L, st);
+}
+
+// ---- projection stage (project_cloud / project_cloud_backward) ------------
+
+int gmr_project(const void* means, const void* cov3d, int64_t K, const GmrCamera* cam, int32_t W, int32_t H,
+                int32_t dtype, void* mean2d, void* cov2d, void* conic, void* depth, void* radius, void* t_cam,
+                uint8_t* kept, void* stream) {
+  if (K < 0 || !cam || W < 1 || H < 1) return fail(GMR_EINVAL, "bad projection arguments");
+  if (dtype != GMR_F32 && dtype != GMR_F64) return fail(GMR_EINVAL, "bad dtype");
+  if (K == 0) return GMR_OK;
+  if (!means || !cov3d || !mean2d || !cov2d || !conic || !depth || !radius || !t_cam || !kept)
+    return fail(GMR_EINVAL, "null pointer argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == GMR_F64) {
+    project_gaussians<double><<<grid_for(K, 256), 256, 0, st>>>(
+        (const double*)means, (const double*)cov3d, K, make_cams<double>(cam, 0, 1).cam[0], W, H, (double*)mean2d,
+        (double*)cov2d, (double*)conic, (double*)depth, (double*)radius, (double*)t_cam, kept);
+  } else {
+    project_gaussians<float><<<grid_for(K, 256), 256, 0, st>>>(
+        (const float*)means, (const float*)cov3d, K, make_cams<float>(cam, 0, 1).cam[0], W, H, (float*)mean2d,
+        (float*)cov2d, (float*)conic, (float*)depth, (float*)radius, (float*)t_cam, kept);
+  }
+  GMR_LAUNCHED();
+  return GMR_OK;
+}
+
+int gmr_project_backward(const void* t_cam, const void* cov3d, int64_t K, const GmrCamera* cam, int32_t dtype,
+                         const void* g_mean2d, const void* g_cov2d, void* g_mean3d, void* g_cov3d, void* stream) {
+  if (K < 0 || !cam) return fail(GMR_EINVAL, "bad projection arguments");
+  if (dtype != GMR_F32 && dtype != GMR_F64) return fail(GMR_EINVAL, "bad dtype");
+  if (K == 0) return GMR_OK;
+  if (!t_cam || !cov3d || !g_mean2d || !g_cov2d || !g_mean3d || !g_cov3d) return fail(GMR_EINVAL, "null pointer argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == GMR_F64) {
+    project_gaussians_backward<double><<<grid_for(K, 256), 256, 0, st>>>(
+        (const double*)t_cam, (const double*)cov3d, K, make_cams<double>(cam, 0, 1).cam[0], (const double*)g_mean2d,
+        (const double*)g_cov2d, (double*)g_mean3d, (double*)g_cov3d);
+  } else {
+    project_gaussians_backward<float><<<grid_for(K, 256), 256, 0, st>>>(
+        (const float*)t_cam, (const float*)cov3d, K, make_cams<float>(cam, 0, 1).cam[0], (const float*)g_mean2d,
+        (const float*)g_cov2d, (float*)g_mean3d, (float*)g_cov3d);
+  }
+  GMR_LAUNCHED();
+  return GMR_OK;
 }
 
 // ---- splat path ----------------------------------------------------------

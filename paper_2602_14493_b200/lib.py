@@ -86,6 +86,8 @@ _SIGNATURES = {
     "gmr_fit_step_scheduled": ([P(GmrFitState), P(GmrMeshGraph), c_i64, c_vp, c_vp, c_vp] + [ctypes.c_double] * 6
                                + [c_vp, c_vp] + [ctypes.c_double] * 3 + [c_i32, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp],
                                c_i32),
+    "gmr_project": ([c_vp, c_vp, c_i64, P(GmrCamera), c_i32, c_i32, c_i32] + [c_vp] * 7 + [c_vp], c_i32),
+    "gmr_project_backward": ([c_vp, c_vp, c_i64, P(GmrCamera), c_i32, c_vp, c_vp, c_vp, c_vp, c_vp], c_i32),
     "gmr_mesh_regularizers": ([c_vp, P(GmrMeshGraph), c_i64, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp], c_i32),
     "gmr_image_loss_scratch_size": ([c_i64, P(c_sz)], c_i32),
     "gmr_image_loss": ([c_i32, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_sz, c_vp], c_i32),
