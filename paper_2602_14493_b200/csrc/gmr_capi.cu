@@ -195,7 +195,7 @@ struct ImageArgs {
 // Binning (K2) + blend forward (K3) over prepared item records.
 template <typename S>
 int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void* alpha,
-                  cudaStream_t st, const LossArgs* la = nullptr, const ImageArgs* ia = nullptr,
+                  cudaStream_t st, bool unit_opacity, const LossArgs* la = nullptr, const ImageArgs* ia = nullptr,
                   void* status_host = nullptr, void* status_event = nullptr) {
   typedef typename KeyOf<S>::type K;
   const uint32_t items = (uint32_t)L.items;
@@ -316,10 +316,18 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
     // all of the SM's unified L1/shared memory as shared memory: the
     // default carveout would cap residency below what registers allow
     // once per instantiation (thread-safe static init; also keeps it out of graph captures)
-    static const cudaError_t attr_rc = cudaFuncSetAttribute(
-        blend_forward<S>, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+    static const cudaError_t attr_rc = [] {
+      const cudaError_t e = cudaFuncSetAttribute(blend_forward<S, false>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                                 (int)cudaSharedmemCarveoutMaxShared);
+      return e != cudaSuccess ? e
+                              : cudaFuncSetAttribute(blend_forward<S, true>,
+                                                     cudaFuncAttributePreferredSharedMemoryCarveout,
+                                                     (int)cudaSharedmemCarveoutMaxShared);
+    }();
     GMR_CUDA(attr_rc);
-    blend_forward<S><<<(unsigned)L.bins, kBlendThreads, 0, st>>>(a);
+    // mesh splats all have opacity 1 (convert.py:326): the evaluator skips the product
+    if (unit_opacity) blend_forward<S, false><<<(unsigned)L.bins, kBlendThreads, 0, st>>>(a);
+    else blend_forward<S, true><<<(unsigned)L.bins, kBlendThreads, 0, st>>>(a);
     GMR_LAUNCHED();
   }
   if (la && L.bins) {
@@ -365,7 +373,7 @@ int render_forward_t(const GmrMesh* m, const GmrCamera* cams, int B, const GmrRa
       GMR_LAUNCHED();
     }
   }
-  return bin_and_blend<S>(L, ws, r, rgb, alpha, st, la, ia, status_host, status_event);
+  return bin_and_blend<S>(L, ws, r, rgb, alpha, st, true, la, ia, status_host, status_event);
 }
 
 template <typename S, bool kOpacity>
@@ -491,7 +499,7 @@ int rasterize_forward_t(const GmrSplats* sp, const GmrRaster* r, void* rgb, void
     pack_splats<S><<<grid_for(sp->count, 256), 256, 0, st>>>(a);
     GMR_LAUNCHED();
   }
-  return bin_and_blend<S>(L, ws, r, rgb, alpha, st);
+  return bin_and_blend<S>(L, ws, r, rgb, alpha, st, false);
 }
 
 int check_splats(const GmrSplats* sp) {

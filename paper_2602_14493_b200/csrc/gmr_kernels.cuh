@@ -965,41 +965,42 @@ __device__ __forceinline__ float inv_om(float om) {
 }
 __device__ __forceinline__ double inv_om(double om) { return 1.0 / om; }
 
-// Per-pixel alpha of a staged splat (render.py:251-256).  `q` holds the
-// splat's conic in the form the evaluator wants (Eval<S>::prep).
+// Per-pixel alpha of a staged splat (render.py:251-256) from its conic in the
+// form the evaluator wants (Eval<S>::prep: coefficients A, B, C) and its
+// opacity o.  kOp = false: o == 1 (every mesh-path splat, convert.py:326),
+// where o * e == e exactly, so the product is skipped without changing a bit.
 //  double (parity path): the reference's expression and exp(), with each
 //    operation rounded as numpy rounds it;
 //  float (fast path): power * log2(e) as dx (A dx + B dy) + C dy^2 with the
 //    coefficients folded at staging time, then ex2.approx.
 template <typename S> struct Eval;
 template <> struct Eval<double> {
-  static __device__ __forceinline__ V4<double> prep(double ca, double cb, double cc, double o) {
-    V4<double> q;
-    q.x = ca; q.y = cb; q.z = cc; q.w = o;
-    return q;
+  static __device__ __forceinline__ void prep(double ca, double cb, double cc, double& A, double& B, double& C) {
+    A = ca; B = cb; C = cc;
   }
-  static __device__ __forceinline__ double alpha(double dx, double dy, const V4<double>& q, double& ep,
-                                                 double& raw) {
-    const double qq = add_rn(mul_rn(mul_rn(q.x, dx), dx), mul_rn(mul_rn(q.z, dy), dy));
-    const double power = sub_rn(mul_rn(-0.5, qq), mul_rn(mul_rn(q.y, dx), dy));
+  template <bool kOp>
+  static __device__ __forceinline__ double alpha(double dx, double dy, double A, double B, double C, double o,
+                                                 double& ep, double& raw) {
+    const double qq = add_rn(mul_rn(mul_rn(A, dx), dx), mul_rn(mul_rn(C, dy), dy));
+    const double power = sub_rn(mul_rn(-0.5, qq), mul_rn(mul_rn(B, dx), dy));
     ep = exp(power);
-    raw = mul_rn(q.w, ep);
+    raw = kOp ? mul_rn(o, ep) : ep;
     return raw < 0.99 ? raw : 0.99;
   }
 };
 template <> struct Eval<float> {
-  static __device__ __forceinline__ V4<float> prep(float ca, float cb, float cc, float o) {
+  static __device__ __forceinline__ void prep(float ca, float cb, float cc, float& A, float& B, float& C) {
     const float l2e = 1.4426950408889634f;
-    V4<float> q;
-    q.x = -0.5f * l2e * ca; q.y = -l2e * cb; q.z = -0.5f * l2e * cc; q.w = o;
-    return q;
+    A = -0.5f * l2e * ca; B = -l2e * cb; C = -0.5f * l2e * cc;
   }
-  static __device__ __forceinline__ float alpha(float dx, float dy, const V4<float>& q, float& ep, float& raw) {
-    const float p2 = __fmaf_rn(dx, __fmaf_rn(q.x, dx, __fmul_rn(q.y, dy)), __fmul_rn(__fmul_rn(q.z, dy), dy));
+  template <bool kOp>
+  static __device__ __forceinline__ float alpha(float dx, float dy, float A, float B, float C, float o, float& ep,
+                                                float& raw) {
+    const float p2 = __fmaf_rn(dx, __fmaf_rn(A, dx, __fmul_rn(B, dy)), __fmul_rn(__fmul_rn(C, dy), dy));
     float e;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(p2));
     ep = e;
-    raw = __fmul_rn(q.w, e);
+    raw = kOp ? __fmul_rn(o, e) : e;
     return raw < 0.99f ? raw : 0.99f;
   }
 };
@@ -1014,36 +1015,60 @@ __device__ __forceinline__ void prefetch_records(const BlendArgs<S>& p, uint32_t
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p.col4 + (item - vbase_item)));
 }
 
+#ifndef GMR_BWD_BATCH
+#define GMR_BWD_BATCH 128
+#endif
+#ifndef GMR_BWD_PAIR_KB
+#define GMR_BWD_PAIR_KB 24
+#endif
+#ifndef GMR_BWD_MINB
+#define GMR_BWD_MINB 5
+#endif
 constexpr int kFwdBatch = 256;
-constexpr int kBwdBatch = 128;
-constexpr int kBwdSlots = 16;
+constexpr int kBwdBatch = GMR_BWD_BATCH;
 
-template <typename S, int NB> struct StageSmem {
-  V2<S> mean[NB];         // mx, my
-  V4<S> q[NB];            // evaluator coefficients + opacity
-  V4<S> col[NB];          // r, g, b, -
-  uint32_t cov[NB][9];    // 8 coverage words (+1 pad: conflict-free transposes)
-  uint32_t tw[NB / 32][kBlendThreads];   // transposed: per pixel, covering entries per chunk
+// A staged batch.  Per entry two 16-byte (float) records, read with two
+// vector loads per (pixel, entry) pair:
+//   ea = (mean_x, mean_y, A, B), eb = (C, r, g, b)
+// plus the opacity (splat path only), the 8 coverage words (+1 pad:
+// conflict-free transposes) and, per pixel, the covering entries of each
+// 32-entry chunk.
+template <typename S, int NB, bool kOp> struct StageSmem {
+  V4<S> ea[NB];
+  V4<S> eb[NB];
+  S op[kOp ? NB : 1];
+  uint32_t cov[NB][9];
+  uint32_t tw[NB / 32][kBlendThreads];
 };
 
-// Stage one batch: thread i < n loads entry base+i (i >= n: empty mask),
-// then every warp transposes its coverage words into per-pixel bit lists.
-template <typename S, int NB>
-__device__ __forceinline__ void stage_batch(const BlendArgs<S>& p, StageSmem<S, NB>& sm, uint32_t base, int n,
+// One entry of a batch: its records from the item's splat and colour.
+template <typename S, int NB, bool kOp>
+__device__ __forceinline__ void stage_entry(const BlendArgs<S>& p, StageSmem<S, NB, kOp>& sm, int i, uint32_t item,
+                                            uint32_t vbase_item, Splat<S>& s) {
+  s = p.splat[item];
+  const V4<S> c = p.col4[item - vbase_item];
+  V4<S> a, b;
+  a.x = s.a.x; a.y = s.a.y;
+  Eval<S>::prep(s.a.z, s.a.w, s.b.x, a.z, a.w, b.x);
+  b.y = c.x; b.z = c.y; b.w = c.z;
+  sm.ea[i] = a;
+  sm.eb[i] = b;
+  if constexpr (kOp) sm.op[i] = c.w;
+}
+
+// Stage one batch (forward): thread i < n loads entry base+i and solves its
+// coverage rows (i >= n: empty mask), then every warp transposes its
+// coverage words into per-pixel bit lists.
+template <typename S, int NB, bool kOp>
+__device__ __forceinline__ void stage_batch(const BlendArgs<S>& p, StageSmem<S, NB, kOp>& sm, uint32_t base, int n,
                                             uint32_t vbase_item, int x0, int y0) {
   for (int i = threadIdx.x; i < NB; i += kBlendThreads) {
     uint32_t* w = sm.cov[i];
 #pragma unroll
     for (int q = 0; q < 8; ++q) w[q] = 0;
     if (i < n) {
-      const uint32_t item = p.entry_item[base + i];
-      const Splat<S> s = p.splat[item];
-      const V4<S> c = p.col4[item - vbase_item];
-      V2<S> m;
-      m.x = s.a.x; m.y = s.a.y;
-      sm.mean[i] = m;
-      sm.q[i] = Eval<S>::prep(s.a.z, s.a.w, s.b.x, c.w);
-      sm.col[i] = c;
+      Splat<S> s;
+      stage_entry<S, NB, kOp>(p, sm, i, p.entry_item[base + i], vbase_item, s);
       tile_coverage(s.a, s.b, x0, y0, w);
     }
   }
@@ -1063,14 +1088,6 @@ struct BitWalk {
     nch = skip ? 0 : (n + 31) >> 5;
     c = 0;
     bits = nch ? tw[0][threadIdx.x] : 0u;
-  }
-  template <int NB>
-  __device__ __forceinline__ int next(const uint32_t (&tw)[NB / 32][kBlendThreads]) {
-    while (!bits && ++c < nch) bits = tw[c][threadIdx.x];
-    if (!bits) return -1;
-    const int k = __ffs(bits) - 1;
-    bits &= bits - 1;
-    return c * 32 + k;
   }
   // Up to two candidates from the current chunk (j2 = -1 if it has only one
   // left); refills from the next non-empty chunk only when the current one
@@ -1093,9 +1110,13 @@ struct BitWalk {
   __device__ __forceinline__ void stop() { bits = 0; nch = 0; }
 };
 
-template <typename S>
-__global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 4 : 7) blend_forward(BlendArgs<S> p) {
-  __shared__ StageSmem<S, kFwdBatch> sm;
+
+#ifndef GMR_FWD_MINB
+#define GMR_FWD_MINB 7   // 32 registers: a few loop-invariant spills, measured faster than 40 registers at 6 CTAs
+#endif
+template <typename S, bool kOp>
+__global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 4 : GMR_FWD_MINB) blend_forward(BlendArgs<S> p) {
+  __shared__ StageSmem<S, kFwdBatch, kOp> sm;
   const uint32_t g = p.sched ? p.sched[blockIdx.x] : blockIdx.x;
   const uint32_t view = g / p.tiles_per_view, t = g % p.tiles_per_view;
   const int tx = (int)(t % (uint32_t)p.tiles_x), ty = (int)(t / (uint32_t)p.tiles_x);
@@ -1111,7 +1132,7 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 4 : 7) blend_f
   for (uint32_t base = start; base < end; base += kFwdBatch) {
     if (__syncthreads_count(done) == kBlendThreads) break;
     const int n = (int)min((uint32_t)kFwdBatch, end - base);
-    stage_batch<S, kFwdBatch>(p, sm, base, n, vbase_item, x0, y0);
+    stage_batch<S, kFwdBatch, kOp>(p, sm, base, n, vbase_item, x0, y0);
     __syncthreads();
     if (p.covbuf) {   // keep the coverage masks for the backward (coalesced 32-byte rows)
       for (int i = threadIdx.x; i < n; i += kBlendThreads) {
@@ -1128,41 +1149,47 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 4 : 7) blend_f
     // two candidates per trip: their alphas are independent, only the
     // transmittance update is sequential (front-to-back order kept)
     for (int j1, j2; it.pair<kFwdBatch>(sm.tw, j1, j2);) {
-      const V2<S> m1 = sm.mean[j1];
+      const V4<S> a1 = sm.ea[j1], b1 = sm.eb[j1];
       S ep, raw;
-      const S a1 = Eval<S>::alpha(sub_rn(fpx, m1.x), sub_rn(fpy, m1.y), sm.q[j1], ep, raw);
-      S a2 = S(0);
+      const S al1 = Eval<S>::template alpha<kOp>(sub_rn(fpx, a1.x), sub_rn(fpy, a1.y), a1.z, a1.w, b1.x,
+                                                 kOp ? sm.op[j1] : one, ep, raw);
+      V4<S> b2;
+      S al2 = S(0);
       if (j2 >= 0) {
-        const V2<S> m2 = sm.mean[j2];
-        a2 = Eval<S>::alpha(sub_rn(fpx, m2.x), sub_rn(fpy, m2.y), sm.q[j2], ep, raw);
+        const V4<S> a2 = sm.ea[j2];
+        b2 = sm.eb[j2];
+        al2 = Eval<S>::template alpha<kOp>(sub_rn(fpx, a2.x), sub_rn(fpy, a2.y), a2.z, a2.w, b2.x,
+                                           kOp ? sm.op[j2] : one, ep, raw);
       }
-      if (a1 >= Const<S>::contrib_floor()) {
-        const S test = mul_rn(T, sub_rn(one, a1));
+      bool stop = false;
+      if (al1 >= Const<S>::contrib_floor()) {
+        const S test = mul_rn(T, sub_rn(one, al1));
         if (test < Const<S>::t_stop()) {
-          done = true;
-          it.stop();
-          break;
+          stop = true;
+        } else {
+          const S w = mul_rn(al1, T);
+          ar += w * b1.y;
+          ag += w * b1.z;
+          ab += w * b1.w;
+          T = test;
         }
-        const V4<S> co = sm.col[j1];
-        const S w = mul_rn(a1, T);
-        ar += w * co.x;
-        ag += w * co.y;
-        ab += w * co.z;
-        T = test;
       }
-      if (a2 >= Const<S>::contrib_floor()) {
-        const S test = mul_rn(T, sub_rn(one, a2));
+      if (!stop && al2 >= Const<S>::contrib_floor()) {
+        const S test = mul_rn(T, sub_rn(one, al2));
         if (test < Const<S>::t_stop()) {
-          done = true;
-          it.stop();
-          break;
+          stop = true;
+        } else {
+          const S w = mul_rn(al2, T);
+          ar += w * b2.y;
+          ag += w * b2.z;
+          ab += w * b2.w;
+          T = test;
         }
-        const V4<S> co = sm.col[j2];
-        const S w = mul_rn(a2, T);
-        ar += w * co.x;
-        ag += w * co.y;
-        ab += w * co.z;
-        T = test;
+      }
+      if (stop) {
+        done = true;
+        it.stop();
+        break;
       }
     }
     prefetch_records(p, nxt, vbase_item);
@@ -1196,37 +1223,39 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 4 : 7) blend_f
 template <typename S, bool kOpacity> struct RecOf { typedef V2<S> type; };
 template <typename S> struct RecOf<S, true> { typedef V4<S> type; };
 
-constexpr int kBwdPairBytes = 24 * 1024;
+constexpr int kBwdPairBytes = GMR_BWD_PAIR_KB * 1024;
 
 template <typename S, bool kOpacity> struct BwdSmem {
   typedef typename RecOf<S, kOpacity>::type Rec;
   static constexpr int kCap = kBwdPairBytes / (int)(sizeof(Rec) + 1);
-  StageSmem<S, kBwdBatch> st;
-  uint32_t pre[kBwdBatch][2];       // per entry: covered-pixel count before each row pair (bytes)
-  uint32_t off[kBwdBatch + 1];      // per entry: first record (exclusive scan of covered counts)
-  uint32_t scan_tmp[8];
+  StageSmem<S, kBwdBatch, kOpacity> st;
+  uint16_t wbase[kBwdBatch][8];     // per entry and warp: first record of the warp's covered pixels
+  uint2 rng[kBwdBatch];             // per entry: [first, end) of its records
+  uint32_t wsum[kBlendThreads / 32];
   V4<S> pix[kBlendThreads];         // per tile pixel (col + 16 row): g_r, g_g, g_b
-  Rec rec[kCap];                    // per (entry, covered pixel in row-major order): (dp, w[, dL/dalpha * ep])
+  Rec rec[kCap];                    // per (entry, covered pixel): (dp, w[, dL/dalpha * ep])
   uint8_t rq[kCap];                 // tile pixel (col + 16 row) of each record
 };
 
 // Backward (render.py:294-361).  Per batch of staged entries:
-//  - every entry's covered pixels get a contiguous record range (block scan
-//    of the coverage popcounts; the batch is cut where the ranges would
-//    overflow shared memory) and the records are zeroed;
+//  - each staging thread takes one entry's records and the forward's
+//    coverage words, counts its covered pixels per warp block, and a
+//    scan over the batch gives every entry a contiguous record range
+//    [rng.x, rng.y) (the batch is cut where the ranges would overflow
+//    shared memory), ordered by warp, then lane; the records are zeroed;
 //  - pass 1 (lane = pixel) re-scans front to back with the forward's exact
 //    decisions.  With C = g.(rgb - T_f bg) = sum_j (g.c_j) w_j the suffix is
 //    S_k = C - sum_{j<=k} (g.c_j) w_j, so (render.py:327-334)
 //      dL/dalpha_k = (g.c_k) T_k - (S_k + (g.bg - g_a) T_f) / (1 - alpha_k)
 //    and each included pair writes (dp = dL/dalpha * alpha, 0 where the 0.99
 //    clamp is active (:336-338), w = alpha T) to record
-//    off[j] + (rank of this pixel among j's covered pixels);
+//    wbase[j][warp] + (rank of this lane among the warp's lanes covering j);
 //  - pass 2 (two threads per entry, halves of its records) sums
 //      [dp dx, dp dy, dp dx^2, dp dx dy, dp dy^2, w g_r, w g_g, w g_b]
-//    in pixel order; the halves are combined in a fixed order.
+//    in record order; the halves are combined in a fixed order.
 //  No atomics, fixed orders: the result is deterministic.
 template <typename S, bool kOpacity>
-__global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : 5) blend_backward(BlendArgs<S> p) {
+__global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : GMR_BWD_MINB) blend_backward(BlendArgs<S> p) {
   extern __shared__ __align__(32) unsigned char dyn[];
   typedef BwdSmem<S, kOpacity> Sm;
   typedef typename Sm::Rec Rec;
@@ -1260,70 +1289,64 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : 5) blend_b
   bool done = !inside;
   const uint32_t start = p.bounds[g], end = p.bounds[g + 1];
   const uint32_t vbase_item = view * p.items_per_view;
-  const int je = tid >> 1, half = tid & 1;
+  // pass 2: two threads per entry (halves of its records) for 128-entry
+  // batches, one per entry for 256
+  constexpr int kSplit = kBlendThreads / kBwdBatch;
+  static_assert(kSplit == 1 || kSplit == 2, "backward batch must be 128 or 256 entries");
+  const int je = kSplit == 2 ? tid >> 1 : tid, half = kSplit == 2 ? tid & 1 : 0;
   uint32_t base = start;
   while (base < end) {
     if (__syncthreads_count(done) == kBlendThreads) break;
     const int n_st = (int)min((uint32_t)kBwdBatch, end - base);
-    // ---- stage records + coverage ----
-    for (int i = tid; i < kBwdBatch; i += kBlendThreads) {
-      uint32_t* w = sm.st.cov[i];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) w[q] = 0;
-      if (i < n_st) {
-        const uint32_t item = p.entry_item[base + i];
-        const Splat<S> s = p.splat[item];
-        const V4<S> c = p.col4[item - vbase_item];
-        V2<S> m;
-        m.x = s.a.x; m.y = s.a.y;
-        sm.st.mean[i] = m;
-        sm.st.q[i] = Eval<S>::prep(s.a.z, s.a.w, s.b.x, c.w);
-        sm.st.col[i] = c;
-        if (p.covbuf) {   // the forward's masks for these entries
-          const uint4* src = reinterpret_cast<const uint4*>(p.covbuf + (size_t)(base + i) * 8);
-          const uint4 lo = src[0], hi = src[1];
-          w[0] = lo.x; w[1] = lo.y; w[2] = lo.z; w[3] = lo.w;
-          w[4] = hi.x; w[5] = hi.y; w[6] = hi.z; w[7] = hi.w;
-        } else {
-          tile_coverage(s.a, s.b, x0, y0, w);
-        }
-      }
-    }
-    __syncthreads();
-    // ---- per entry: covered count, row-pair prefixes; block scan -> offsets ----
+    // ---- stage records + the forward's coverage words; per-warp counts ----
     uint32_t ncov = 0;
-    if (tid < kBwdBatch) {
-      uint32_t pre0 = 0, pre1 = 0;
+    uint32_t wcnt[8];   // covered pixels of this entry in warp blocks before each warp
+#pragma unroll
+    for (int q = 0; q < 8; ++q) wcnt[q] = 0;
+    if (tid < n_st) {
+      Splat<S> s;
+      stage_entry<S, kBwdBatch, kOpacity>(p, sm.st, tid, p.entry_item[base + tid], vbase_item, s);
+      const uint4* src = reinterpret_cast<const uint4*>(p.covbuf + (size_t)(base + tid) * 8);
+      const uint4 lo = src[0], hi = src[1];
+      const uint32_t w[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+      uint32_t* cw = sm.st.cov[tid];
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        if (q < 4) pre0 |= ncov << (8 * q); else pre1 |= ncov << (8 * (q - 4));
-        ncov += __popc(sm.st.cov[tid][q]);
+        cw[q] = w[q];
+        wcnt[q] = ncov;
+        ncov += __popc(w[q]);
       }
-      sm.pre[tid][0] = pre0;
-      sm.pre[tid][1] = pre1;
     }
-    uint32_t total;
-    const uint32_t excl = block_exclusive_scan_256(ncov, sm.scan_tmp, &total);
-    const bool fits = tid < n_st && excl + ncov <= (uint32_t)Sm::kCap;
-    if (tid < kBwdBatch) sm.off[tid] = excl;
-    const int n = __syncthreads_count(fits);          // entries taken this batch (prefix property)
-    // entries not taken are re-staged next batch: clear their coverage
-    for (int i = n + tid; i < kBwdBatch; i += kBlendThreads) {
+    // exclusive scan of the covered counts over the batch (threads < 128)
+    uint32_t x = ncov;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) sm.st.cov[i][q] = 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
     }
+    if (lane == 31) sm.wsum[warp] = x;
     __syncthreads();
-    const uint32_t rec_end = (n == kBwdBatch) ? total : sm.off[n];
+    uint32_t excl = x - ncov;
+    for (int w2 = 0; w2 < warp; ++w2) excl += sm.wsum[w2];
+    const bool fits = tid < n_st && excl + ncov <= (uint32_t)Sm::kCap;
+    if (fits) {
+      sm.rng[tid] = make_uint2(excl, excl + ncov);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) sm.wbase[tid][q] = (uint16_t)(excl + wcnt[q]);
+    }
+    const int n = __syncthreads_count(fits);          // entries taken this batch (prefix property)
+    const uint32_t rec_end = n ? sm.rng[n - 1].y : 0u;
     for (uint32_t r = tid; r < rec_end; r += kBlendThreads) {
       Rec z;
       z.x = z.y = S(0);
       if constexpr (kOpacity) { z.z = z.w = S(0); }
       sm.rec[r] = z;
     }
-    const int warp_ = warp;
+    // entries past n are re-staged next batch: their coverage reads as empty
 #pragma unroll
     for (int c = 0; c < kBwdBatch / 32; ++c)
-      if (c * 32 < n) sm.st.tw[c][tid] = transpose32(sm.st.cov[c * 32 + lane][warp_], lane);
+      if (c * 32 < n)
+        sm.st.tw[c][tid] = transpose32(c * 32 + lane < n ? sm.st.cov[c * 32 + lane][warp] : 0u, lane);
     __syncthreads();
     const uint32_t nxt_e = base + (uint32_t)n + threadIdx.x;
     const uint32_t nxt = (threadIdx.x < kBwdBatch && nxt_e < end) ? p.entry_item[nxt_e] : 0xffffffffu;
@@ -1331,18 +1354,22 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : 5) blend_b
     {
       BitWalk it;
       it.start<kBwdBatch>(sm.st.tw, n, done);
-      const uint32_t my_word_shift = 8 * (warp & 3);
       for (int j1, j2; it.pair<kBwdBatch>(sm.st.tw, j1, j2);) {
         int js[2] = {j1, j2};
         S as[2], eps[2], raws[2];
+        V4<S> bs[2];
         {
-          const V2<S> m = sm.st.mean[j1];
-          as[0] = Eval<S>::alpha(sub_rn(fpx, m.x), sub_rn(fpy, m.y), sm.st.q[j1], eps[0], raws[0]);
+          const V4<S> a = sm.st.ea[j1];
+          bs[0] = sm.st.eb[j1];
+          as[0] = Eval<S>::template alpha<kOpacity>(sub_rn(fpx, a.x), sub_rn(fpy, a.y), a.z, a.w, bs[0].x,
+                                                    kOpacity ? sm.st.op[j1] : one, eps[0], raws[0]);
         }
         as[1] = S(0);
         if (j2 >= 0) {
-          const V2<S> m = sm.st.mean[j2];
-          as[1] = Eval<S>::alpha(sub_rn(fpx, m.x), sub_rn(fpy, m.y), sm.st.q[j2], eps[1], raws[1]);
+          const V4<S> a = sm.st.ea[j2];
+          bs[1] = sm.st.eb[j2];
+          as[1] = Eval<S>::template alpha<kOpacity>(sub_rn(fpx, a.x), sub_rn(fpy, a.y), a.z, a.w, bs[1].x,
+                                                    kOpacity ? sm.st.op[j2] : one, eps[1], raws[1]);
         }
         bool stop = false;
 #pragma unroll
@@ -1356,9 +1383,8 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : 5) blend_b
             stop = true;
             continue;
           }
-          const V4<S> co = sm.st.col[j];
           const S w = mul_rn(a, T);
-          const S gdc = mypix.x * co.x + mypix.y * co.y + mypix.z * co.z;
+          const S gdc = mypix.x * bs[u].y + mypix.y * bs[u].z + mypix.z * bs[u].w;
           P += gdc * w;
           const S d_alpha = gdc * T - ((Ctot - P) + bterm) * inv_om(om);
           Rec s;
@@ -1368,9 +1394,7 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : 5) blend_b
             s.z = raws[u] < Const<S>::alpha_clamp() ? d_alpha * eps[u] : S(0);
             s.w = S(0);
           }
-          const uint32_t pw = sm.pre[j][warp >> 2];
-          const uint32_t r = sm.off[j] + ((pw >> my_word_shift) & 255u) +
-                             (uint32_t)__popc(sm.st.cov[j][warp] & lt);
+          const uint32_t r = (uint32_t)sm.wbase[j][warp] + (uint32_t)__popc(sm.st.cov[j][warp] & lt);
           sm.rec[r] = s;
           sm.rq[r] = (uint8_t)my_pix;
           T = test;
@@ -1383,7 +1407,7 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : 5) blend_b
       }
     }
     prefetch_records(p, nxt, vbase_item);
-    if (p.covbuf && nxt != 0xffffffffu)   // and the next batch's coverage words
+    if (nxt != 0xffffffffu)   // and the next batch's coverage words
       asm volatile("prefetch.global.L2 [%0];" ::"l"(p.covbuf + (size_t)nxt_e * 8));
     __syncthreads();
     // ---- pass 2: my entry, my half of its records (pixel order) ----
@@ -1392,12 +1416,11 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : 5) blend_b
     for (int q = 0; q < 8; ++q) acc[q] = S(0);
     S aop = S(0);
     if (je < n) {
-      const uint32_t r0 = sm.off[je];
-      const uint32_t r1 = (je + 1 < n) ? sm.off[je + 1] : rec_end;
-      const uint32_t mid = r0 + ((r1 - r0 + 1) >> 1);
-      const uint32_t lo = half ? mid : r0, hi = half ? r1 : mid;
-      const V2<S> em = sm.st.mean[je];
-      const S ex0 = S(x0) - em.x, ey0 = S(y0) - em.y;
+      const uint2 rr = sm.rng[je];
+      const uint32_t mid = kSplit == 2 ? rr.x + ((rr.y - rr.x + 1) >> 1) : rr.y;
+      const uint32_t lo = half ? mid : rr.x, hi = half ? rr.y : mid;
+      const V4<S> ea = sm.st.ea[je];
+      const S ex0 = S(x0) - ea.x, ey0 = S(y0) - ea.y;
       for (uint32_t r = lo; r < hi; ++r) {
         const Rec s = sm.rec[r];
         const int q = sm.rq[r];
@@ -1416,9 +1439,11 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : 5) blend_b
       }
     }
     // combine the two halves (fixed order) and store at the pre-sort slot
+    if constexpr (kSplit == 2) {
 #pragma unroll
-    for (int q = 0; q < 8; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], 1);
-    if (kOpacity) aop += __shfl_xor_sync(0xffffffffu, aop, 1);
+      for (int q = 0; q < 8; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], 1);
+      if (kOpacity) aop += __shfl_xor_sync(0xffffffffu, aop, 1);
+    }
     if (half == 0 && je < n) {
       const uint32_t item_j = p.entry_item[base + je];
       const uint4 bi = p.bin[item_j];
