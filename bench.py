@@ -250,17 +250,27 @@ def run_gmr(args, cfg):
         # one step behind, so the device never drains between steps
         nv = B if views is None else views
         gp = gc = None
-        states = []
+        states, reds = [], []
         for c0 in range(0, nv, chunk):
             c1 = min(nv, c0 + chunk)
             rgb, alpha, st = engine.render_forward(pos, col, faces, cams[c0:c1], W, H, BG, flags=flags, check=False)
             a, b = engine.render_backward(st, pos, col, faces, rgb, g_rgb[c0:c1], g_a[c0:c1])
+            if multi and nv > chunk:
+                # this view group's reduction runs on NCCL's stream while the
+                # next group renders
+                reds.append(gdist.allreduce_vertex_grads(a, b, async_op=True))
             gp, gc = (a, b) if gp is None else (gp + a, gc + b)
             states.append(st)
         pending.extend(states)
         last["states"] = states
-        if multi:
-            gdist.allreduce_vertex_grads(gp, gc)
+        if reds:
+            parts = [r.wait() for r in reds]
+            gp, gc = parts[0][0].clone(), parts[0][1].clone()
+            for x in parts[1:]:
+                gp += x[0]
+                gc += x[1]
+        elif multi:
+            gp, gc, _ = gdist.allreduce_vertex_grads(gp, gc)
         keep = 0 if final else len(states)
         while len(pending) > keep:
             engine.check_status(pending.pop(0))   # raises on overflow / non-finite
@@ -365,16 +375,28 @@ def run_gmr(args, cfg):
         main.wait_event(s["up"])
         p = s["p"].detach().requires_grad_(True)
         c = s["c"].detach().requires_grad_(True)
+        reds = []
         for c0 in range(0, B, chunk):
             c1 = min(B, c0 + chunk)
             rgb, alpha = gmr.render_views(p, c, faces, cams[c0:c1], W, H, BG)
             if prefetch and c0 == 0:
                 upload(slots[(k + 1) % 2])        # next step's inputs, behind this forward
             main.wait_event(s["up_g"])
-            torch.autograd.backward([rgb, alpha], [s["g"][c0:c1], s["a"][c0:c1]])
-        gp, gc = p.grad, c.grad
-        if multi:
-            gp, gc, _ = gdist.allreduce_vertex_grads(gp, gc)
+            if multi and B > chunk:               # per view group, reduced while the next group renders
+                a, b = torch.autograd.grad([rgb, alpha], [p, c], [s["g"][c0:c1], s["a"][c0:c1]])
+                reds.append(gdist.allreduce_vertex_grads(a, b, async_op=True))
+            else:
+                torch.autograd.backward([rgb, alpha], [s["g"][c0:c1], s["a"][c0:c1]])
+        if reds:
+            parts = [r.wait() for r in reds]
+            gp, gc = parts[0][0].clone(), parts[0][1].clone()
+            for x in parts[1:]:
+                gp += x[0]
+                gc += x[1]
+        else:
+            gp, gc = p.grad, c.grad
+            if multi:
+                gp, gc, _ = gdist.allreduce_vertex_grads(gp, gc)
         s["used"].record(main)
         with torch.cuda.stream(down_s):
             down_s.wait_event(s["used"])

@@ -404,6 +404,11 @@ int blend_backward_launch(const Layout& L, void* ws, const GmrRaster* r, const v
   a.partial = at<S>(ws, L.partial);
   a.partial_op = kOpacity ? at<S>(ws, L.partial_op) : nullptr;
   const size_t dyn = sizeof(BwdSmem<S, kOpacity>);
+  // the float mesh path's occupancy (GMR_BWD_MINB CTAs per SM) is what the
+  // shared-memory layout is sized for: 228 KB per SM, allocated per CTA in
+  // 128-byte units plus 1 KB reserved
+  static_assert(((sizeof(BwdSmem<float, false>) + 127) / 128 * 128 + 1024) * GMR_BWD_MINB <= 228 * 1024,
+                "blend_backward shared memory no longer fits GMR_BWD_MINB CTAs per SM");
   // once per instantiation (thread-safe static init; also keeps it out of graph captures)
   static const cudaError_t attr_rc = [dyn] {
     const cudaError_t e = cudaFuncSetAttribute(blend_backward<S, kOpacity>,

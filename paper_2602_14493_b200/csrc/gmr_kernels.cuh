@@ -909,16 +909,37 @@ __global__ void __launch_bounds__(256) loss_reduce(const double* __restrict__ ti
   block_sum2(a, b, out2);
 }
 
-// lane r holds row r of a 32x32 bit matrix (bit c = M[r][c]); returns column
-// `lane` (bit r = M[r][lane]).  5 shuffle stages.
-__device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
-#pragma unroll
-  for (int j = 16; j > 0; j >>= 1) {
-    const uint32_t lo = j == 16 ? 0x0000FFFFu : j == 8 ? 0x00FF00FFu : j == 4 ? 0x0F0F0F0Fu
-                      : j == 2 ? 0x33333333u : 0x55555555u;
-    const uint32_t y = __shfl_xor_sync(0xffffffffu, x, j);
-    x = (lane & j) ? ((x & ~lo) | ((y & ~lo) >> j)) : ((x & lo) | ((y & lo) << j));
+// lane r holds row r of a 32x32 bit matrix (bit c = M[r][c]); transpose32
+// returns column `lane` (bit r = M[r][lane]) in 5 shuffle stages.  Stage j
+// exchanges j-bit groups with lane ^ j: a lane with (lane & j) keeps the high
+// group of every 2j-bit block and takes its partner's high groups shifted
+// down, the other lane keeps the low groups and takes the partner's low
+// groups shifted up.  Per lane and stage that is one fixed byte permutation
+// (j = 16, 8: PRMT) or a rotate by j or 32 - j plus a select mask (j < 8:
+// SHF + LOP3), so the per-lane constants are made once per batch
+// (TransposeLanes) and each stage costs 2-3 instructions.
+struct TransposeLanes {
+  uint32_t s16, s8, r4, r2, r1, m4, m2, m1;
+  __device__ __forceinline__ explicit TransposeLanes(int lane) {
+    s16 = (lane & 16) ? 0x3276u : 0x5410u;
+    s8 = (lane & 8) ? 0x3715u : 0x6240u;
+    r4 = (lane & 4) ? 4u : 28u;
+    r2 = (lane & 2) ? 2u : 30u;
+    r1 = (lane & 1) ? 1u : 31u;
+    m4 = (lane & 4) ? 0x0F0F0F0Fu : 0xF0F0F0F0u;
+    m2 = (lane & 2) ? 0x33333333u : 0xCCCCCCCCu;
+    m1 = (lane & 1) ? 0x55555555u : 0xAAAAAAAAu;
   }
+};
+__device__ __forceinline__ uint32_t transpose32(uint32_t x, const TransposeLanes& k) {
+  x = __byte_perm(x, __shfl_xor_sync(0xffffffffu, x, 16), k.s16);
+  x = __byte_perm(x, __shfl_xor_sync(0xffffffffu, x, 8), k.s8);
+  uint32_t y = __shfl_xor_sync(0xffffffffu, x, 4);
+  x = (x & ~k.m4) | (__funnelshift_r(y, y, k.r4) & k.m4);
+  y = __shfl_xor_sync(0xffffffffu, x, 2);
+  x = (x & ~k.m2) | (__funnelshift_r(y, y, k.r2) & k.m2);
+  y = __shfl_xor_sync(0xffffffffu, x, 1);
+  x = (x & ~k.m1) | (__funnelshift_r(y, y, k.r1) & k.m1);
   return x;
 }
 
@@ -1018,8 +1039,8 @@ __device__ __forceinline__ void prefetch_records(const BlendArgs<S>& p, uint32_t
 #ifndef GMR_BWD_BATCH
 #define GMR_BWD_BATCH 128
 #endif
-#ifndef GMR_BWD_PAIR_KB
-#define GMR_BWD_PAIR_KB 24
+#ifndef GMR_BWD_PAIR_BYTES
+#define GMR_BWD_PAIR_BYTES 24448   // 24 KB less 128 B: keeps BwdSmem<float> at 5 CTAs per SM
 #endif
 #ifndef GMR_BWD_MINB
 #define GMR_BWD_MINB 5
@@ -1033,17 +1054,17 @@ constexpr int kBwdBatch = GMR_BWD_BATCH;
 // plus the opacity (splat path only), the 8 coverage words (+1 pad:
 // conflict-free transposes) and, per pixel, the covering entries of each
 // 32-entry chunk.
-template <typename S, int NB, bool kOp> struct StageSmem {
+template <typename S, int NB, bool kOp, bool kCov = true> struct StageSmem {
   V4<S> ea[NB];
   V4<S> eb[NB];
   S op[kOp ? NB : 1];
-  uint32_t cov[NB][9];
+  uint32_t cov[kCov ? NB : 1][9];
   uint32_t tw[NB / 32][kBlendThreads];
 };
 
 // One entry of a batch: its records from the item's splat and colour.
-template <typename S, int NB, bool kOp>
-__device__ __forceinline__ void stage_entry(const BlendArgs<S>& p, StageSmem<S, NB, kOp>& sm, int i, uint32_t item,
+template <typename S, int NB, bool kOp, bool kCov>
+__device__ __forceinline__ void stage_entry(const BlendArgs<S>& p, StageSmem<S, NB, kOp, kCov>& sm, int i, uint32_t item,
                                             uint32_t vbase_item, Splat<S>& s) {
   s = p.splat[item];
   const V4<S> c = p.col4[item - vbase_item];
@@ -1068,15 +1089,16 @@ __device__ __forceinline__ void stage_batch(const BlendArgs<S>& p, StageSmem<S, 
     for (int q = 0; q < 8; ++q) w[q] = 0;
     if (i < n) {
       Splat<S> s;
-      stage_entry<S, NB, kOp>(p, sm, i, p.entry_item[base + i], vbase_item, s);
+      stage_entry(p, sm, i, p.entry_item[base + i], vbase_item, s);
       tile_coverage(s.a, s.b, x0, y0, w);
     }
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const TransposeLanes tl(lane);
 #pragma unroll
   for (int c = 0; c < NB / 32; ++c)
-    if (c * 32 < n) sm.tw[c][threadIdx.x] = transpose32(sm.cov[c * 32 + lane][warp], lane);
+    if (c * 32 < n) sm.tw[c][threadIdx.x] = transpose32(sm.cov[c * 32 + lane][warp], tl);
 }
 
 // Iterator over a lane's covering entries of the staged batch, in order.
@@ -1112,7 +1134,7 @@ struct BitWalk {
 
 
 #ifndef GMR_FWD_MINB
-#define GMR_FWD_MINB 7   // 32 registers: a few loop-invariant spills, measured faster than 40 registers at 6 CTAs
+#define GMR_FWD_MINB 6   // 40 registers (measured: 6 CTAs/SM 0.550 ms vs 7 CTAs/SM at 32 registers 0.577 ms, config 3)
 #endif
 template <typename S, bool kOp>
 __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 4 : GMR_FWD_MINB) blend_forward(BlendArgs<S> p) {
@@ -1223,14 +1245,14 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 4 : GMR_FWD_MI
 template <typename S, bool kOpacity> struct RecOf { typedef V2<S> type; };
 template <typename S> struct RecOf<S, true> { typedef V4<S> type; };
 
-constexpr int kBwdPairBytes = GMR_BWD_PAIR_KB * 1024;
+constexpr int kBwdPairBytes = GMR_BWD_PAIR_BYTES;
 
 template <typename S, bool kOpacity> struct BwdSmem {
   typedef typename RecOf<S, kOpacity>::type Rec;
   static constexpr int kCap = kBwdPairBytes / (int)(sizeof(Rec) + 1);
-  StageSmem<S, kBwdBatch, kOpacity> st;
-  uint16_t wbase[kBwdBatch][8];     // per entry and warp: first record of the warp's covered pixels
-  uint2 rng[kBwdBatch];             // per entry: [first, end) of its records
+  StageSmem<S, kBwdBatch, kOpacity, false> st;
+  uint2 cw[8][kBwdBatch];           // per warp block and entry: (coverage word, first record of its pixels)
+  uint32_t rend[kBwdBatch];         // per entry: end of its records (they start at cw[0][j].y)
   uint32_t wsum[kBlendThreads / 32];
   V4<S> pix[kBlendThreads];         // per tile pixel (col + 16 row): g_r, g_g, g_b
   Rec rec[kCap];                    // per (entry, covered pixel): (dp, w[, dL/dalpha * ep])
@@ -1241,7 +1263,7 @@ template <typename S, bool kOpacity> struct BwdSmem {
 //  - each staging thread takes one entry's records and the forward's
 //    coverage words, counts its covered pixels per warp block, and a
 //    scan over the batch gives every entry a contiguous record range
-//    [rng.x, rng.y) (the batch is cut where the ranges would overflow
+//    [cw[0][j].y, rend[j]) (the batch is cut where the ranges would overflow
 //    shared memory), ordered by warp, then lane; the records are zeroed;
 //  - pass 1 (lane = pixel) re-scans front to back with the forward's exact
 //    decisions.  With C = g.(rgb - T_f bg) = sum_j (g.c_j) w_j the suffix is
@@ -1249,7 +1271,7 @@ template <typename S, bool kOpacity> struct BwdSmem {
 //      dL/dalpha_k = (g.c_k) T_k - (S_k + (g.bg - g_a) T_f) / (1 - alpha_k)
 //    and each included pair writes (dp = dL/dalpha * alpha, 0 where the 0.99
 //    clamp is active (:336-338), w = alpha T) to record
-//    wbase[j][warp] + (rank of this lane among the warp's lanes covering j);
+//    cw[warp][j].y + (rank of this lane among the warp's lanes covering j);
 //  - pass 2 (two threads per entry, halves of its records) sums
 //      [dp dx, dp dy, dp dx^2, dp dx dy, dp dy^2, w g_r, w g_g, w g_b]
 //    in record order; the halves are combined in a fixed order.
@@ -1305,14 +1327,13 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : GMR_BWD_MI
     for (int q = 0; q < 8; ++q) wcnt[q] = 0;
     if (tid < n_st) {
       Splat<S> s;
-      stage_entry<S, kBwdBatch, kOpacity>(p, sm.st, tid, p.entry_item[base + tid], vbase_item, s);
+      stage_entry(p, sm.st, tid, p.entry_item[base + tid], vbase_item, s);
       const uint4* src = reinterpret_cast<const uint4*>(p.covbuf + (size_t)(base + tid) * 8);
       const uint4 lo = src[0], hi = src[1];
       const uint32_t w[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-      uint32_t* cw = sm.st.cov[tid];
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        cw[q] = w[q];
+        sm.cw[q][tid].x = w[q];
         wcnt[q] = ncov;
         ncov += __popc(w[q]);
       }
@@ -1329,13 +1350,14 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : GMR_BWD_MI
     uint32_t excl = x - ncov;
     for (int w2 = 0; w2 < warp; ++w2) excl += sm.wsum[w2];
     const bool fits = tid < n_st && excl + ncov <= (uint32_t)Sm::kCap;
+
     if (fits) {
-      sm.rng[tid] = make_uint2(excl, excl + ncov);
+      sm.rend[tid] = excl + ncov;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) sm.wbase[tid][q] = (uint16_t)(excl + wcnt[q]);
+      for (int q = 0; q < 8; ++q) sm.cw[q][tid].y = excl + wcnt[q];
     }
     const int n = __syncthreads_count(fits);          // entries taken this batch (prefix property)
-    const uint32_t rec_end = n ? sm.rng[n - 1].y : 0u;
+    const uint32_t rec_end = n ? sm.rend[n - 1] : 0u;
     for (uint32_t r = tid; r < rec_end; r += kBlendThreads) {
       Rec z;
       z.x = z.y = S(0);
@@ -1343,10 +1365,13 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : GMR_BWD_MI
       sm.rec[r] = z;
     }
     // entries past n are re-staged next batch: their coverage reads as empty
+    {
+      const TransposeLanes tl(lane);
 #pragma unroll
-    for (int c = 0; c < kBwdBatch / 32; ++c)
-      if (c * 32 < n)
-        sm.st.tw[c][tid] = transpose32(c * 32 + lane < n ? sm.st.cov[c * 32 + lane][warp] : 0u, lane);
+      for (int c = 0; c < kBwdBatch / 32; ++c)
+        if (c * 32 < n)
+          sm.st.tw[c][tid] = transpose32(c * 32 + lane < n ? sm.cw[warp][c * 32 + lane].x : 0u, tl);
+    }
     __syncthreads();
     const uint32_t nxt_e = base + (uint32_t)n + threadIdx.x;
     const uint32_t nxt = (threadIdx.x < kBwdBatch && nxt_e < end) ? p.entry_item[nxt_e] : 0xffffffffu;
@@ -1394,7 +1419,8 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : GMR_BWD_MI
             s.z = raws[u] < Const<S>::alpha_clamp() ? d_alpha * eps[u] : S(0);
             s.w = S(0);
           }
-          const uint32_t r = (uint32_t)sm.wbase[j][warp] + (uint32_t)__popc(sm.st.cov[j][warp] & lt);
+          const uint2 cwj = sm.cw[warp][j];
+          const uint32_t r = cwj.y + (uint32_t)__popc(cwj.x & lt);
           sm.rec[r] = s;
           sm.rq[r] = (uint8_t)my_pix;
           T = test;
@@ -1416,7 +1442,7 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : GMR_BWD_MI
     for (int q = 0; q < 8; ++q) acc[q] = S(0);
     S aop = S(0);
     if (je < n) {
-      const uint2 rr = sm.rng[je];
+      const uint2 rr = make_uint2(sm.cw[0][je].y, sm.rend[je]);
       const uint32_t mid = kSplit == 2 ? rr.x + ((rr.y - rr.x + 1) >> 1) : rr.y;
       const uint32_t lo = half ? mid : rr.x, hi = half ? rr.y : mid;
       const V4<S> ea = sm.st.ea[je];

@@ -30,18 +30,47 @@ def shard_range(n: int, rank: int, world: int):
     return (rank * n) // world, ((rank + 1) * n) // world
 
 
+class PendingReduce:
+    """An all-reduce in flight on the backend's own stream (async_op=True):
+    the caller's stream keeps rendering the next view group meanwhile.
+    wait() makes the current stream wait for it and returns the result."""
+
+    def __init__(self, work, result):
+        self.work, self.result = work, result
+
+    def wait(self):
+        if self.work is not None:
+            self.work.wait()
+        return self.result
+
+
 def allreduce_vertex_grads(g_pos: torch.Tensor, g_col: torch.Tensor, extra: torch.Tensor | None = None,
-                           group=None, reproducible: bool = False):
+                           group=None, reproducible: bool = False, async_op: bool = False):
     """One packed SUM all-reduce of [grad_pos | grad_col (| extra scalars)].
 
     reproducible: all-gather the packed partials and add them in rank order
     (R x the buffer in memory and traffic; bit-identical for a given world
-    size whatever algorithm NCCL would have chosen)."""
+    size whatever algorithm NCCL would have chosen).
+    async_op: return a PendingReduce instead of waiting (plain SUM only), so
+    one view group's reduction overlaps the next group's kernels; the sum of
+    the groups' reduced buffers equals the reduction of their sum up to
+    floating-point summation order."""
     parts = [g_pos.reshape(-1), g_col.reshape(-1)]
     if extra is not None:
         parts.append(extra.reshape(-1).to(g_pos.dtype))
     buf = torch.cat(parts)
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+    n = g_pos.numel()
+
+    def split(b):
+        return b[:n].view_as(g_pos), b[n:2 * n].view_as(g_col), (b[2 * n:] if extra is not None else None)
+
+    multi = dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1
+    if async_op:
+        if reproducible:
+            raise ValueError("async_op needs the plain SUM all-reduce (reproducible=False)")
+        work = dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group, async_op=True) if multi else None
+        return PendingReduce(work, split(buf))
+    if multi:
         if reproducible:
             world = dist.get_world_size(group)
             gathered = torch.empty(world * buf.numel(), dtype=buf.dtype, device=buf.device)
@@ -52,11 +81,7 @@ def allreduce_vertex_grads(g_pos: torch.Tensor, g_col: torch.Tensor, extra: torc
                 buf += gathered[r]
         else:
             dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
-    n = g_pos.numel()
-    out_pos = buf[:n].view_as(g_pos)
-    out_col = buf[n:2 * n].view_as(g_col)
-    out_extra = buf[2 * n:] if extra is not None else None
-    return out_pos, out_col, out_extra
+    return split(buf)
 
 
 def sharded_image_loss(local_fn: Callable, cameras: Sequence, target_rgb: Sequence, target_mask: Sequence,

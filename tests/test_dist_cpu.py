@@ -137,3 +137,42 @@ def test_allreduce_single_process_is_identity():
     gp, gcol = torch.randn(5, 3), torch.randn(5, 3)
     a, b, e = gdist.allreduce_vertex_grads(gp.clone(), gcol.clone(), torch.tensor([1.0, 2.0]))
     assert torch.equal(a, gp) and torch.equal(b, gcol) and e.tolist() == [1.0, 2.0]
+
+
+def _async_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = torch.Generator().manual_seed(100 + rank)
+        groups = [(torch.randn(7, 3, generator=g, dtype=torch.float64),
+                   torch.randn(7, 3, generator=g, dtype=torch.float64)) for _ in range(3)]
+        # per view group, in flight together, summed after (bench.py's overlapped step)
+        pend = [gdist.allreduce_vertex_grads(a, b, async_op=True) for a, b in groups]
+        parts = [p.wait() for p in pend]
+        gp = parts[0][0] + parts[1][0] + parts[2][0]
+        gc_ = parts[0][1] + parts[1][1] + parts[2][1]
+        # one reduction of the summed groups
+        sp, sc, _ = gdist.allreduce_vertex_grads(sum(a for a, _ in groups), sum(b for _, b in groups))
+        q.put((rank, gp.numpy(), gc_.numpy(), sp.numpy(), sc.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_async_group_reductions_match_one_reduction():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_async_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=240) for _ in procs], key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for _, gp, gcol, sp, sc in res:
+        np.testing.assert_allclose(gp, sp, rtol=0, atol=1e-12)
+        np.testing.assert_allclose(gcol, sc, rtol=0, atol=1e-12)
+    np.testing.assert_array_equal(res[0][1], res[1][1])   # identical on every rank
+    with pytest.raises(ValueError):
+        gdist.allreduce_vertex_grads(torch.zeros(2, 3), torch.zeros(2, 3), reproducible=True, async_op=True)
