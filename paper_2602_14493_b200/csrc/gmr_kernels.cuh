@@ -1045,7 +1045,10 @@ __device__ __forceinline__ void prefetch_records(const BlendArgs<S>& p, uint32_t
 #ifndef GMR_BWD_MINB
 #define GMR_BWD_MINB 5
 #endif
-constexpr int kFwdBatch = 256;
+#ifndef GMR_FWD_BATCH
+#define GMR_FWD_BATCH 256
+#endif
+constexpr int kFwdBatch = GMR_FWD_BATCH;
 constexpr int kBwdBatch = GMR_BWD_BATCH;
 
 // A staged batch.  Per entry two 16-byte (float) records, read with two
@@ -1081,8 +1084,8 @@ __device__ __forceinline__ void stage_entry(const BlendArgs<S>& p, StageSmem<S, 
 // coverage rows (i >= n: empty mask), then every warp transposes its
 // coverage words into per-pixel bit lists.
 template <typename S, int NB, bool kOp>
-__device__ __forceinline__ void stage_batch(const BlendArgs<S>& p, StageSmem<S, NB, kOp>& sm, uint32_t base, int n,
-                                            uint32_t vbase_item, int x0, int y0) {
+__device__ __forceinline__ uint32_t stage_batch(const BlendArgs<S>& p, StageSmem<S, NB, kOp>& sm, uint32_t base,
+                                                int n, uint32_t vbase_item, int x0, int y0) {
   for (int i = threadIdx.x; i < NB; i += kBlendThreads) {
     uint32_t* w = sm.cov[i];
 #pragma unroll
@@ -1096,20 +1099,28 @@ __device__ __forceinline__ void stage_batch(const BlendArgs<S>& p, StageSmem<S, 
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const TransposeLanes tl(lane);
+  uint32_t cmask = 0;   // chunks holding at least one candidate of this thread's pixel
 #pragma unroll
   for (int c = 0; c < NB / 32; ++c)
-    if (c * 32 < n) sm.tw[c][threadIdx.x] = transpose32(sm.cov[c * 32 + lane][warp], tl);
+    if (c * 32 < n) {
+      const uint32_t x = transpose32(sm.cov[c * 32 + lane][warp], tl);
+      sm.tw[c][threadIdx.x] = x;
+      cmask |= (x != 0u) << c;
+    }
+  return cmask;
 }
 
 // Iterator over a lane's covering entries of the staged batch, in order.
+// `cmask` (bit c: chunk c holds a candidate of this lane, from the
+// transposes) lets a refill jump straight to the next non-empty chunk.
 struct BitWalk {
-  int c, nch;
-  uint32_t bits;
+  int base;
+  uint32_t bits, cmask;
   template <int NB>
-  __device__ __forceinline__ void start(const uint32_t (&tw)[NB / 32][kBlendThreads], int n, bool skip) {
-    nch = skip ? 0 : (n + 31) >> 5;
-    c = 0;
-    bits = nch ? tw[0][threadIdx.x] : 0u;
+  __device__ __forceinline__ void start(const uint32_t (&tw)[NB / 32][kBlendThreads], uint32_t chunks, bool skip) {
+    cmask = skip ? 0u : chunks;
+    bits = 0u;
+    base = 0;
   }
   // Up to two candidates from the current chunk (j2 = -1 if it has only one
   // left); refills from the next non-empty chunk only when the current one
@@ -1117,19 +1128,19 @@ struct BitWalk {
   template <int NB>
   __device__ __forceinline__ bool pair(const uint32_t (&tw)[NB / 32][kBlendThreads], int& j1, int& j2) {
     if (__builtin_expect(bits == 0, 0)) {
-      do {
-        if (++c >= nch) return false;
-        bits = tw[c][threadIdx.x];
-      } while (!bits);
+      if (!cmask) return false;
+      const int c = __ffs(cmask) - 1;
+      cmask &= cmask - 1;
+      bits = tw[c][threadIdx.x];
+      base = c << 5;
     }
-    const int base = c << 5;
     j1 = base + __ffs(bits) - 1;
     bits &= bits - 1;
     j2 = bits ? base + __ffs(bits) - 1 : -1;
     bits &= bits - 1;   // no-op when empty
     return true;
   }
-  __device__ __forceinline__ void stop() { bits = 0; nch = 0; }
+  __device__ __forceinline__ void stop() { bits = 0; cmask = 0; }
 };
 
 
@@ -1154,7 +1165,7 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 4 : GMR_FWD_MI
   for (uint32_t base = start; base < end; base += kFwdBatch) {
     if (__syncthreads_count(done) == kBlendThreads) break;
     const int n = (int)min((uint32_t)kFwdBatch, end - base);
-    stage_batch<S, kFwdBatch, kOp>(p, sm, base, n, vbase_item, x0, y0);
+    const uint32_t chunks = stage_batch<S, kFwdBatch, kOp>(p, sm, base, n, vbase_item, x0, y0);
     __syncthreads();
     if (p.covbuf) {   // keep the coverage masks for the backward (coalesced 32-byte rows)
       for (int i = threadIdx.x; i < n; i += kBlendThreads) {
@@ -1167,7 +1178,7 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 4 : GMR_FWD_MI
     const uint32_t nxt_e = base + kFwdBatch + threadIdx.x;
     const uint32_t nxt = nxt_e < end ? p.entry_item[nxt_e] : 0xffffffffu;
     BitWalk it;
-    it.start<kFwdBatch>(sm.tw, n, done);
+    it.start<kFwdBatch>(sm.tw, chunks, done);
     // two candidates per trip: their alphas are independent, only the
     // transmittance update is sequential (front-to-back order kept)
     for (int j1, j2; it.pair<kFwdBatch>(sm.tw, j1, j2);) {
@@ -1215,7 +1226,7 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 4 : GMR_FWD_MI
       }
     }
     prefetch_records(p, nxt, vbase_item);
-    __syncthreads();
+    // no barrier here: the next batch's __syncthreads_count is one
   }
   double sq = 0.0, bce = 0.0;
   if (inside) {
@@ -1365,12 +1376,16 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : GMR_BWD_MI
       sm.rec[r] = z;
     }
     // entries past n are re-staged next batch: their coverage reads as empty
+    uint32_t chunks = 0;   // chunks holding at least one candidate of this thread's pixel
     {
       const TransposeLanes tl(lane);
 #pragma unroll
       for (int c = 0; c < kBwdBatch / 32; ++c)
-        if (c * 32 < n)
-          sm.st.tw[c][tid] = transpose32(c * 32 + lane < n ? sm.cw[warp][c * 32 + lane].x : 0u, tl);
+        if (c * 32 < n) {
+          const uint32_t x = transpose32(c * 32 + lane < n ? sm.cw[warp][c * 32 + lane].x : 0u, tl);
+          sm.st.tw[c][tid] = x;
+          chunks |= (x != 0u) << c;
+        }
     }
     __syncthreads();
     const uint32_t nxt_e = base + (uint32_t)n + threadIdx.x;
@@ -1378,7 +1393,7 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : GMR_BWD_MI
     // ---- pass 1: my pixel (two candidates per trip, sequential T) ----
     {
       BitWalk it;
-      it.start<kBwdBatch>(sm.st.tw, n, done);
+      it.start<kBwdBatch>(sm.st.tw, chunks, done);
       for (int j1, j2; it.pair<kBwdBatch>(sm.st.tw, j1, j2);) {
         int js[2] = {j1, j2};
         S as[2], eps[2], raws[2];
