@@ -1111,13 +1111,17 @@ __device__ __forceinline__ uint32_t stage_batch(const BlendArgs<S>& p, StageSmem
 }
 
 // Iterator over a lane's covering entries of the staged batch, in order.
-// `cmask` (bit c: chunk c holds a candidate of this lane, from the
-// transposes) lets a refill jump straight to the next non-empty chunk.
+// `col` points at the lane's word of chunk 0 of the transposed candidate
+// bits, chunk c at col[c * kStride]; `cmask` (bit c: chunk c holds a
+// candidate of this lane, from the transposes) lets a refill jump straight
+// to the next non-empty chunk.
+template <int kStride>
 struct BitWalk {
+  const uint32_t* col;
   int base;
   uint32_t bits, cmask;
-  template <int NB>
-  __device__ __forceinline__ void start(const uint32_t (&tw)[NB / 32][kBlendThreads], uint32_t chunks, bool skip) {
+  __device__ __forceinline__ void start(const uint32_t* lane_col, uint32_t chunks, bool skip) {
+    col = lane_col;
     cmask = skip ? 0u : chunks;
     bits = 0u;
     base = 0;
@@ -1125,13 +1129,12 @@ struct BitWalk {
   // Up to two candidates from the current chunk (j2 = -1 if it has only one
   // left); refills from the next non-empty chunk only when the current one
   // is exhausted, so the common path is straight-line.  false = done.
-  template <int NB>
-  __device__ __forceinline__ bool pair(const uint32_t (&tw)[NB / 32][kBlendThreads], int& j1, int& j2) {
+  __device__ __forceinline__ bool pair(int& j1, int& j2) {
     if (__builtin_expect(bits == 0, 0)) {
       if (!cmask) return false;
       const int c = __ffs(cmask) - 1;
       cmask &= cmask - 1;
-      bits = tw[c][threadIdx.x];
+      bits = col[c * kStride];
       base = c << 5;
     }
     j1 = base + __ffs(bits) - 1;
@@ -1177,11 +1180,11 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 4 : GMR_FWD_MI
     }
     const uint32_t nxt_e = base + kFwdBatch + threadIdx.x;
     const uint32_t nxt = nxt_e < end ? p.entry_item[nxt_e] : 0xffffffffu;
-    BitWalk it;
-    it.start<kFwdBatch>(sm.tw, chunks, done);
+    BitWalk<kBlendThreads> it;
+    it.start(&sm.tw[0][threadIdx.x], chunks, done);
     // two candidates per trip: their alphas are independent, only the
     // transmittance update is sequential (front-to-back order kept)
-    for (int j1, j2; it.pair<kFwdBatch>(sm.tw, j1, j2);) {
+    for (int j1, j2; it.pair(j1, j2);) {
       const V4<S> a1 = sm.ea[j1], b1 = sm.eb[j1];
       S ep, raw;
       const S al1 = Eval<S>::template alpha<kOp>(sub_rn(fpx, a1.x), sub_rn(fpy, a1.y), a1.z, a1.w, b1.x,
@@ -1392,9 +1395,9 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : GMR_BWD_MI
     const uint32_t nxt = (threadIdx.x < kBwdBatch && nxt_e < end) ? p.entry_item[nxt_e] : 0xffffffffu;
     // ---- pass 1: my pixel (two candidates per trip, sequential T) ----
     {
-      BitWalk it;
-      it.start<kBwdBatch>(sm.st.tw, chunks, done);
-      for (int j1, j2; it.pair<kBwdBatch>(sm.st.tw, j1, j2);) {
+      BitWalk<kBlendThreads> it;
+      it.start(&sm.st.tw[0][tid], chunks, done);
+      for (int j1, j2; it.pair(j1, j2);) {
         int js[2] = {j1, j2};
         S as[2], eps[2], raws[2];
         V4<S> bs[2];
