@@ -943,6 +943,29 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x, const TransposeLanes
   return x;
 }
 
+// Opaque copies: the compiler must keep these per-thread constants in
+// registers instead of re-deriving them from threadIdx.x in every loop trip
+// (it does that under the occupancy's register cap; measured per variant).
+__device__ __forceinline__ float pin(float x) { asm volatile("" : "+f"(x)); return x; }
+__device__ __forceinline__ double pin(double x) { asm volatile("" : "+d"(x)); return x; }
+__device__ __forceinline__ int pin(int x) { asm volatile("" : "+r"(x)); return x; }
+#ifndef GMR_PIN_CONSTS
+#define GMR_PIN_CONSTS 1
+#endif
+#ifndef GMR_PIN_FWD
+#define GMR_PIN_FWD 1
+#endif
+#if GMR_PIN_CONSTS
+#define GMR_PIN(x) pin(x)
+#else
+#define GMR_PIN(x) (x)
+#endif
+#if GMR_PIN_FWD
+#define GMR_PIN_F(x) pin(x)
+#else
+#define GMR_PIN_F(x) (x)
+#endif
+
 // Pixel layout of a tile CTA: warp w owns the 8x4 block at columns
 // 8 (w & 1) .. +7, rows 4 (w >> 1) .. +3; lane l is column l & 7, row l >> 3
 // of it.  Square blocks keep a warp's lanes on nearly the same splats.
@@ -1159,7 +1182,7 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 4 : GMR_FWD_MI
   const int x0 = tx * kTile, y0 = ty * kTile;
   const int px = x0 + tile_col(threadIdx.x), py = y0 + tile_row(threadIdx.x);
   const bool inside = px < p.W && py < p.H;
-  const S fpx = S(px), fpy = S(py);
+  const S fpx = GMR_PIN_F(S(px)), fpy = GMR_PIN_F(S(py));
   const S one = S(1);
   S T = one, ar = 0, ag = 0, ab = 0;
   bool done = !inside;
@@ -1303,7 +1326,7 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : GMR_BWD_MI
   const int x0 = tx * kTile, y0 = ty * kTile;
   const int px = x0 + tile_col(threadIdx.x), py = y0 + tile_row(threadIdx.x);
   const bool inside = px < p.W && py < p.H;
-  const S fpx = S(px), fpy = S(py);
+  const S fpx = GMR_PIN(S(px)), fpy = GMR_PIN(S(py));
   const S one = S(1);
   const unsigned lt = lanemask_lt();
   S Ctot = 0, bterm = 0;
@@ -1319,7 +1342,7 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : GMR_BWD_MI
   }
   // per-pixel data and record pixel ids use the natural tile index
   // col + 16 row (pass 2 recovers the offsets with two bit operations)
-  const int my_pix = tile_col(tid) + 16 * tile_row(tid);
+  const int my_pix = GMR_PIN(tile_col(tid) + 16 * tile_row(tid));
   sm.pix[my_pix] = mypix;
   S T = one, P = 0;
   bool done = !inside;
