@@ -1062,8 +1062,20 @@ __device__ __forceinline__ void prefetch_records(const BlendArgs<S>& p, uint32_t
 #ifndef GMR_BWD_BATCH
 #define GMR_BWD_BATCH 128
 #endif
+#ifndef GMR_BWD_TMA
+// 1: the coverage rows of the next batch arrive by a 1-D bulk copy (TMA
+// engine, UBLKCP + mbarrier) issued one batch ahead.  Measured slower
+// (1.171 -> 1.274 ms at config 3): its 4 KB buffer comes out of the record
+// buffer at 5 CTAs/SM, so batches are cut shorter.  Kept as the option.
+#define GMR_BWD_TMA 0
+#endif
+
 #ifndef GMR_BWD_PAIR_BYTES
+#if GMR_BWD_TMA
+#define GMR_BWD_PAIR_BYTES 20224   // less the 4 KB coverage staging buffer
+#else
 #define GMR_BWD_PAIR_BYTES 24448   // 24 KB less 128 B: keeps BwdSmem<float> at 5 CTAs per SM
+#endif
 #endif
 #ifndef GMR_BWD_MINB
 #define GMR_BWD_MINB 5
@@ -1279,6 +1291,29 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 4 : GMR_FWD_MI
   if (p.target_rgb) block_sum2(sq, bce, p.loss_tile + 2 * (size_t)g);
 }
 
+// 1-D bulk copies (TMA engine, cp.async.bulk) completing on an mbarrier.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// One thread: arm the barrier with `bytes` and start the copy global -> shared.
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // prior generic reads of dst before the async write
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+
 template <typename S, bool kOpacity> struct RecOf { typedef V2<S> type; };
 template <typename S> struct RecOf<S, true> { typedef V4<S> type; };
 
@@ -1291,6 +1326,10 @@ template <typename S, bool kOpacity> struct BwdSmem {
   uint2 cw[8][kBwdBatch];           // per warp block and entry: (coverage word, first record of its pixels)
   uint32_t rend[kBwdBatch];         // per entry: end of its records (they start at cw[0][j].y)
   uint32_t wsum[kBlendThreads / 32];
+#if GMR_BWD_TMA
+  uint4 covq[kBwdBatch][2];         // the batch's coverage rows (bulk copy of covbuf, issued one batch ahead)
+  uint64_t bar;
+#endif
   V4<S> pix[kBlendThreads];         // per tile pixel (col + 16 row): g_r, g_g, g_b
   Rec rec[kCap];                    // per (entry, covered pixel): (dp, w[, dL/dalpha * ep])
   uint8_t rq[kCap];                 // tile pixel (col + 16 row) of each record
@@ -1348,6 +1387,17 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : GMR_BWD_MI
   bool done = !inside;
   const uint32_t start = p.bounds[g], end = p.bounds[g + 1];
   const uint32_t vbase_item = view * p.items_per_view;
+#if GMR_BWD_TMA
+  uint32_t phase = 0;
+  bool inflight = false;   // CTA-uniform: a coverage copy is outstanding
+  if (tid == 0) {
+    mbar_init(&sm.bar);
+    if (start < end)
+      bulk_load(sm.covq, p.covbuf + (size_t)start * 8, min((uint32_t)kBwdBatch, end - start) * 32u, &sm.bar);
+  }
+  inflight = start < end;
+  __syncthreads();
+#endif
   // pass 2: two threads per entry (halves of its records) for 128-entry
   // batches, one per entry for 256
   constexpr int kSplit = kBlendThreads / kBwdBatch;
@@ -1362,11 +1412,20 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : GMR_BWD_MI
     uint32_t wcnt[8];   // covered pixels of this entry in warp blocks before each warp
 #pragma unroll
     for (int q = 0; q < 8; ++q) wcnt[q] = 0;
+#if GMR_BWD_TMA
+    mbar_wait(&sm.bar, phase);
+    phase ^= 1u;
+    inflight = false;
+#endif
     if (tid < n_st) {
       Splat<S> s;
       stage_entry(p, sm.st, tid, p.entry_item[base + tid], vbase_item, s);
+#if GMR_BWD_TMA
+      const uint4 lo = sm.covq[tid][0], hi = sm.covq[tid][1];
+#else
       const uint4* src = reinterpret_cast<const uint4*>(p.covbuf + (size_t)(base + tid) * 8);
       const uint4 lo = src[0], hi = src[1];
+#endif
       const uint32_t w[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
@@ -1394,6 +1453,15 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : GMR_BWD_MI
       for (int q = 0; q < 8; ++q) sm.cw[q][tid].y = excl + wcnt[q];
     }
     const int n = __syncthreads_count(fits);          // entries taken this batch (prefix property)
+#if GMR_BWD_TMA
+    {   // every thread has read sm.covq (before the count barrier): fetch the next batch's rows
+      const uint32_t nb = base + (uint32_t)n;
+      if (nb < end) {
+        if (tid == 0) bulk_load(sm.covq, p.covbuf + (size_t)nb * 8, min((uint32_t)kBwdBatch, end - nb) * 32u, &sm.bar);
+        inflight = true;
+      }
+    }
+#endif
     const uint32_t rec_end = n ? sm.rend[n - 1] : 0u;
     for (uint32_t r = tid; r < rec_end; r += kBlendThreads) {
       Rec z;
@@ -1474,8 +1542,10 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : GMR_BWD_MI
       }
     }
     prefetch_records(p, nxt, vbase_item);
+#if !GMR_BWD_TMA
     if (nxt != 0xffffffffu)   // and the next batch's coverage words
       asm volatile("prefetch.global.L2 [%0];" ::"l"(p.covbuf + (size_t)nxt_e * 8));
+#endif
     __syncthreads();
     // ---- pass 2: my entry, my half of its records (pixel order) ----
     S acc[8];
@@ -1488,10 +1558,7 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : GMR_BWD_MI
       const uint32_t lo = half ? mid : rr.x, hi = half ? rr.y : mid;
       const V4<S> ea = sm.st.ea[je];
       const S ex0 = S(x0) - ea.x, ey0 = S(y0) - ea.y;
-      for (uint32_t r = lo; r < hi; ++r) {
-        const Rec s = sm.rec[r];
-        const int q = sm.rq[r];
-        const V4<S> pd = sm.pix[q];
+      auto add = [&](const Rec& s, int q, const V4<S>& pd) {
         const S dx = ex0 + S(q & 15), dy = ey0 + S(q >> 4);
         const S dpx = s.x * dx, dpy = s.x * dy;
         acc[0] += dpx;
@@ -1503,6 +1570,14 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : GMR_BWD_MI
         acc[6] += s.y * pd.y;
         acc[7] += s.y * pd.z;
         if constexpr (kOpacity) aop += s.z;
+      };
+      // not unrolled: measured 1.188 -> 1.171 ms at config 3 (the 4x unrolled
+      // loop serialised its loads under the 48-register cap anyway)
+#pragma unroll 1
+      for (uint32_t r = lo; r < hi; ++r) {
+        const Rec s = sm.rec[r];
+        const int q = sm.rq[r];
+        add(s, q, sm.pix[q]);
       }
     }
     // combine the two halves (fixed order) and store at the pre-sort slot
@@ -1525,6 +1600,9 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : GMR_BWD_MI
     }
     base += (uint32_t)n;
   }
+#if GMR_BWD_TMA
+  if (inflight) mbar_wait(&sm.bar, phase);   // no bulk copy may land after the CTA exits
+#endif
   // the tile finished early: entries never loaded still own a partial slot,
   // which must hold zeros (every slot is written exactly once)
   for (uint32_t e = base + threadIdx.x; e < end; e += kBlendThreads) {
