@@ -220,6 +220,7 @@ def run_gmr(args, cfg):
         # NCCL's init lines (rank count, transport) go to stderr for the record
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")   # stdout carries only the JSON line
         dist.init_process_group("nccl", device_id=dev)
     L = lib.load()
     mesh = build_mesh(cfg)

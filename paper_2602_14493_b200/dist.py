@@ -102,7 +102,7 @@ def sharded_image_loss(local_fn: Callable, cameras: Sequence, target_rgb: Sequen
     if device is None:
         # every rank must hand the collective a tensor on the backend's device,
         # including ranks whose shard is empty (more ranks than views)
-        nccl = world > 1 and dist.get_backend(group) == "nccl"
+        nccl = dist.is_available() and dist.is_initialized() and dist.get_backend(group) == "nccl"
         device = torch.device("cuda", torch.cuda.current_device()) if nccl else torch.device("cpu")
     n = len(cameras)
     lo, hi = shard_range(n, rank, world)
