@@ -210,7 +210,8 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
   if (!tile_depth_sort) {
     uint32_t* di[2] = {at<uint32_t>(ws, L.ditem[0]), at<uint32_t>(ws, L.ditem[1])};
     StageScope sc(kStDepthSort, st);
-    const int cur = radix_sort_pairs<K>(dk, di, nullptr, items, items, L.depth_bits, at<uint32_t>(ws, L.hist), st);
+    const int cur = radix_sort_pairs<K>(dk, di, nullptr, items, items, L.depth_bits, at<uint32_t>(ws, L.hist), st,
+                                        /*random_digits=*/true);
     g_launches += radix_sort_launches<K>((uint32_t)items, L.depth_bits) - 1;
     GMR_LAUNCHED();
     order = di[cur];
@@ -254,7 +255,10 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
   int ecur;
   {
     StageScope sc(kStTileSort, st);
-    ecur = radix_sort_pairs<uint32_t>(ek, ev, nent, 0, ecap, L.entry_bits, at<uint32_t>(ws, L.hist), st);
+    // entries emitted in depth order carry spatially random tile keys (ballot
+    // ranking); in item order they are coherent (match_any)
+    ecur = radix_sort_pairs<uint32_t>(ek, ev, nent, 0, ecap, L.entry_bits, at<uint32_t>(ws, L.hist), st,
+                                      /*random_digits=*/!tile_depth_sort);
     g_launches += radix_sort_launches<uint32_t>(ecap, L.entry_bits);
     tile_ranges<<<grid_for((uint64_t)ecap / 4 + 1, 256), 256, 0, st>>>(ek[ecur], nent, 0, (uint32_t)L.bins,
                                                                   at<uint32_t>(ws, L.bounds));
