@@ -207,14 +207,26 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
   const bool tile_depth_sort = (r->flags & GMR_FLAG_TILE_DEPTH_SORT) != 0;
   K* dk[2] = {at<K>(ws, L.dkey[0]), at<K>(ws, L.dkey[1])};
   const uint32_t* order = nullptr;
+  // range-reduced global depth sort: the consumers pick the result buffer on
+  // the device (order, order_alt, krange)
+  const uint32_t* order_alt = nullptr;
+  const uint32_t* krange = nullptr;
   if (!tile_depth_sort) {
     uint32_t* di[2] = {at<uint32_t>(ws, L.ditem[0]), at<uint32_t>(ws, L.ditem[1])};
     StageScope sc(kStDepthSort, st);
+    // mesh path: K1 recorded the kept splats' depth-key span in the status
+    const uint32_t* kr = unit_opacity ? &at<DevStatus>(ws, L.status)->key_lo : nullptr;
+    bool reduced = false;
     const int cur = radix_sort_pairs<K>(dk, di, nullptr, items, items, L.depth_bits, at<uint32_t>(ws, L.hist), st,
-                                        /*random_digits=*/true);
+                                        /*random_digits=*/true, kr, &reduced);
     g_launches += radix_sort_launches<K>((uint32_t)items, L.depth_bits) - 1;
     GMR_LAUNCHED();
     order = di[cur];
+    if (reduced) {
+      order = di[0];
+      order_alt = di[1];
+      krange = kr;
+    }
   }
   StageScope* emit_scope = new StageScope(kStEmit, st);
   const uint32_t* count = at<uint32_t>(ws, L.count);
@@ -223,7 +235,7 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
   uint32_t* nent = at<uint32_t>(ws, L.nent);
   DevStatus* dst = at<DevStatus>(ws, L.status);
   if (items) {
-    scan_reduce<<<nb, 256, 0, st>>>(order, count, items, bsum);
+    scan_reduce<<<nb, 256, 0, st>>>(order, order_alt, krange, L.depth_bits, count, items, bsum);
     GMR_LAUNCHED();
   }
   scan_top<<<1, kTopThreads, 0, st>>>(bsum, nb, dst, (unsigned long long)L.ecap, nent);
@@ -236,7 +248,7 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
   uint32_t* ek[2] = {at<uint32_t>(ws, L.ekey[0]), at<uint32_t>(ws, L.ekey[1])};
   uint32_t* ev[2] = {at<uint32_t>(ws, L.eval[0]), at<uint32_t>(ws, L.eval[1])};
   if (items) {
-    scan_emit<<<nb, 256, 0, st>>>(order, at<uint4>(ws, L.bin), items, bsum,
+    scan_emit<<<nb, 256, 0, st>>>(order, order_alt, krange, L.depth_bits, at<uint4>(ws, L.bin), items, bsum,
                                   (uint32_t)L.faces,
                                   L.tiles_x, (uint32_t)L.tiles, nent, ek[0], ev[0]);
     GMR_LAUNCHED();

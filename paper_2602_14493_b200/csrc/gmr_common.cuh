@@ -106,7 +106,8 @@ struct DevStatus {
   unsigned long long kept;       // items with count > 0
   unsigned int bad_item[6];      // per field: min offending item (0xffffffff = none)
   unsigned int overflow;
-  unsigned int pad[4];
+  unsigned int key_lo, key_hi;   // float32 path: min / max depth key of the kept splats (KeyRange)
+  unsigned int pad[2];
   unsigned int max_bin;          // longest (view, tile) list of the last forward (byte 60)
 };
 

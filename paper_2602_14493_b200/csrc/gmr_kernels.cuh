@@ -27,8 +27,23 @@ __global__ void reset_status(DevStatus* st) {
   st->kept = 0;
   for (int i = 0; i < 6; ++i) st->bad_item[i] = 0xffffffffu;
   st->overflow = 0;
+  st->key_lo = 0xffffffffu;
+  st->key_hi = 0u;
   st->max_bin = 0;
 }
+
+// min / max of the kept splats' 32-bit depth keys into the status (warp-
+// aggregated); the global depth sort then runs only the passes their span
+// needs (radix_sort.cuh KeyRange).  64-bit keys: no reduction.
+__device__ __forceinline__ void note_key_range(DevStatus* st, uint32_t lo, uint32_t hi) {
+  lo = __reduce_min_sync(0xffffffffu, lo);
+  hi = __reduce_max_sync(0xffffffffu, hi);
+  if ((threadIdx.x & 31) == 0 && lo <= hi) {
+    atomicMin(&st->key_lo, lo);
+    atomicMax(&st->key_hi, hi);
+  }
+}
+__device__ __forceinline__ void note_key_range(DevStatus*, unsigned long long, unsigned long long) {}
 
 __device__ __forceinline__ void flag_bad(DevStatus* st, int field, uint32_t item) {
   atomicMin(&st->bad_item[field], item);
@@ -267,6 +282,8 @@ __global__ void __launch_bounds__(256) mesh_to_splats(MeshFwdArgs<S> p, const __
   const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool live = f < p.F;
   uint32_t kept = 0;
+  typedef typename KeyOf<S>::type Key;
+  Key klo = ~(Key)0, khi = 0;
   if (live) {
     FaceGeo g;
     int32_t idx[3];
@@ -323,6 +340,8 @@ __global__ void __launch_bounds__(256) mesh_to_splats(MeshFwdArgs<S> p, const __
           cnt = item_count(emask, area);
           rc = make_uint2((uint32_t)tx0 | ((uint32_t)ty0 << 16), (uint32_t)tx1 | ((uint32_t)ty1 << 16));
           key = order_key(t[2]);
+          klo = min(klo, key);
+          khi = max(khi, key);
           ++kept;
           // render.py:191-197 on kept splats
           if (!(finite_s(mx) && finite_s(my))) flag_bad(p.st, 0, (uint32_t)item);
@@ -345,6 +364,7 @@ __global__ void __launch_bounds__(256) mesh_to_splats(MeshFwdArgs<S> p, const __
       if (p.ditem) p.ditem[item] = (uint32_t)item;
     }
   }
+  note_key_range(p.st, klo, khi);
   // warp-aggregated kept count
   uint32_t tot = kept;
 #pragma unroll
@@ -415,10 +435,12 @@ __global__ void __launch_bounds__(256) pack_splats(PackArgs<S> p) {
 
 constexpr int kScanTile = 256;   // one splat per thread
 
-__global__ void __launch_bounds__(256) scan_reduce(const uint32_t* __restrict__ order,
+__global__ void __launch_bounds__(256) scan_reduce(const uint32_t* order, const uint32_t* order_alt,
+                                                  const uint32_t* krange, int key_bits,
                                                   const uint32_t* __restrict__ count, uint32_t n,
                                                   uint32_t* __restrict__ bsum) {
   __shared__ uint32_t sw[8];
+  if (krange) order = result_buffer(order, order_alt, krange, key_bits);
   const uint32_t i = blockIdx.x * (uint32_t)kScanTile + threadIdx.x;
   const uint32_t s = i < n ? count[order ? order[i] : i] : 0u;
   uint32_t tot;
@@ -492,7 +514,8 @@ __global__ void __launch_bounds__(kTopThreads) scan_top(uint32_t* __restrict__ b
 // thread; block scan + the block's carry from scan_top), write its tile
 // entries row-major over its rectangle (render.py:218-226): key = view * T +
 // tile, value = item.  Skipped when the entries overflow.
-__global__ void __launch_bounds__(256) scan_emit(const uint32_t* __restrict__ order,
+__global__ void __launch_bounds__(256) scan_emit(const uint32_t* order, const uint32_t* order_alt,
+                                                const uint32_t* krange, int key_bits,
                                                 const uint4* __restrict__ bin, uint32_t n,
                                                 const uint32_t* __restrict__ bsum,
                                                 uint32_t items_per_view, int tiles_x,
@@ -500,6 +523,7 @@ __global__ void __launch_bounds__(256) scan_emit(const uint32_t* __restrict__ or
                                                 const uint32_t* __restrict__ n_entries,
                                                 uint32_t* __restrict__ key, uint32_t* __restrict__ val) {
   __shared__ uint32_t sw[8];
+  if (krange) order = result_buffer(order, order_alt, krange, key_bits);
   const uint32_t i = blockIdx.x * (uint32_t)kScanTile + threadIdx.x;
   const uint32_t item = i < n ? (order ? order[i] : i) : 0u;
   const uint4 bi = i < n ? bin[item] : make_uint4(0, 0, 0, 0);

@@ -50,12 +50,37 @@ __device__ __forceinline__ uint32_t sort_count(const uint32_t* n_dev, uint32_t n
   return n_dev ? *n_dev : n_host;
 }
 
+// Key-range reduction (32-bit keys): krange = {min, max} of the keys that
+// matter, written on the device before the sort (K1's depth keys of kept
+// splats).  Digits are those of key - min, and only the passes that
+// max - min needs run: a later pass exits at once.  Keys outside the range
+// (culled splats, key ~0) land anywhere; their consumers skip them.
+struct KeyRange {
+  uint32_t lo;
+  int passes;   // 8-bit passes max - lo needs (0: all keys equal or none)
+};
+__device__ __forceinline__ KeyRange key_range(const uint32_t* krange, int bits) {
+  KeyRange r{0u, (bits + 7) / 8};
+  if (krange) {
+    const uint32_t lo = krange[0], hi = krange[1];
+    r.lo = lo;
+    r.passes = hi > lo ? (39 - __clz(hi - lo)) / 8 : 0;   // bytes of hi - lo
+  }
+  return r;
+}
+template <typename K>
+__device__ __forceinline__ uint32_t sort_digit(K key, int shift, uint32_t lo) {
+  return (uint32_t)((key - (K)lo) >> shift) & 255u;
+}
+
 template <typename K>
 __global__ void __launch_bounds__(kSortThreads) radix_upsweep(const K* __restrict__ keys,
                                                               const uint32_t* n_dev,
                                                               uint32_t n_host, int shift,
                                                               uint32_t* __restrict__ hist,
-                                                              int nblocks) {
+                                                              int nblocks, const uint32_t* krange, int bits) {
+  const KeyRange kr = key_range(krange, bits);
+  if (shift >= 8 * kr.passes) return;
   __shared__ uint32_t h[kSortWarps][256];
   const int tid = threadIdx.x, warp = tid >> 5;
   for (int i = tid; i < kSortWarps * 256; i += kSortThreads) (&h[0][0])[i] = 0;
@@ -65,8 +90,7 @@ __global__ void __launch_bounds__(kSortThreads) radix_upsweep(const K* __restric
   if (base < n) {
     const uint32_t end = min(n, base + (uint32_t)kSortTile);
     for (uint32_t i = base + tid; i < end; i += kSortThreads) {
-      uint32_t d = (uint32_t)(keys[i] >> shift) & 255u;
-      atomicAdd(&h[warp][d], 1u);
+      atomicAdd(&h[warp][sort_digit(keys[i], shift, kr.lo)], 1u);
     }
   }
   __syncthreads();
@@ -109,7 +133,9 @@ __device__ __forceinline__ uint32_t block_exclusive_scan_256(uint32_t v, uint32_
 // digit total into totals[d].
 __global__ void __launch_bounds__(kSortThreads) radix_scan(uint32_t* __restrict__ hist,
                                                            uint32_t* __restrict__ totals,
-                                                           int nblocks) {
+                                                           int nblocks, const uint32_t* krange, int bits,
+                                                           int shift) {
+  if (shift >= 8 * key_range(krange, bits).passes) return;
   __shared__ uint32_t sw[kSortWarps];
   uint32_t* row = hist + (size_t)blockIdx.x * nblocks;
   uint32_t carry = 0;
@@ -152,7 +178,10 @@ template <typename K, bool kBallot>
 __global__ void __launch_bounds__(kSortThreads, 3) radix_downsweep(
     const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __restrict__ kout,
     uint32_t* __restrict__ vout, const uint32_t* n_dev, uint32_t n_host, int shift,
-    const uint32_t* __restrict__ hist, const uint32_t* __restrict__ totals, int nblocks) {
+    const uint32_t* __restrict__ hist, const uint32_t* __restrict__ totals, int nblocks,
+    const uint32_t* krange, int bits) {
+  const KeyRange kr = key_range(krange, bits);
+  if (shift >= 8 * kr.passes) return;
   extern __shared__ __align__(16) unsigned char dsm_raw[];
   DownSmem<K>& sm = *reinterpret_cast<DownSmem<K>*>(dsm_raw);
   const uint32_t n = sort_count(n_dev, n_host);
@@ -187,7 +216,7 @@ __global__ void __launch_bounds__(kSortThreads, 3) radix_downsweep(
   for (int r = 0; r < kSortPerThread; ++r) {
     const uint32_t idx = seg + r * 32 + lane;
     const bool valid = idx < n;
-    const uint32_t d = valid ? ((uint32_t)(key[r] >> shift) & 255u) : 256u;
+    const uint32_t d = valid ? sort_digit(key[r], shift, kr.lo) : 256u;
     // depth keys: digits of random floats, where the nine pipelined ballots
     // beat one long-latency match_any; tile keys: coherent digits, match_any
     const unsigned peers = kBallot ? digit_peers_ballot(d) : __match_any_sync(0xffffffffu, d);
@@ -217,7 +246,7 @@ __global__ void __launch_bounds__(kSortThreads, 3) radix_downsweep(
   for (int r = 0; r < kSortPerThread; ++r) {
     const uint32_t idx = seg + r * 32 + lane;
     if (idx < n) {
-      const uint32_t d = (uint32_t)(key[r] >> shift) & 255u;
+      const uint32_t d = sort_digit(key[r], shift, kr.lo);
       const uint32_t lp = sm.boff[d] + sm.wc[warp][d] + rank[r];
       sm.keys[lp] = key[r];
       sm.vals[lp] = vin[idx];
@@ -227,7 +256,7 @@ __global__ void __launch_bounds__(kSortThreads, 3) radix_downsweep(
   // coalesced write-out: local position i -> digit run -> global slot
   for (uint32_t i = tid; i < cnt_blk; i += kSortThreads) {
     const K k = sm.keys[i];
-    const uint32_t d = (uint32_t)(k >> shift) & 255u;
+    const uint32_t d = sort_digit(k, shift, kr.lo);
     const uint32_t pos = sm.gbase[d] + (i - sm.boff[d]);
     kout[pos] = k;
     vout[pos] = sm.vals[i];
@@ -378,7 +407,12 @@ inline void launch_small_sort(K* keys[2], uint32_t* vals[2], const uint32_t* n_d
 template <typename K>
 inline int radix_sort_pairs(K* keys[2], uint32_t* vals[2], const uint32_t* n_dev,
                             uint32_t n_host, uint32_t capacity, int bits, uint32_t* hist,
-                            cudaStream_t stream, bool random_digits = false) {
+                            cudaStream_t stream, bool random_digits = false,
+                            const uint32_t* krange = nullptr, bool* reduced = nullptr) {
+  // krange (32-bit keys, multi-block path only): see KeyRange.  *reduced
+  // tells the caller that the result buffer is then chosen on the device
+  // (result_buffer) instead of the returned index.
+  if (reduced) *reduced = false;
   const int nblocks = (int)((capacity + kSortTile - 1) / kSortTile);
   if (nblocks == 0 || bits <= 0) return 0;
   if (capacity <= SmallSortLimit<K>::value) {   // one block, one launch
@@ -398,17 +432,26 @@ inline int radix_sort_pairs(K* keys[2], uint32_t* vals[2], const uint32_t* n_dev
       radix_downsweep<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DownSmem<K>));
   (void)attr_rc;
   (void)attr_rb;
+  if (sizeof(K) != 4) krange = nullptr;
+  if (reduced) *reduced = krange != nullptr;
   int cur = 0;
   for (int shift = 0; shift < bits; shift += 8) {
     radix_upsweep<K><<<nblocks, kSortThreads, 0, stream>>>(keys[cur], n_dev, n_host, shift, hist,
-                                                           nblocks);
-    radix_scan<<<256, kSortThreads, 0, stream>>>(hist, totals, nblocks);
+                                                           nblocks, krange, bits);
+    radix_scan<<<256, kSortThreads, 0, stream>>>(hist, totals, nblocks, krange, bits, shift);
     auto down = random_digits ? radix_downsweep<K, true> : radix_downsweep<K, false>;
     down<<<nblocks, kSortThreads, sizeof(DownSmem<K>), stream>>>(
-        keys[cur], vals[cur], keys[cur ^ 1], vals[cur ^ 1], n_dev, n_host, shift, hist, totals, nblocks);
+        keys[cur], vals[cur], keys[cur ^ 1], vals[cur ^ 1], n_dev, n_host, shift, hist, totals, nblocks,
+        krange, bits);
     cur ^= 1;
   }
   return cur;
+}
+
+// Buffer holding a range-reduced sort's result: the executed passes flip it.
+__device__ __forceinline__ const uint32_t* result_buffer(const uint32_t* v0, const uint32_t* v1,
+                                                         const uint32_t* krange, int bits) {
+  return (key_range(krange, bits).passes & 1) ? v1 : v0;
 }
 
 // kernel launches of one radix_sort_pairs call

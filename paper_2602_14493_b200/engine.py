@@ -10,6 +10,7 @@ losses.py) and the batched torch entry `render_views`.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -128,8 +129,8 @@ class _TileOrder:
 
 _order = _TileOrder()
 # False: never add GMR_FLAG_TILE_DEPTH_SORT on our own (tests pin the mode
-# through DEFAULT_FLAGS)
-AUTO_TILE_ORDER = True
+# through DEFAULT_FLAGS; GMR_TILE_ORDER=global does the same for a process)
+AUTO_TILE_ORDER = os.environ.get("GMR_TILE_ORDER", "auto") != "global"
 _topologies = {}
 
 
