@@ -48,6 +48,8 @@ thread_local long long g_launches = 0;   // kernels launched by this thread (ben
   do {                                                                                   \
     ++g_launches;                                                                        \
     cudaError_t e_ = cudaGetLastError();                                                 \
+    if (e_ == cudaSuccess) e_ = g_launch_err;                                            \
+    g_launch_err = cudaSuccess;                                                          \
     if (e_ != cudaSuccess) return fail(GMR_ECUDA, "launch: %s (%s:%d)", cudaGetErrorString(e_), __FILE__, __LINE__); \
   } while (0)
 
@@ -235,10 +237,10 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
   uint32_t* nent = at<uint32_t>(ws, L.nent);
   DevStatus* dst = at<DevStatus>(ws, L.status);
   if (items) {
-    scan_reduce<<<nb, 256, 0, st>>>(order, order_alt, krange, L.depth_bits, count, items, bsum);
+    pdl_launch(scan_reduce, dim3(nb), dim3(256), 0, st, order, order_alt, krange, L.depth_bits, count, items, bsum);
     GMR_LAUNCHED();
   }
-  scan_top<<<1, kTopThreads, 0, st>>>(bsum, nb, dst, (unsigned long long)L.ecap, nent);
+  pdl_launch(scan_top, dim3(1), dim3(kTopThreads), 0, st, bsum, nb, dst, (unsigned long long)L.ecap, nent);
   GMR_LAUNCHED();
   // the status is final here (K1's non-finite items, the entry count and the
   // capacity verdict): publish it early so the host can validate the call
@@ -248,17 +250,17 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
   uint32_t* ek[2] = {at<uint32_t>(ws, L.ekey[0]), at<uint32_t>(ws, L.ekey[1])};
   uint32_t* ev[2] = {at<uint32_t>(ws, L.eval[0]), at<uint32_t>(ws, L.eval[1])};
   if (items) {
-    scan_emit<<<nb, 256, 0, st>>>(order, order_alt, krange, L.depth_bits, at<uint4>(ws, L.bin), items, bsum,
+    pdl_launch(scan_emit, dim3(nb), dim3(256), 0, st, order, order_alt, krange, L.depth_bits, at<uint4>(ws, L.bin), items, bsum,
                                   (uint32_t)L.faces,
                                   L.tiles_x, (uint32_t)L.tiles, nent, ek[0], ev[0]);
     GMR_LAUNCHED();
     // face-major partial offsets (bsum and offs are free again here)
     const int fb = (int)((L.faces + 255) / 256);
-    face_counts<<<fb, 256, 0, st>>>(count, (uint32_t)L.faces, L.views, at<uint32_t>(ws, L.offs), bsum);
+    pdl_launch(face_counts, dim3(fb), dim3(256), 0, st, count, (uint32_t)L.faces, L.views, at<uint32_t>(ws, L.offs), bsum);
     GMR_LAUNCHED();
-    scan_inplace<<<1, kTopThreads, 0, st>>>(bsum, fb);
+    pdl_launch(scan_inplace, dim3(1), dim3(kTopThreads), 0, st, bsum, fb);
     GMR_LAUNCHED();
-    item_offsets<<<fb, 256, 0, st>>>(count, (uint32_t)L.faces, L.views, at<uint32_t>(ws, L.offs), bsum,
+    pdl_launch(item_offsets, dim3(fb), dim3(256), 0, st, count, (uint32_t)L.faces, L.views, at<uint32_t>(ws, L.offs), bsum,
                                      at<uint32_t>(ws, L.entry_off));
     GMR_LAUNCHED();
   }
@@ -272,11 +274,11 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
     ecur = radix_sort_pairs<uint32_t>(ek, ev, nent, 0, ecap, L.entry_bits, at<uint32_t>(ws, L.hist), st,
                                       /*random_digits=*/!tile_depth_sort);
     g_launches += radix_sort_launches<uint32_t>(ecap, L.entry_bits);
-    tile_ranges<<<grid_for((uint64_t)ecap / 4 + 1, 256), 256, 0, st>>>(ek[ecur], nent, 0, (uint32_t)L.bins,
+    pdl_launch(tile_ranges, dim3(grid_for((uint64_t)ecap / 4 + 1, 256)), dim3(256), 0, st, ek[ecur], nent, 0, (uint32_t)L.bins,
                                                                   at<uint32_t>(ws, L.bounds));
     GMR_LAUNCHED();
     if (L.bins) {
-      tile_schedule<<<1, kSchedThreads, 0, st>>>(at<uint32_t>(ws, L.bounds), (uint32_t)L.bins,
+      pdl_launch(tile_schedule, dim3(1), dim3(kSchedThreads), 0, st, at<uint32_t>(ws, L.bounds), (uint32_t)L.bins,
                                                  at<uint32_t>(ws, L.sched), dst);
       GMR_LAUNCHED();
     }
@@ -288,7 +290,7 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
     K* gk0 = at<K>(ws, L.partial);
     K* gk1 = gk0 + ecap;
     uint32_t* gv1 = reinterpret_cast<uint32_t*>(gk1 + ecap);
-    bin_depth_sort<K><<<(unsigned)L.bins, kBinSortThreads, 0, st>>>(at<uint32_t>(ws, L.bounds),
+    pdl_launch(bin_depth_sort<K>, dim3((unsigned)L.bins), dim3(kBinSortThreads), 0, st, at<uint32_t>(ws, L.bounds),
                                                                     at<uint32_t>(ws, L.sched), dk[0], ev[ecur],
                                                                     gk0, gk1, gv1);
     GMR_LAUNCHED();
@@ -342,12 +344,12 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
     }();
     GMR_CUDA(attr_rc);
     // mesh splats all have opacity 1 (convert.py:326): the evaluator skips the product
-    if (unit_opacity) blend_forward<S, false><<<(unsigned)L.bins, kBlendThreads, 0, st>>>(a);
-    else blend_forward<S, true><<<(unsigned)L.bins, kBlendThreads, 0, st>>>(a);
+    if (unit_opacity) pdl_launch(blend_forward<S, false>, dim3((unsigned)L.bins), dim3(kBlendThreads), 0, st, a);
+    else pdl_launch(blend_forward<S, true>, dim3((unsigned)L.bins), dim3(kBlendThreads), 0, st, a);
     GMR_LAUNCHED();
   }
   if (la && L.bins) {
-    loss_reduce<<<1, 256, 0, st>>>(at<double>(ws, L.loss_tile), (uint32_t)L.bins, la->sums);
+    pdl_launch(loss_reduce, dim3(1), dim3(256), 0, st, at<double>(ws, L.loss_tile), (uint32_t)L.bins, la->sums);
     GMR_LAUNCHED();
   }
   return GMR_OK;
@@ -357,7 +359,7 @@ template <typename S>
 int render_forward_t(const GmrMesh* m, const GmrCamera* cams, int B, const GmrRaster* r, void* rgb,
                      void* alpha, void* ws, const Layout& L, cudaStream_t st, const LossArgs* la = nullptr,
                      const ImageArgs* ia = nullptr, void* status_host = nullptr, void* status_event = nullptr) {
-  reset_status<<<1, 1, 0, st>>>(at<DevStatus>(ws, L.status));
+  pdl_launch(reset_status, dim3(1), dim3(1), 0, st, at<DevStatus>(ws, L.status));
   GMR_LAUNCHED();
   const uint64_t F = L.faces;
   for (int v0 = 0; v0 < B; v0 += kMaxViewsPerLaunch) {
@@ -385,7 +387,7 @@ int render_forward_t(const GmrMesh* m, const GmrCamera* cams, int B, const GmrRa
     a.st = at<DevStatus>(ws, L.status);
     if (F) {
       StageScope sc(kStProject, st);
-      mesh_to_splats<S><<<grid_for(F, 256), 256, 0, st>>>(a, make_cams<S>(cams, v0, nv));
+      pdl_launch(mesh_to_splats<S>, dim3(grid_for(F, 256)), dim3(256), 0, st, a, make_cams<S>(cams, v0, nv));
       GMR_LAUNCHED();
     }
   }
@@ -437,7 +439,7 @@ int blend_backward_launch(const Layout& L, void* ws, const GmrRaster* r, const v
   GMR_CUDA(attr_rc);
   if (L.bins) {
     StageScope sc(kStBlendBwd, st);
-    blend_backward<S, kOpacity><<<(unsigned)L.bins, kBlendThreads, dyn, st>>>(a);
+    pdl_launch(blend_backward<S, kOpacity>, dim3((unsigned)L.bins), dim3(kBlendThreads), dyn, st, a);
     GMR_LAUNCHED();
   }
   return GMR_OK;
@@ -469,7 +471,7 @@ int render_backward_t(const GmrMesh* m, const GmrCamera* cams, int B, const GmrR
     a.st = at<DevStatus>(ws, L.status);
     if (F) {
       StageScope sc(kStFaceBwd, st);
-      face_views_backward<S><<<grid_for(F, 128), 128, 0, st>>>(a, make_cams<S>(cams, v0, nv));
+      pdl_launch(face_views_backward<S>, dim3(grid_for(F, 128)), dim3(128), 0, st, a, make_cams<S>(cams, v0, nv));
       GMR_LAUNCHED();
     }
   }
@@ -477,7 +479,7 @@ int render_backward_t(const GmrMesh* m, const GmrCamera* cams, int B, const GmrR
   const uint32_t* slots = vstart + align_up((V + 1) * 4) / 4;
   if (V) {
     StageScope sc(kStVertex, st);
-    vertex_gather<S><<<grid_for(V, 256), 256, 0, st>>>(vstart, slots, (int64_t)V, (int64_t)F,
+    pdl_launch(vertex_gather<S>, dim3(grid_for(V, 256)), dim3(256), 0, st, vstart, slots, (int64_t)V, (int64_t)F,
                                                        at<S>(ws, L.corner), (S*)g_pos, (S*)g_col);
     GMR_LAUNCHED();
   }
@@ -497,7 +499,7 @@ int check_mesh(const GmrMesh* m) {
 template <typename S>
 int rasterize_forward_t(const GmrSplats* sp, const GmrRaster* r, void* rgb, void* alpha, void* ws,
                         const Layout& L, cudaStream_t st) {
-  reset_status<<<1, 1, 0, st>>>(at<DevStatus>(ws, L.status));
+  pdl_launch(reset_status, dim3(1), dim3(1), 0, st, at<DevStatus>(ws, L.status));
   GMR_LAUNCHED();
   PackArgs<S> a{};
   a.mean2d = (const S*)sp->mean2d;
@@ -517,7 +519,7 @@ int rasterize_forward_t(const GmrSplats* sp, const GmrRaster* r, void* rgb, void
   a.cull = (r->flags & GMR_FLAG_FULL_TILE_LISTS) ? 0 : 1;
   a.st = at<DevStatus>(ws, L.status);
   if (sp->count) {
-    pack_splats<S><<<grid_for(sp->count, 256), 256, 0, st>>>(a);
+    pdl_launch(pack_splats<S>, dim3(grid_for(sp->count, 256)), dim3(256), 0, st, a);
     GMR_LAUNCHED();
   }
   return bin_and_blend<S>(L, ws, r, rgb, alpha, st, false);
@@ -538,7 +540,7 @@ int rasterize_backward_t(const GmrSplats* sp, const GmrRaster* r, const void* rg
   int rc = blend_backward_launch<S, true>(L, ws, r, rgb, g_rgb, g_alpha, st);
   if (rc) return rc;
   if (sp->count) {
-    splat_grads<S><<<grid_for(sp->count, 256), 256, 0, st>>>(
+    pdl_launch(splat_grads<S>, dim3(grid_for(sp->count, 256)), dim3(256), 0, st,
         at<uint32_t>(ws, L.count), at<uint32_t>(ws, L.entry_off), at<Splat<S>>(ws, L.splat),
         at<S>(ws, L.partial), at<S>(ws, L.partial_op), sp->count, at<DevStatus>(ws, L.status), (S*)gm, (S*)gc,
         (S*)gcol, (S*)gop);
@@ -554,15 +556,15 @@ int convert_backward_t(const GmrMesh* m, int rescale, const void* gm, const void
   double* acc = (double*)scratch;
   S* corner = (S*)((char*)scratch + align_up(F * 12 * 8));
   if (F) {
-    pack_face_grads<S><<<grid_for(F, 256), 256, 0, st>>>((const S*)gm, (const S*)gc, (const S*)gcol, F, acc);
+    pdl_launch(pack_face_grads<S>, dim3(grid_for(F, 256)), dim3(256), 0, st, (const S*)gm, (const S*)gc, (const S*)gcol, F, acc);
     GMR_LAUNCHED();
-    face_convert_backward<S><<<grid_for(F, 128), 128, 0, st>>>((const S*)m->positions, m->faces, F, rescale, acc, corner);
+    pdl_launch(face_convert_backward<S>, dim3(grid_for(F, 128)), dim3(128), 0, st, (const S*)m->positions, m->faces, F, rescale, acc, corner);
     GMR_LAUNCHED();
   }
   const uint32_t* vstart = (const uint32_t*)topo;
   const uint32_t* slots = vstart + align_up((V + 1) * 4) / 4;
   if (V) {
-    vertex_gather<S><<<grid_for(V, 256), 256, 0, st>>>(vstart, slots, V, F, corner, (S*)gp, (S*)gcv);
+    pdl_launch(vertex_gather<S>, dim3(grid_for(V, 256)), dim3(256), 0, st, vstart, slots, V, F, corner, (S*)gp, (S*)gcv);
     GMR_LAUNCHED();
   }
   return GMR_OK;
@@ -710,20 +712,20 @@ int reg_terms(const double* pos, const GmrMeshGraph* gr, int64_t V, void* scratc
   double* part_dev = part + nbe + 1;
   double* part_lap = part + 2 * (nbe + 1);
   if (E) {
-    edge_lengths<<<nbe, kTrainThreads, 0, st>>>(pos, gr->edges, E, evec4, part_len);
+    pdl_launch(edge_lengths, dim3(nbe), dim3(kTrainThreads), 0, st, pos, gr->edges, E, evec4, part_len);
     GMR_LAUNCHED();
-    sum_partials<<<1, kTrainThreads, 0, st>>>(part_len, nbe, sums);
+    pdl_launch(sum_partials, dim3(1), dim3(kTrainThreads), 0, st, part_len, nbe, sums);
     GMR_LAUNCHED();
-    edge_terms<<<nbe, kTrainThreads, 0, st>>>(evec4, E, sums, part_dev);
+    pdl_launch(edge_terms, dim3(nbe), dim3(kTrainThreads), 0, st, evec4, E, sums, part_dev);
     GMR_LAUNCHED();
-    sum_partials<<<1, kTrainThreads, 0, st>>>(part_dev, nbe, sums + 1);
+    pdl_launch(sum_partials, dim3(1), dim3(kTrainThreads), 0, st, part_dev, nbe, sums + 1);
     GMR_LAUNCHED();
   } else {
     GMR_CUDA(cudaMemsetAsync(sums, 0, 16, st));
   }
-  laplacian_terms<<<nbv, kTrainThreads, 0, st>>>(pos, gr->adj_ptr, gr->adj, V, lap4, part_lap);
+  pdl_launch(laplacian_terms, dim3(nbv), dim3(kTrainThreads), 0, st, pos, gr->adj_ptr, gr->adj, V, lap4, part_lap);
   GMR_LAUNCHED();
-  sum_partials<<<1, kTrainThreads, 0, st>>>(part_lap, nbv, sums + 2);
+  pdl_launch(sum_partials, dim3(1), dim3(kTrainThreads), 0, st, part_lap, nbv, sums + 2);
   GMR_LAUNCHED();
   *out = RegScratch{evec4, lap4, gpos, gcol, sums};
   return GMR_OK;
@@ -758,11 +760,11 @@ int fit_step_impl(const GmrFitState* s, const GmrMeshGraph* gr, int64_t V, const
   a.render_status = (const DevStatus*)status_src;
   a.reg.ve_ptr = gr->ve_ptr; a.reg.ve_slot = gr->ve_slot; a.reg.adj_ptr = gr->adj_ptr; a.reg.adj = gr->adj;
   a.reg.evec4 = evec4; a.reg.lap4 = lap4; a.reg.V = V; a.reg.w_edge = w_edge; a.reg.w_lap = w_lap;
-  fit_grads<<<nbv, kTrainThreads, 0, st>>>(a, gpos, gcol);
+  pdl_launch(fit_grads, dim3(nbv), dim3(kTrainThreads), 0, st, a, gpos, gcol);
   GMR_LAUNCHED();
-  fit_update<<<nbv, kTrainThreads, 0, st>>>(a, gpos, gcol);
+  pdl_launch(fit_update, dim3(nbv), dim3(kTrainThreads), 0, st, a, gpos, gcol);
   GMR_LAUNCHED();
-  fit_finish<<<1, 32, 0, st>>>(a, img_loss_sums, inv_nc, inv_na, w_color, w_sil, sums + 1, E, sums + 2, history_row,
+  pdl_launch(fit_finish, dim3(1), dim3(32), 0, st, a, img_loss_sums, inv_nc, inv_na, w_color, w_sil, sums + 1, E, sums + 2, history_row,
                                (const uint32_t*)status_src, (uint32_t*)statuses);
   GMR_LAUNCHED();
   return GMR_OK;
@@ -802,13 +804,13 @@ int gmr_mesh_regularizers(const double* positions, const GmrMeshGraph* gr, int64
   cudaStream_t st = (cudaStream_t)stream;
   RegScratch rs;
   if ((rc = reg_terms(positions, gr, V, scratch, st, &rs))) return rc;
-  reg_values<<<1, 1, 0, st>>>(rs.sums, gr->num_edges, V, values);
+  pdl_launch(reg_values, dim3(1), dim3(1), 0, st, rs.sums, gr->num_edges, V, values);
   GMR_LAUNCHED();
   if (grad_edge || grad_laplacian) {
     RegArgs r{};
     r.ve_ptr = gr->ve_ptr; r.ve_slot = gr->ve_slot; r.adj_ptr = gr->adj_ptr; r.adj = gr->adj;
     r.evec4 = rs.evec4; r.lap4 = rs.lap4; r.V = V; r.w_edge = 1.0; r.w_lap = 1.0;
-    reg_grads<<<(unsigned)((V + kTrainThreads - 1) / kTrainThreads), kTrainThreads, 0, st>>>(r, grad_edge,
+    pdl_launch(reg_grads, dim3((unsigned)((V + kTrainThreads - 1) / kTrainThreads)), dim3(kTrainThreads), 0, st, r, grad_edge,
                                                                                           grad_laplacian);
     GMR_LAUNCHED();
   }
@@ -832,11 +834,11 @@ int gmr_image_loss(int32_t kind, const double* x, const double* target, int64_t 
   cudaStream_t st = (cudaStream_t)stream;
   const int nb = (int)((n + kTrainThreads - 1) / kTrainThreads);
   double* part = (double*)scratch;
-  image_loss_terms<<<nb, kTrainThreads, 0, st>>>(kind, x, target, n, grad, part);
+  pdl_launch(image_loss_terms, dim3(nb), dim3(kTrainThreads), 0, st, kind, x, target, n, grad, part);
   GMR_LAUNCHED();
-  sum_partials<<<1, kTrainThreads, 0, st>>>(part, nb, value);
+  pdl_launch(sum_partials, dim3(1), dim3(kTrainThreads), 0, st, part, nb, value);
   GMR_LAUNCHED();
-  scale_value<<<1, 1, 0, st>>>(value, 1.0 / (double)n);
+  pdl_launch(scale_value, dim3(1), dim3(1), 0, st, value, 1.0 / (double)n);
   GMR_LAUNCHED();
   return GMR_OK;
 }
@@ -891,13 +893,13 @@ int gmr_topology_build(const int32_t* faces, int64_t F, int64_t V, void* topo, s
   uint32_t* v[2] = {(uint32_t*)(scratch + 2 * align_up(n * 4)), (uint32_t*)(scratch + 3 * align_up(n * 4))};
   uint32_t* hist = (uint32_t*)(scratch + 4 * align_up(n * 4));
   if (n) {
-    topo_keys<<<grid_for(n, 256), 256, 0, st>>>(faces, F, k[0], v[0]);
+    pdl_launch(topo_keys, dim3(grid_for(n, 256)), dim3(256), 0, st, faces, F, k[0], v[0]);
     GMR_LAUNCHED();
   }
   const int bits = std::max(1, ceil_log2((uint64_t)std::max<int64_t>(V, 1)));
   int cur = radix_sort_pairs<uint32_t>(k, v, nullptr, (uint32_t)n, (uint32_t)n, bits, hist, st);
   GMR_LAUNCHED();
-  tile_ranges<<<grid_for(n / 4 + 1, 256), 256, 0, st>>>(k[cur], nullptr, (uint32_t)n, (uint32_t)V, vstart);
+  pdl_launch(tile_ranges, dim3(grid_for(n / 4 + 1, 256)), dim3(256), 0, st, k[cur], nullptr, (uint32_t)n, (uint32_t)V, vstart);
   GMR_LAUNCHED();
   GMR_CUDA(cudaMemcpyAsync(slots, v[cur], n * 4, cudaMemcpyDeviceToDevice, st));
   return GMR_OK;
@@ -932,11 +934,11 @@ int gmr_project(const void* means, const void* cov3d, int64_t K, const GmrCamera
     return fail(GMR_EINVAL, "null pointer argument");
   cudaStream_t st = (cudaStream_t)stream;
   if (dtype == GMR_F64) {
-    project_gaussians<double><<<grid_for(K, 256), 256, 0, st>>>(
+    pdl_launch(project_gaussians<double>, dim3(grid_for(K, 256)), dim3(256), 0, st, 
         (const double*)means, (const double*)cov3d, K, make_cams<double>(cam, 0, 1).cam[0], W, H, (double*)mean2d,
         (double*)cov2d, (double*)conic, (double*)depth, (double*)radius, (double*)t_cam, kept);
   } else {
-    project_gaussians<float><<<grid_for(K, 256), 256, 0, st>>>(
+    pdl_launch(project_gaussians<float>, dim3(grid_for(K, 256)), dim3(256), 0, st, 
         (const float*)means, (const float*)cov3d, K, make_cams<float>(cam, 0, 1).cam[0], W, H, (float*)mean2d,
         (float*)cov2d, (float*)conic, (float*)depth, (float*)radius, (float*)t_cam, kept);
   }
@@ -952,11 +954,11 @@ int gmr_project_backward(const void* t_cam, const void* cov3d, int64_t K, const 
   if (!t_cam || !cov3d || !g_mean2d || !g_cov2d || !g_mean3d || !g_cov3d) return fail(GMR_EINVAL, "null pointer argument");
   cudaStream_t st = (cudaStream_t)stream;
   if (dtype == GMR_F64) {
-    project_gaussians_backward<double><<<grid_for(K, 256), 256, 0, st>>>(
+    pdl_launch(project_gaussians_backward<double>, dim3(grid_for(K, 256)), dim3(256), 0, st, 
         (const double*)t_cam, (const double*)cov3d, K, make_cams<double>(cam, 0, 1).cam[0], (const double*)g_mean2d,
         (const double*)g_cov2d, (double*)g_mean3d, (double*)g_cov3d);
   } else {
-    project_gaussians_backward<float><<<grid_for(K, 256), 256, 0, st>>>(
+    pdl_launch(project_gaussians_backward<float>, dim3(grid_for(K, 256)), dim3(256), 0, st, 
         (const float*)t_cam, (const float*)cov3d, K, make_cams<float>(cam, 0, 1).cam[0], (const float*)g_mean2d,
         (const float*)g_cov2d, (float*)g_mean3d, (float*)g_cov3d);
   }
@@ -1053,11 +1055,11 @@ int gmr_convert(const GmrMesh* mesh, int32_t rescale, int32_t dtype, void* means
   if (!F) return GMR_OK;
   cudaStream_t st = (cudaStream_t)stream;
   if (dtype == GMR_F64)
-    convert_forward<double><<<grid_for(F, 128), 128, 0, st>>>((const double*)mesh->positions, (const double*)mesh->colors,
+    pdl_launch(convert_forward<double>, dim3(grid_for(F, 128)), dim3(128), 0, st, (const double*)mesh->positions, (const double*)mesh->colors,
                                                               mesh->faces, F, rescale, (double*)means, (double*)cov3d,
                                                               (double*)colors, degenerate);
   else
-    convert_forward<float><<<grid_for(F, 128), 128, 0, st>>>((const float*)mesh->positions, (const float*)mesh->colors,
+    pdl_launch(convert_forward<float>, dim3(grid_for(F, 128)), dim3(128), 0, st, (const float*)mesh->positions, (const float*)mesh->colors,
                                                              mesh->faces, F, rescale, (float*)means, (float*)cov3d,
                                                              (float*)colors, degenerate);
   GMR_LAUNCHED();
@@ -1092,7 +1094,7 @@ int gmr_export_gaussians(const double* means, const double* cov3d, const double*
   if (n < 0) return fail(GMR_EINVAL, "negative count");
   if (n == 0) return GMR_OK;
   if (!means || !cov3d || !colors || !opacities || !records) return fail(GMR_EINVAL, "null pointer argument");
-  export_records<<<grid_for((uint64_t)n, 128), 128, 0, (cudaStream_t)stream>>>(means, cov3d, colors, opacities, n,
+  pdl_launch(export_records, dim3(grid_for((uint64_t)n, 128)), dim3(128), 0, (cudaStream_t)stream, means, cov3d, colors, opacities, n,
                                                                                records);
   GMR_LAUNCHED();
   return GMR_OK;
@@ -1116,9 +1118,9 @@ int nn_run(const double* q, int64_t n, const double* pts, int64_t m, const doubl
   double* bd = (double*)scratch;
   int32_t* bi = (int32_t*)((char*)scratch + align_up((size_t)c * n * 8));
   dim3 grid((unsigned)((n + kNnThreads * kNnQ - 1) / (kNnThreads * kNnQ)), (unsigned)c);
-  nn_partial<<<grid, kNnThreads, 0, st>>>(q, n, pts, m, chunk, bd, bi);
+  pdl_launch(nn_partial, dim3(grid), dim3(kNnThreads), 0, st, q, n, pts, m, chunk, bd, bi);
   GMR_LAUNCHED();
-  nn_merge<<<grid_for((uint64_t)n, 256), 256, 0, st>>>(bd, bi, n, c, qn, pn, d2, cosv, idx);
+  pdl_launch(nn_merge, dim3(grid_for((uint64_t)n, 256)), dim3(256), 0, st, bd, bi, n, c, qn, pn, d2, cosv, idx);
   GMR_LAUNCHED();
   return GMR_OK;
 }
@@ -1172,14 +1174,14 @@ int gmr_chamfer_nc(const double* pts_a, const double* nrm_a, int64_t na, const d
     int rc = nn_run(q, n, p, m, normals ? (dir ? nrm_b : nrm_a) : nullptr, normals ? (dir ? nrm_a : nrm_b) : nullptr,
                     d2, normals ? cs : nullptr, nullptr, scratch, st);
     if (rc) return rc;
-    block_sums<<<kSumBlocks, 256, 0, st>>>(d2, n, part);
+    pdl_launch(block_sums, dim3(kSumBlocks), dim3(256), 0, st, d2, n, part);
     GMR_LAUNCHED();
-    final_sum<<<1, 32, 0, st>>>(part, kSumBlocks, 1.0 / (double)n, out4 + dir);
+    pdl_launch(final_sum, dim3(1), dim3(32), 0, st, part, kSumBlocks, 1.0 / (double)n, out4 + dir);
     GMR_LAUNCHED();
     if (normals) {
-      block_sums<<<kSumBlocks, 256, 0, st>>>(cs, n, part);
+      pdl_launch(block_sums, dim3(kSumBlocks), dim3(256), 0, st, cs, n, part);
       GMR_LAUNCHED();
-      final_sum<<<1, 32, 0, st>>>(part, kSumBlocks, 1.0 / (double)n, out4 + 2 + dir);
+      pdl_launch(final_sum, dim3(1), dim3(32), 0, st, part, kSumBlocks, 1.0 / (double)n, out4 + 2 + dir);
       GMR_LAUNCHED();
     }
   }
@@ -1222,13 +1224,13 @@ int gmr_surface_prepare(const double* positions, const int32_t* faces, int64_t V
   if (prep_bytes < need) return fail(GMR_EWORKSPACE, "prepared buffer too small");
   cudaStream_t st = (cudaStream_t)stream;
   SurfaceLayout L = surface_layout(prep, F);
-  surface_faces<<<grid_for((uint64_t)F, 256), 256, 0, st>>>(positions, faces, F, L.area, L.nrm, L.fsorted);
+  pdl_launch(surface_faces, dim3(grid_for((uint64_t)F, 256)), dim3(256), 0, st, positions, faces, F, L.area, L.nrm, L.fsorted);
   GMR_LAUNCHED();
-  pairwise_total<<<1, kPwThreads, 0, st>>>(L.area, F, L.leaf_off, L.leaf_sum, L.total);
+  pdl_launch(pairwise_total, dim3(1), dim3(kPwThreads), 0, st, L.area, F, L.leaf_off, L.leaf_sum, L.total);
   GMR_LAUNCHED();
-  cumsum_seq<<<1, 32, 0, st>>>(L.area, F, L.cdf);
+  pdl_launch(cumsum_seq, dim3(1), dim3(32), 0, st, L.area, F, L.cdf);
   GMR_LAUNCHED();
-  cdf_divide<<<grid_for((uint64_t)F, 256), 256, 0, st>>>(L.cdf, F, L.total);
+  pdl_launch(cdf_divide, dim3(grid_for((uint64_t)F, 256)), dim3(256), 0, st, L.cdf, F, L.total);
   GMR_LAUNCHED();
   if (total_out) GMR_CUDA(cudaMemcpyAsync(total_out, L.total, 8, cudaMemcpyDeviceToDevice, st));
   return GMR_OK;
@@ -1240,7 +1242,7 @@ int gmr_surface_sample(const double* positions, int64_t F, const void* prep, con
   if (n == 0) return GMR_OK;
   if (!positions || !prep || !uniforms || !points || !normals) return fail(GMR_EINVAL, "null pointer argument");
   SurfaceLayout L = surface_layout((void*)prep, F);
-  surface_points<<<grid_for((uint64_t)n, 256), 256, 0, (cudaStream_t)stream>>>(positions, L.fsorted, L.nrm, L.cdf, F,
+  pdl_launch(surface_points, dim3(grid_for((uint64_t)n, 256)), dim3(256), 0, (cudaStream_t)stream, positions, L.fsorted, L.nrm, L.cdf, F,
                                                                                uniforms, n, points, normals);
   GMR_LAUNCHED();
   return GMR_OK;
@@ -1270,9 +1272,9 @@ int gmr_image_metrics(const double* a, const double* b, int32_t B, int32_t H, in
   double* smap = (double*)(base + align_up(px * C * 8) + align_up(px * 5 * 8));
   double* kern = (double*)(base + align_up(px * C * 8) + align_up(px * 5 * 8) + align_up(px * 8));
   // PSNR: per-image mean squared error (metrics.py:96)
-  sq_diff<<<grid_for(px * C, 256), 256, 0, st>>>(a, b, (int64_t)(px * C), sq);
+  pdl_launch(sq_diff, dim3(grid_for(px * C, 256)), dim3(256), 0, st, a, b, (int64_t)(px * C), sq);
   GMR_LAUNCHED();
-  image_sums<<<B, 256, 0, st>>>(sq, (int64_t)H * W * C, 1.0 / ((double)H * W * C), mse, 0);
+  pdl_launch(image_sums, dim3(B), dim3(256), 0, st, sq, (int64_t)H * W * C, 1.0 / ((double)H * W * C), mse, 0);
   GMR_LAUNCHED();
   if (!ssim) return GMR_OK;
   // Gaussian window (metrics.py:102-106) in float64, k / k.sum() with the
@@ -1293,11 +1295,11 @@ int gmr_image_metrics(const double* a, const double* b, int32_t B, int32_t H, in
   const double c1 = (0.01 * 1.0) * (0.01 * 1.0), c2 = (0.03 * 1.0) * (0.03 * 1.0);
   const double inner = (double)(H - 2 * kSsimHalf) * (double)(W - 2 * kSsimHalf);
   for (int ch = 0; ch < C; ++ch) {
-    ssim_axis0<<<grid_for(px, 256), 256, 0, st>>>(a, b, B, H, W, C, ch, kern, tmp);
+    pdl_launch(ssim_axis0, dim3(grid_for(px, 256)), dim3(256), 0, st, a, b, B, H, W, C, ch, kern, tmp);
     GMR_LAUNCHED();
-    ssim_axis1<<<grid_for(px, 256), 256, 0, st>>>(tmp, B, H, W, kern, c1, c2, smap);
+    pdl_launch(ssim_axis1, dim3(grid_for(px, 256)), dim3(256), 0, st, tmp, B, H, W, kern, c1, c2, smap);
     GMR_LAUNCHED();
-    image_sums<<<B, 256, 0, st>>>(smap, (int64_t)H * W, 1.0 / (inner * C), ssim, ch > 0);
+    pdl_launch(image_sums, dim3(B), dim3(256), 0, st, smap, (int64_t)H * W, 1.0 / (inner * C), ssim, ch > 0);
     GMR_LAUNCHED();
   }
   return GMR_OK;

@@ -10,10 +10,47 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
+
+#include <utility>
 
 #include "../../include/gmr.h"
 
 namespace gmr {
+
+// Programmatic dependent launch (sm_90+): every kernel of the library waits
+// here for its stream predecessor's completion and memory before touching
+// anything, so a launch with the programmatic-serialization attribute can be
+// processed while the predecessor drains (the inter-kernel gap shrinks;
+// nothing runs early).  A no-op for ordinary launches.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// Host side: launch with the attribute (GMR_PDL=0 in the environment turns it
+// off).  A failed launch is kept for the next GMR_LAUNCHED check.
+inline thread_local cudaError_t g_launch_err = cudaSuccess;
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("GMR_PDL");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+template <typename... KArgs, typename... Args>
+inline void pdl_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+  if (e != cudaSuccess && g_launch_err == cudaSuccess) g_launch_err = e;
+}
 
 constexpr int kTile = 16;
 constexpr int kBlendThreads = 256;   // one CTA per 16x16 tile, one pixel per thread

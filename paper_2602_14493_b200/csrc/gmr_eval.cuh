@@ -107,6 +107,7 @@ __global__ void __launch_bounds__(128) export_records(const double* __restrict__
                                                       const double* __restrict__ colors,
                                                       const double* __restrict__ opacities, int64_t n,
                                                       float* __restrict__ rec) {
+  pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double a[3][3], lam[3], v[3][3];
@@ -180,6 +181,7 @@ __global__ void __launch_bounds__(kNnThreads) nn_partial(const double* __restric
                                                          const double* __restrict__ pts, int64_t m,
                                                          int64_t chunk, double* __restrict__ best_d,
                                                          int32_t* __restrict__ best_i) {
+  pdl_wait();
   __shared__ double sx[kNnTile], sy[kNnTile], sz[kNnTile];
   const int64_t q0 = ((int64_t)blockIdx.x * kNnThreads) * kNnQ + threadIdx.x;
   double qx[kNnQ], qy[kNnQ], qz[kNnQ], bd[kNnQ];
@@ -235,6 +237,7 @@ __global__ void __launch_bounds__(256) nn_merge(const double* __restrict__ best_
                                                 const double* __restrict__ qn, const double* __restrict__ pn,
                                                 double* __restrict__ d2_out, double* __restrict__ cos_out,
                                                 int32_t* __restrict__ idx_out) {
+  pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double bd = best_d[i];
@@ -260,6 +263,7 @@ __global__ void __launch_bounds__(256) nn_merge(const double* __restrict__ best_
 // order by one block): out[0] = sum.
 __global__ void __launch_bounds__(256) block_sums(const double* __restrict__ x, int64_t n,
                                                   double* __restrict__ partial) {
+  pdl_wait();
   __shared__ double sh[256];
   double s = 0.0;
   const int64_t per = (int64_t)gridDim.x * blockDim.x;
@@ -274,6 +278,7 @@ __global__ void __launch_bounds__(256) block_sums(const double* __restrict__ x, 
 }
 
 __global__ void final_sum(const double* __restrict__ partial, int nb, double scale, double* __restrict__ out) {
+  pdl_wait();
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     double s = 0.0;
     for (int b = 0; b < nb; ++b) s += partial[b];
@@ -294,6 +299,7 @@ constexpr double kDegenArea = 1e-12;   // mesh.py:15
 __global__ void __launch_bounds__(256) surface_faces(const double* __restrict__ pos, const int32_t* __restrict__ faces,
                                                      int64_t F, double* __restrict__ area, double* __restrict__ nrm,
                                                      int32_t* __restrict__ fsorted) {
+  pdl_wait();
   const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= F) return;
   const int32_t i0 = faces[3 * f], i1 = faces[3 * f + 1], i2 = faces[3 * f + 2];
@@ -351,6 +357,7 @@ constexpr int kPwThreads = 1024;
 __global__ void __launch_bounds__(kPwThreads) pairwise_total(const double* __restrict__ a, int64_t n,
                                                              int64_t* __restrict__ leaf_off,
                                                              double* __restrict__ leaf_sum, double* __restrict__ out) {
+  pdl_wait();
   __shared__ int nleaves;
   if (threadIdx.x == 0) {
     int cnt = 0;
@@ -418,6 +425,7 @@ __global__ void __launch_bounds__(kPwThreads) pairwise_total(const double* __res
 // every prefix depends on the previous one); the division by the total is
 // elementwise and runs in parallel afterwards (cdf_divide)
 __global__ void cumsum_seq(const double* __restrict__ area, int64_t n, double* __restrict__ cdf) {
+  pdl_wait();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   double s = 0.0;
   int64_t i = 0;
@@ -438,6 +446,7 @@ __global__ void cumsum_seq(const double* __restrict__ area, int64_t n, double* _
 
 __global__ void __launch_bounds__(256) cdf_divide(double* __restrict__ cdf, int64_t n,
                                                   const double* __restrict__ total) {
+  pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) cdf[i] = __ddiv_rn(cdf[i], *total);
 }
@@ -447,6 +456,7 @@ __global__ void __launch_bounds__(256) surface_points(const double* __restrict__
                                                       const double* __restrict__ nrm, const double* __restrict__ cdf,
                                                       int64_t F, const double* __restrict__ u, int64_t n,
                                                       double* __restrict__ pts, double* __restrict__ out_n) {
+  pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double u0 = u[3 * i], u1 = u[3 * i + 1], u2 = u[3 * i + 2];
@@ -490,6 +500,7 @@ __device__ __forceinline__ int reflect_idx(int i, int n) {
 __global__ void __launch_bounds__(256) ssim_axis0(const double* __restrict__ a, const double* __restrict__ b,
                                                   int B, int H, int W, int C, int ch,
                                                   const double* __restrict__ kern, double* __restrict__ tmp) {
+  pdl_wait();
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t HW = (int64_t)H * W;
   if (idx >= (int64_t)B * HW) return;
@@ -515,6 +526,7 @@ __global__ void __launch_bounds__(256) ssim_axis0(const double* __restrict__ a, 
 __global__ void __launch_bounds__(256) ssim_axis1(const double* __restrict__ tmp, int B, int H, int W,
                                                   const double* __restrict__ kern, double c1, double c2,
                                                   double* __restrict__ smap) {
+  pdl_wait();
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t HW = (int64_t)H * W;
   if (idx >= (int64_t)B * HW) return;
@@ -542,6 +554,7 @@ __global__ void __launch_bounds__(256) ssim_axis1(const double* __restrict__ tmp
 // per-image sums of `x` over [B][HW] (one block per image, fixed order)
 __global__ void __launch_bounds__(256) image_sums(const double* __restrict__ x, int64_t HW, double scale,
                                                   double* __restrict__ out, int accumulate) {
+  pdl_wait();
   __shared__ double sh[256];
   const double* p = x + (int64_t)blockIdx.x * HW;
   double s = 0.0;
@@ -558,6 +571,7 @@ __global__ void __launch_bounds__(256) image_sums(const double* __restrict__ x, 
 // squared differences (for PSNR's MSE) into sq [B][H*W*C]
 __global__ void __launch_bounds__(256) sq_diff(const double* __restrict__ a, const double* __restrict__ b,
                                                int64_t n, double* __restrict__ sq) {
+  pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) {
     const double d = a[i] - b[i];

@@ -23,6 +23,7 @@ namespace gmr {
 // ---------------------------------------------------------------------------
 
 __global__ void reset_status(DevStatus* st) {
+  pdl_wait();
   st->entries = 0;
   st->kept = 0;
   for (int i = 0; i < 6; ++i) st->bad_item[i] = 0xffffffffu;
@@ -279,6 +280,7 @@ template <typename S> struct MeshFwdArgs {
 
 template <typename S>
 __global__ void __launch_bounds__(256) mesh_to_splats(MeshFwdArgs<S> p, const __grid_constant__ CamBatch<S> cams) {
+  pdl_wait();
   const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool live = f < p.F;
   uint32_t kept = 0;
@@ -393,6 +395,7 @@ template <typename S> struct PackArgs {
 
 template <typename S>
 __global__ void __launch_bounds__(256) pack_splats(PackArgs<S> p) {
+  pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= p.K) return;
   const S mx = p.mean2d[2 * i], my = p.mean2d[2 * i + 1];
@@ -439,6 +442,7 @@ __global__ void __launch_bounds__(256) scan_reduce(const uint32_t* order, const 
                                                   const uint32_t* krange, int key_bits,
                                                   const uint32_t* __restrict__ count, uint32_t n,
                                                   uint32_t* __restrict__ bsum) {
+  pdl_wait();
   __shared__ uint32_t sw[8];
   if (krange) order = result_buffer(order, order_alt, krange, key_bits);
   const uint32_t i = blockIdx.x * (uint32_t)kScanTile + threadIdx.x;
@@ -501,6 +505,7 @@ __device__ __forceinline__ unsigned long long scan_runs_inplace(uint32_t* __rest
 
 __global__ void __launch_bounds__(kTopThreads) scan_top(uint32_t* __restrict__ bsum, int nb, DevStatus* st,
                                                        unsigned long long capacity, uint32_t* n_entries) {
+  pdl_wait();
   const unsigned long long carry = scan_runs_inplace(bsum, nb);
   if (threadIdx.x == 0) {
     st->entries = carry;
@@ -522,6 +527,7 @@ __global__ void __launch_bounds__(256) scan_emit(const uint32_t* order, const ui
                                                 uint32_t tiles_per_view,
                                                 const uint32_t* __restrict__ n_entries,
                                                 uint32_t* __restrict__ key, uint32_t* __restrict__ val) {
+  pdl_wait();
   __shared__ uint32_t sw[8];
   if (krange) order = result_buffer(order, order_alt, krange, key_bits);
   const uint32_t i = blockIdx.x * (uint32_t)kScanTile + threadIdx.x;
@@ -560,6 +566,7 @@ __global__ void __launch_bounds__(256) scan_emit(const uint32_t* order, const ui
 __global__ void __launch_bounds__(256) face_counts(const uint32_t* __restrict__ count, uint32_t F, int B,
                                                   uint32_t* __restrict__ face_local,
                                                   uint32_t* __restrict__ bsum) {
+  pdl_wait();
   __shared__ uint32_t sw[8];
   const uint32_t f = blockIdx.x * 256u + threadIdx.x;
   uint32_t s = 0;
@@ -573,6 +580,7 @@ __global__ void __launch_bounds__(256) face_counts(const uint32_t* __restrict__ 
 
 // single-block exclusive scan in place
 __global__ void __launch_bounds__(kTopThreads) scan_inplace(uint32_t* __restrict__ a, int n) {
+  pdl_wait();
   scan_runs_inplace(a, n);
 }
 
@@ -580,6 +588,7 @@ __global__ void __launch_bounds__(256) item_offsets(const uint32_t* __restrict__
                                                    const uint32_t* __restrict__ face_local,
                                                    const uint32_t* __restrict__ bsum,
                                                    uint32_t* __restrict__ entry_off) {
+  pdl_wait();
   const uint32_t f = blockIdx.x * 256u + threadIdx.x;
   if (f >= F) return;
   uint32_t run = bsum[blockIdx.x] + face_local[f];
@@ -594,6 +603,7 @@ __global__ void __launch_bounds__(256) item_offsets(const uint32_t* __restrict__
 __global__ void __launch_bounds__(256) tile_ranges(const uint32_t* __restrict__ key,
                                                   const uint32_t* n_dev, uint32_t n_host,
                                                   uint32_t num_bins, uint32_t* __restrict__ bounds) {
+  pdl_wait();
   // four positions per thread (one 16-byte load; key buffers are 256-B aligned)
   const uint32_t n = n_dev ? *n_dev : n_host;
   const uint32_t s0 = 4u * (blockIdx.x * blockDim.x + threadIdx.x);
@@ -628,6 +638,7 @@ __device__ __forceinline__ uint32_t sched_bucket(uint32_t cnt) { return 255u - m
 
 __global__ void __launch_bounds__(kSchedThreads) tile_schedule(const uint32_t* __restrict__ bounds, uint32_t bins,
                                                                uint32_t* __restrict__ order, DevStatus* st) {
+  pdl_wait();
   __shared__ uint32_t hist[256];
   __shared__ uint32_t longest;
   for (int i = threadIdx.x; i < 256; i += kSchedThreads) hist[i] = 0;
@@ -767,6 +778,7 @@ __global__ void __launch_bounds__(kBinSortThreads, 4) bin_depth_sort(const uint3
                                                                   uint32_t* __restrict__ entry_item,
                                                                   K* __restrict__ gk0, K* __restrict__ gk1,
                                                                   uint32_t* __restrict__ gv1) {
+  pdl_wait();
   __shared__ BinSortSmem<K> sm;
   const uint32_t g = sched ? sched[blockIdx.x] : blockIdx.x;
   const uint32_t s = bounds[g], n = bounds[g + 1] - s;
@@ -925,6 +937,7 @@ __device__ __forceinline__ void block_sum2(double a, double b, double* out2) {
 // Sum the per-tile loss partials in tile order (single block, fixed tree).
 __global__ void __launch_bounds__(256) loss_reduce(const double* __restrict__ tile, uint32_t bins,
                                                   double* __restrict__ out2) {
+  pdl_wait();
   double a = 0.0, b = 0.0;
   for (uint32_t i = threadIdx.x; i < bins; i += 256) {
     a += tile[2 * i];
@@ -1211,6 +1224,7 @@ struct BitWalk {
 #endif
 template <typename S, bool kOp>
 __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 4 : GMR_FWD_MINB) blend_forward(BlendArgs<S> p) {
+  pdl_wait();
   __shared__ StageSmem<S, kFwdBatch, kOp> sm;
   const uint32_t g = p.sched ? p.sched[blockIdx.x] : blockIdx.x;
   const uint32_t view = g / p.tiles_per_view, t = g % p.tiles_per_view;
@@ -1378,6 +1392,7 @@ template <typename S, bool kOpacity> struct BwdSmem {
 //  No atomics, fixed orders: the result is deterministic.
 template <typename S, bool kOpacity>
 __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : GMR_BWD_MINB) blend_backward(BlendArgs<S> p) {
+  pdl_wait();
   extern __shared__ __align__(32) unsigned char dyn[];
   typedef BwdSmem<S, kOpacity> Sm;
   typedef typename Sm::Rec Rec;
@@ -1711,6 +1726,7 @@ template <typename S>
 #define GMR_K5_MINB 4   // 128 registers: four partial runs in flight per face (latency-bound gathers)
 #endif
 __global__ void __launch_bounds__(128, GMR_K5_MINB) face_views_backward(FaceBwdArgs<S> p, const __grid_constant__ CamBatch<S> cams) {
+  pdl_wait();
   const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= p.F) return;
   FaceGeo g;
@@ -1889,6 +1905,7 @@ __global__ void __launch_bounds__(128) face_convert_backward(const S* __restrict
                                                              int64_t F, int rescale,
                                                              const double* __restrict__ face_acc,
                                                              S* __restrict__ corner) {
+  pdl_wait();
   const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= F) return;
   FaceGeo g;
@@ -1907,6 +1924,7 @@ __global__ void __launch_bounds__(256) vertex_gather(const uint32_t* __restrict_
                                                     const uint32_t* __restrict__ slots, int64_t V,
                                                     int64_t F, const S* __restrict__ corner,
                                                     S* __restrict__ g_pos, S* __restrict__ g_col) {
+  pdl_wait();
   const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= V) return;
   S gp[3] = {0, 0, 0}, gc[3] = {0, 0, 0};
@@ -1952,6 +1970,7 @@ __global__ void __launch_bounds__(256) splat_grads(const uint32_t* __restrict__ 
                                                   const S* __restrict__ partial_op, int64_t K,
                                                   const DevStatus* __restrict__ st,
                                                   S* g_mean2d, S* g_cov2d, S* g_color, S* g_opacity) {
+  pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= K) return;
   // after an entry overflow no partial exists (see face_views_backward)
@@ -1984,6 +2003,7 @@ __global__ void __launch_bounds__(256) splat_grads(const uint32_t* __restrict__ 
 
 // topology: slot s = c * F + f -> key faces[3f + c]
 __global__ void topo_keys(const int32_t* __restrict__ faces, int64_t F, uint32_t* key, uint32_t* val) {
+  pdl_wait();
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= 3 * F) return;
   const int64_t c = s / F, f = s - c * F;
@@ -2000,6 +2020,7 @@ __global__ void __launch_bounds__(128) convert_forward(const S* __restrict__ pos
                                                        const int32_t* __restrict__ faces, int64_t F,
                                                        int rescale, S* means, S* cov3d, S* colors,
                                                        uint8_t* degenerate) {
+  pdl_wait();
   const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= F) return;
   FaceGeo g;
@@ -2022,6 +2043,7 @@ template <typename S>
 __global__ void __launch_bounds__(256) pack_face_grads(const S* __restrict__ gm, const S* __restrict__ gcov,
                                                       const S* __restrict__ gcol, int64_t F,
                                                       double* __restrict__ face_acc) {
+  pdl_wait();
   const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= F) return;
   const S* G = gcov + f * 9;

@@ -20,6 +20,7 @@ __global__ void __launch_bounds__(256) project_gaussians(const S* __restrict__ m
                                                          S* __restrict__ conic, S* __restrict__ depth,
                                                          S* __restrict__ radius, S* __restrict__ t_cam,
                                                          uint8_t* __restrict__ kept) {
+  pdl_wait();
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= K) return;
   S m[3], t[3];
@@ -81,6 +82,7 @@ __global__ void __launch_bounds__(256) project_gaussians_backward(const S* __res
                                                                   const S* __restrict__ g_mean2d,
                                                                   const S* __restrict__ g_cov2d,
                                                                   S* __restrict__ g_mean3d, S* __restrict__ g_cov3d) {
+  pdl_wait();
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= K) return;
   S t[3];

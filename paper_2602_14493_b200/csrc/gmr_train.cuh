@@ -34,6 +34,7 @@ __device__ __forceinline__ void block_sum1(double a, double* out) {
 // single block: out[0] = sum of part[0..n) in a fixed order
 __global__ void __launch_bounds__(kTrainThreads) sum_partials(const double* __restrict__ part, int n,
                                                              double* __restrict__ out) {
+  pdl_wait();
   double a = 0.0;
   for (int i = threadIdx.x; i < n; i += kTrainThreads) a += part[i];
   block_sum1(a, out);
@@ -43,6 +44,7 @@ __global__ void __launch_bounds__(kTrainThreads) sum_partials(const double* __re
 __global__ void __launch_bounds__(kTrainThreads) edge_lengths(const double* __restrict__ pos,
                                                              const int32_t* __restrict__ edges, int64_t E,
                                                              double* __restrict__ vec4, double* __restrict__ part) {
+  pdl_wait();
   const int64_t e = (int64_t)blockIdx.x * kTrainThreads + threadIdx.x;
   double len = 0.0;
   if (e < E) {
@@ -59,6 +61,7 @@ __global__ void __launch_bounds__(kTrainThreads) edge_lengths(const double* __re
 __global__ void __launch_bounds__(kTrainThreads) edge_terms(double* __restrict__ vec4, int64_t E,
                                                            const double* __restrict__ len_sum,
                                                            double* __restrict__ part) {
+  pdl_wait();
   const int64_t e = (int64_t)blockIdx.x * kTrainThreads + threadIdx.x;
   double d2 = 0.0;
   if (e < E) {
@@ -78,6 +81,7 @@ __global__ void __launch_bounds__(kTrainThreads) laplacian_terms(const double* _
                                                                 const int32_t* __restrict__ adj_ptr,
                                                                 const int32_t* __restrict__ adj, int64_t V,
                                                                 double* __restrict__ lap4, double* __restrict__ part) {
+  pdl_wait();
   const int64_t v = (int64_t)blockIdx.x * kTrainThreads + threadIdx.x;
   double l2 = 0.0;
   if (v < V) {
@@ -150,6 +154,7 @@ __device__ __forceinline__ void reg_grad(const RegArgs& r, int64_t v, double g[3
 // the two regulariser gradients as separate [V,3] arrays (either may be null)
 __global__ void __launch_bounds__(kTrainThreads) reg_grads(RegArgs r, double* __restrict__ g_edge,
                                                           double* __restrict__ g_lap) {
+  pdl_wait();
   const int64_t v = (int64_t)blockIdx.x * kTrainThreads + threadIdx.x;
   if (v >= r.V) return;
   double g[3];
@@ -165,6 +170,7 @@ __global__ void __launch_bounds__(kTrainThreads) reg_grads(RegArgs r, double* __
 
 // values (edge, laplacian) = (sum dev^2 / E, sum |lap|^2 / V)
 __global__ void reg_values(const double* __restrict__ sums, int64_t E, int64_t V, double* __restrict__ out) {
+  pdl_wait();
   out[0] = E ? sums[1] / (double)E : 0.0;
   out[1] = sums[2] / (double)V;
 }
@@ -178,6 +184,7 @@ __global__ void __launch_bounds__(kTrainThreads) image_loss_terms(int kind, cons
                                                                  const double* __restrict__ t, int64_t n,
                                                                  double* __restrict__ grad,
                                                                  double* __restrict__ part) {
+  pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * kTrainThreads + threadIdx.x;
   double term = 0.0;
   if (i < n) {
@@ -197,7 +204,8 @@ __global__ void __launch_bounds__(kTrainThreads) image_loss_terms(int kind, cons
   block_sum1(term, part + blockIdx.x);
 }
 
-__global__ void scale_value(double* __restrict__ v, double s) { v[0] *= s; }
+__global__ void scale_value(double* __restrict__ v, double s) {
+  pdl_wait(); v[0] *= s; }
 
 struct AdamArgs {
   double* pos;        // [V,3] float64 parameters (updated)
@@ -239,6 +247,7 @@ __device__ __forceinline__ double sched_lr_col(const AdamArgs& a) { return a.lr_
 // pass 1: total gradients (image + regularisers) -> stash, non-finite flags
 __global__ void __launch_bounds__(kTrainThreads) fit_grads(AdamArgs a, double* __restrict__ gpos,
                                                           double* __restrict__ gcol) {
+  pdl_wait();
   const int64_t v = (int64_t)blockIdx.x * kTrainThreads + threadIdx.x;
   bool bp = false, bc = false;
   if (v < a.reg.V) {
@@ -263,6 +272,7 @@ __global__ void __launch_bounds__(kTrainThreads) fit_grads(AdamArgs a, double* _
 // with any non-finite gradient is rejected whole (optim.py:55-60, :103-106)
 __global__ void __launch_bounds__(kTrainThreads) fit_update(AdamArgs a, const double* __restrict__ gpos,
                                                            const double* __restrict__ gcol) {
+  pdl_wait();
   const int64_t v = (int64_t)blockIdx.x * kTrainThreads + threadIdx.x;
   if (v >= a.reg.V) return;
   const double lr_pos = sched_lr_pos(a), lr_col = sched_lr_col(a);
@@ -309,6 +319,7 @@ __global__ void fit_finish(AdamArgs a, const double* __restrict__ img_sums, doub
                            double w_color, double w_sil, const double* __restrict__ edge_sum, int64_t E,
                            const double* __restrict__ lap_sum, double* __restrict__ history,
                            const uint32_t* __restrict__ status_src, uint32_t* __restrict__ statuses) {
+  pdl_wait();
   const int64_t it = a.iter ? *a.iter : 0;
   if (status_src && statuses && threadIdx.x < 16) statuses[16 * it + threadIdx.x] = status_src[threadIdx.x];
   __syncthreads();

@@ -79,6 +79,7 @@ __global__ void __launch_bounds__(kSortThreads) radix_upsweep(const K* __restric
                                                               uint32_t n_host, int shift,
                                                               uint32_t* __restrict__ hist,
                                                               int nblocks, const uint32_t* krange, int bits) {
+  pdl_wait();
   const KeyRange kr = key_range(krange, bits);
   if (shift >= 8 * kr.passes) return;
   __shared__ uint32_t h[kSortWarps][256];
@@ -135,6 +136,7 @@ __global__ void __launch_bounds__(kSortThreads) radix_scan(uint32_t* __restrict_
                                                            uint32_t* __restrict__ totals,
                                                            int nblocks, const uint32_t* krange, int bits,
                                                            int shift) {
+  pdl_wait();
   if (shift >= 8 * key_range(krange, bits).passes) return;
   __shared__ uint32_t sw[kSortWarps];
   uint32_t* row = hist + (size_t)blockIdx.x * nblocks;
@@ -180,6 +182,7 @@ __global__ void __launch_bounds__(kSortThreads, 3) radix_downsweep(
     uint32_t* __restrict__ vout, const uint32_t* n_dev, uint32_t n_host, int shift,
     const uint32_t* __restrict__ hist, const uint32_t* __restrict__ totals, int nblocks,
     const uint32_t* krange, int bits) {
+  pdl_wait();
   const KeyRange kr = key_range(krange, bits);
   if (shift >= 8 * kr.passes) return;
   extern __shared__ __align__(16) unsigned char dsm_raw[];
@@ -289,6 +292,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_radix_sort(K* __restri
                                                                      K* __restrict__ k1, uint32_t* __restrict__ v1,
                                                                      const uint32_t* n_dev, uint32_t n_host,
                                                                      int bits, uint32_t n_max) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char ss_raw[];
   K* skeys = reinterpret_cast<K*>(ss_raw);
   uint32_t* svals = reinterpret_cast<uint32_t*>(ss_raw + (size_t)n_max * sizeof(K));
@@ -396,7 +400,7 @@ inline void launch_small_sort(K* keys[2], uint32_t* vals[2], const uint32_t* n_d
       small_radix_sort<K, PER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
       (int)small_sort_smem<K>(SmallSortLimit<K>::value));
   (void)attr_rc;
-  small_radix_sort<K, PER><<<1, kSmallThreads, small_sort_smem<K>(n_max), stream>>>(
+  pdl_launch(small_radix_sort<K, PER>, dim3(1), dim3(kSmallThreads), small_sort_smem<K>(n_max), stream, 
       keys[0], vals[0], keys[1], vals[1], n_dev, n_host, bits, n_max);
 }
 
@@ -436,11 +440,11 @@ inline int radix_sort_pairs(K* keys[2], uint32_t* vals[2], const uint32_t* n_dev
   if (reduced) *reduced = krange != nullptr;
   int cur = 0;
   for (int shift = 0; shift < bits; shift += 8) {
-    radix_upsweep<K><<<nblocks, kSortThreads, 0, stream>>>(keys[cur], n_dev, n_host, shift, hist,
+    pdl_launch(radix_upsweep<K>, dim3(nblocks), dim3(kSortThreads), 0, stream, keys[cur], n_dev, n_host, shift, hist,
                                                            nblocks, krange, bits);
-    radix_scan<<<256, kSortThreads, 0, stream>>>(hist, totals, nblocks, krange, bits, shift);
+    pdl_launch(radix_scan, dim3(256), dim3(kSortThreads), 0, stream, hist, totals, nblocks, krange, bits, shift);
     auto down = random_digits ? radix_downsweep<K, true> : radix_downsweep<K, false>;
-    down<<<nblocks, kSortThreads, sizeof(DownSmem<K>), stream>>>(
+    pdl_launch(down, dim3(nblocks), dim3(kSortThreads), sizeof(DownSmem<K>), stream, 
         keys[cur], vals[cur], keys[cur ^ 1], vals[cur ^ 1], n_dev, n_host, shift, hist, totals, nblocks,
         krange, bits);
     cur ^= 1;
