@@ -209,3 +209,48 @@ def test_large_bins_depth_order(gmr, k):
             ok = (dd[1:] > dd[:-1]) | ((dd[1:] == dd[:-1]) & (ii[1:] > ii[:-1]))
             assert ok.all(), (dtype, g)
     _check_splats(gmr, case, W, H)
+
+
+_PDL_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_2602_14493_b200 as gmr
+from paper_2602_14493_b200 import engine
+m = gmr.make_geodesic_sphere(20, seed=0)
+cams = gmr.hemisphere_cameras(3, 3.0, (96, 80))
+dev = torch.device("cuda", 0)
+pos = torch.tensor(np.asarray(m.vertices), dtype=torch.float32, device=dev)
+col = torch.tensor(np.asarray(m.colors), dtype=torch.float32, device=dev)
+faces = torch.tensor(np.asarray(m.facets), dtype=torch.int32, device=dev)
+g = torch.randn((3, 80, 96, 3), generator=torch.Generator(device=dev).manual_seed(0), device=dev)
+ga = torch.randn((3, 80, 96), generator=torch.Generator(device=dev).manual_seed(1), device=dev)
+outs = []
+for _ in range(3):   # global depth order first, then per-tile lists
+    rgb, alpha, st = engine.render_forward(pos, col, faces, cams, 96, 80, (0.1, 0.2, 0.3))
+    gp, gc = engine.render_backward(st, pos, col, faces, rgb, g, ga)
+    torch.cuda.synchronize()
+    outs += [rgb.cpu().numpy(), alpha.cpu().numpy(), gp.cpu().numpy(), gc.cpu().numpy()]
+np.savez(sys.argv[2], *outs)
+"""
+
+
+def test_programmatic_launch_is_bit_identical(gmr, tmp_path):
+    """Every kernel waits for its predecessor (griddepcontrol.wait) before
+    touching memory, so launching with programmatic stream serialization
+    (default) and without it (GMR_PDL=0) gives the same bits."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "pdl.py"
+    script.write_text(_PDL_SCRIPT)
+    res = {}
+    for flag in ("1", "0"):
+        out = tmp_path / f"out{flag}.npz"
+        env = dict(os.environ, GMR_PDL=flag)
+        r = subprocess.run([sys.executable, str(script), root, str(out)], env=env, capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res[flag] = np.load(out)
+    for k in res["1"].files:
+        assert np.array_equal(res["1"][k], res["0"][k]), k
