@@ -40,11 +40,13 @@ CONFIGS = {
                desc="config3: geodesic displaced sphere n=158 (499,280 faces, 249,642 vertices), 800x800"),
     "c3b1": dict(mesh=("geodesic", 158), res=800, views=1,
                  desc="config3 batch 1: geodesic displaced sphere n=158 (499,280 faces), 800x800"),
-    "c4": dict(mesh=("geodesic", 316), res=1024, views=8,
-               desc="config4: geodesic displaced sphere n=316 (1,997,120 faces), 1024x1024"),
+    "c4": dict(mesh=("geodesic", 316), res=1024, views=8, cams="sphere",
+               desc="config4: geodesic displaced sphere n=316 (1,997,120 faces), 1024x1024, full-sphere Fibonacci "
+                    "cameras (SURVEY 8d)"),
     # BASELINE configs[3] as stated: 64 views in total, sharded over the ranks
-    "c4s": dict(mesh=("geodesic", 316), res=1024, views=64, total_views=True, chunk=16,
-                desc="config4: geodesic displaced sphere n=316 (1,997,120 faces), 1024x1024, 64 views in total"),
+    "c4s": dict(mesh=("geodesic", 316), res=1024, views=64, total_views=True, chunk=16, cams="sphere",
+                desc="config4: geodesic displaced sphere n=316 (1,997,120 faces), 1024x1024, full-sphere Fibonacci "
+                     "cameras (SURVEY 8d), 64 views in total"),
     "views": dict(mesh=("geodesic", 158), res=256, views=253,
                   desc="SURVEY 8f row 3: make_views of the config-3 mesh (499,280 faces), 253 hemisphere views "
                        "256x256, float64 like the reference, 8-bit images to host"),
@@ -69,6 +71,9 @@ def build_mesh(cfg):
 
 def all_cams(cfg, total):
     import paper_2602_14493_b200 as gmr
+    if cfg.get("cams") == "sphere":   # C4: full-sphere Fibonacci lattice (reference test_acceptance.py:61-67)
+        from paper_2602_14493_b200.camera import sphere_views
+        return sphere_views(total, 3.0, cfg["res"])
     return gmr.hemisphere_cameras(total, 3.0, (cfg["res"], cfg["res"]))
 
 

@@ -53,9 +53,9 @@ def _worker(rank, world, port, ncams, q, reproducible=False):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         case = gc.loss_case()
-        cams = (case["cameras"] * 2)[:ncams]
-        rgbs = (case["target_rgb"] * 2)[:ncams]
-        masks = (case["target_mask"] * 2)[:ncams]
+        cams = (case["cameras"] * 3)[:ncams]
+        rgbs = (case["target_rgb"] * 3)[:ncams]
+        masks = (case["target_mask"] * 3)[:ncams]
         c, s, gp, gcol = gdist.sharded_image_loss(oracle_local_fn(case), cams, rgbs, masks,
                                                   len(case["vertices"]), reproducible=reproducible)
         q.put((rank, c, s, gp.numpy(), gcol.numpy()))
@@ -123,6 +123,35 @@ def test_four_rank_reproducible_sum_in_rank_order():
         np.testing.assert_array_equal(gcc, exp_c)
         np.testing.assert_allclose(gp, gv, rtol=0, atol=1e-12)
         assert c == pytest.approx(cv, rel=1e-12) and s == pytest.approx(sv, rel=1e-12)
+
+
+def test_eight_rank_sharding_matches_single_process():
+    """World size 8 (R in {1, 2, 4, 8}) over 9 views: shards of
+    one or two views, gradients and losses equal to the single-process
+    reference semantics on every rank."""
+    ncams, world = 9, 8
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, ncams, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in procs], key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    case = gc.loss_case()
+    cams = (case["cameras"] * 3)[:ncams]
+    rgbs = (case["target_rgb"] * 3)[:ncams]
+    masks = (case["target_mask"] * 3)[:ncams]
+    cv, sv, gv, gcol = orc.views_image_grad(case["vertices"], case["facets"], case["colors"], cams, rgbs,
+                                            masks, background=case["background"])
+    for _, c, s, gp, gcc in res:
+        assert c == pytest.approx(cv, rel=1e-12) and s == pytest.approx(sv, rel=1e-12)
+        np.testing.assert_allclose(gp, gv, rtol=0, atol=1e-12)
+        np.testing.assert_allclose(gcc, gcol, rtol=0, atol=1e-12)
+    for r in res[1:]:
+        np.testing.assert_array_equal(res[0][3], r[3])
 
 
 def test_shard_ranges_cover_views_once():
