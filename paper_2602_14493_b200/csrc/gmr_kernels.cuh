@@ -1099,6 +1099,9 @@ __device__ __forceinline__ void prefetch_records(const BlendArgs<S>& p, uint32_t
 #ifndef GMR_BWD_BATCH
 #define GMR_BWD_BATCH 128
 #endif
+#ifndef GMR_RQ_WORDS
+#define GMR_RQ_WORDS 1
+#endif
 #ifndef GMR_BWD_TMA
 // 1: the coverage rows of the next batch arrive by a 1-D bulk copy (TMA
 // engine, UBLKCP + mbarrier) issued one batch ahead.  Measured slower
@@ -1370,7 +1373,7 @@ template <typename S, bool kOpacity> struct BwdSmem {
 #endif
   V4<S> pix[kBlendThreads];         // per tile pixel (col + 16 row): g_r, g_g, g_b
   Rec rec[kCap];                    // per (entry, covered pixel): (dp, w[, dL/dalpha * ep])
-  uint8_t rq[kCap];                 // tile pixel (col + 16 row) of each record
+  uint8_t rq[(kCap + 3) & ~3];       // tile pixel (col + 16 row) of each record (whole words: read 4 at a time)
 };
 
 // Backward (render.py:294-361).  Per batch of staged entries:
@@ -1612,12 +1615,25 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : GMR_BWD_MI
       };
       // not unrolled: measured 1.188 -> 1.171 ms at config 3 (the 4x unrolled
       // loop serialised its loads under the 48-register cap anyway)
+#if GMR_RQ_WORDS
+      // pixel ids four at a time (one 32-bit shared load per 4 records)
+      const uint32_t* rq4 = reinterpret_cast<const uint32_t*>(sm.rq);
+      uint32_t qw = lo < hi ? rq4[lo >> 2] : 0u;
+#pragma unroll 1
+      for (uint32_t r = lo; r < hi; ++r) {
+        if ((r & 3u) == 0u) qw = rq4[r >> 2];
+        const Rec s = sm.rec[r];
+        const int q = (int)((qw >> ((r & 3u) << 3)) & 255u);
+        add(s, q, sm.pix[q]);
+      }
+#else
 #pragma unroll 1
       for (uint32_t r = lo; r < hi; ++r) {
         const Rec s = sm.rec[r];
         const int q = sm.rq[r];
         add(s, q, sm.pix[q]);
       }
+#endif
     }
     // combine the two halves (fixed order) and store at the pre-sort slot
     if constexpr (kSplit == 2) {
