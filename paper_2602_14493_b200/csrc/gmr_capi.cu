@@ -427,6 +427,8 @@ int blend_backward_launch(const Layout& L, void* ws, const GmrRaster* r, const v
   // 128-byte units plus 1 KB reserved
   static_assert(((sizeof(BwdSmem<float, false>) + 127) / 128 * 128 + 1024) * GMR_BWD_MINB <= 228 * 1024,
                 "blend_backward shared memory no longer fits GMR_BWD_MINB CTAs per SM");
+  static_assert(((sizeof(BwdSmem<double, true>) + 127) / 128 * 128 + 1024) * 3 <= 228 * 1024,
+                "float64 blend_backward shared memory no longer fits 3 CTAs per SM");
   // once per instantiation (thread-safe static init; also keeps it out of graph captures)
   static const cudaError_t attr_rc = [dyn] {
     const cudaError_t e = cudaFuncSetAttribute(blend_backward<S, kOpacity>,

@@ -1358,11 +1358,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 template <typename S, bool kOpacity> struct RecOf { typedef V2<S> type; };
 template <typename S> struct RecOf<S, true> { typedef V4<S> type; };
 
-constexpr int kBwdPairBytes = GMR_BWD_PAIR_BYTES;
+#ifndef GMR_BWD_PAIR_BYTES_F64
+// float64 runs 3 CTAs/SM (register-bound): its 16-byte records get a buffer
+// of the same record count as float's instead of half of it
+#define GMR_BWD_PAIR_BYTES_F64 46080
+#endif
+template <typename S> struct BwdPairBytes { static constexpr int value = sizeof(S) == 8 ? GMR_BWD_PAIR_BYTES_F64 : GMR_BWD_PAIR_BYTES; };
 
 template <typename S, bool kOpacity> struct BwdSmem {
   typedef typename RecOf<S, kOpacity>::type Rec;
-  static constexpr int kCap = kBwdPairBytes / (int)(sizeof(Rec) + 1);
+  static constexpr int kCap = BwdPairBytes<S>::value / (int)(sizeof(Rec) + 1);
   StageSmem<S, kBwdBatch, kOpacity, false> st;
   uint2 cw[8][kBwdBatch];           // per warp block and entry: (coverage word, first record of its pixels)
   uint32_t rend[kBwdBatch];         // per entry: end of its records (they start at cw[0][j].y)
