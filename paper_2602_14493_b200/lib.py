@@ -11,6 +11,8 @@ from __future__ import annotations
 import ctypes
 import os
 
+import numpy as np
+
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("GMR_LIB_PATH") or os.path.join(_HERE, "libgmr.so")
 
@@ -166,10 +168,12 @@ def check(code: int):
 
 
 def camera_struct(cams) -> ctypes.Array:
-    arr = (GmrCamera * len(cams))()
+    """GmrCamera[n] (18 float64 each: R row-major, t, fx, fy, cx, cy, near,
+    far) filled from one packed array."""
+    n = len(cams)
+    vals = np.empty((n, 18), np.float64)
     for i, c in enumerate(cams):
-        arr[i].R[:] = [float(x) for x in c.rotation.reshape(-1)]
-        arr[i].t[:] = [float(x) for x in c.translation.reshape(-1)]
-        arr[i].fx, arr[i].fy, arr[i].cx, arr[i].cy = float(c.fx), float(c.fy), float(c.cx), float(c.cy)
-        arr[i].near_plane, arr[i].far_plane = float(c.near), float(c.far)
-    return arr
+        vals[i, 0:9] = np.asarray(c.rotation, np.float64).reshape(-1)
+        vals[i, 9:12] = np.asarray(c.translation, np.float64).reshape(-1)
+        vals[i, 12:] = (c.fx, c.fy, c.cx, c.cy, c.near, c.far)
+    return (GmrCamera * n).from_buffer_copy(vals.tobytes())
