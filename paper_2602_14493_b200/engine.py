@@ -109,7 +109,10 @@ class _TileOrder:
         self._shapes = {}
 
     def flags(self, key, dtype):
-        if not AUTO_TILE_ORDER or key[0] * key[1] >= self.GLOBAL_ITEMS:
+        if not AUTO_TILE_ORDER:
+            return 0
+        items = key[0] * key[1] if isinstance(key[0], int) else key[1]   # (F, B, ...) or ('splats', K, ...)
+        if items >= self.GLOBAL_ITEMS:
             return 0
         sh = self._shapes.get(key)
         if sh is None:
