@@ -94,7 +94,7 @@ inline unsigned grid_for(uint64_t n, unsigned block) { return (unsigned)std::max
 // Workspace layout (byte offsets).
 struct Layout {
   size_t status, splat, col4, bin, count, dkey[2], ditem[2], offs, entry_off, bsum, nent;
-  size_t ekey[2], eval[2], bounds, sched, covbuf, t_final, hist, partial, partial_op, face_acc, corner, aux, loss_tile;
+  size_t ekey[2], eval[2], bounds, sched, schedcnt, covbuf, t_final, hist, partial, partial_op, face_acc, corner, aux, loss_tile;
   size_t total;
   uint64_t items, faces, bins, pixels, ecap;
   int views, tiles_x, tiles_y, tiles;
@@ -137,6 +137,7 @@ Layout plan(uint64_t faces, int views, int W, int H, uint64_t ecap, int dtype, b
   L.eval[1] = take(ecap * 4);
   L.bounds = take((L.bins + 1) * 4);
   L.sched = take(L.bins * 4);
+  L.schedcnt = take(513 * 4);
   L.covbuf = take(ecap * 32);
   L.t_final = take(L.pixels * s);
   L.hist = take(std::max(radix_hist_words((uint32_t)std::min<uint64_t>(L.items, 0xffffffffu)),
@@ -275,12 +276,22 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
                                       /*random_digits=*/!tile_depth_sort);
     g_launches += radix_sort_launches<uint32_t>(ecap, L.entry_bits);
     pdl_launch(tile_ranges, dim3(grid_for((uint64_t)ecap / 4 + 1, 256)), dim3(256), 0, st, ek[ecur], nent, 0, (uint32_t)L.bins,
-                                                                  at<uint32_t>(ws, L.bounds));
+               at<uint32_t>(ws, L.bounds), at<uint32_t>(ws, L.schedcnt));
     GMR_LAUNCHED();
     if (L.bins) {
-      pdl_launch(tile_schedule, dim3(1), dim3(kSchedThreads), 0, st, at<uint32_t>(ws, L.bounds), (uint32_t)L.bins,
-                                                 at<uint32_t>(ws, L.sched), dst);
-      GMR_LAUNCHED();
+      if (L.bins <= 4096) {   // few bins: one block
+        pdl_launch(tile_schedule, dim3(1), dim3(kSchedThreads), 0, st, at<uint32_t>(ws, L.bounds), (uint32_t)L.bins,
+                   at<uint32_t>(ws, L.sched), dst);
+        GMR_LAUNCHED();
+      } else {
+        const unsigned nbs = (unsigned)((L.bins + 255) / 256);
+        pdl_launch(sched_hist, dim3(nbs), dim3(256), 0, st, at<uint32_t>(ws, L.bounds), (uint32_t)L.bins,
+                   at<uint32_t>(ws, L.schedcnt));
+        GMR_LAUNCHED();
+        pdl_launch(sched_place, dim3(nbs), dim3(256), 0, st, at<uint32_t>(ws, L.bounds), (uint32_t)L.bins,
+                   at<uint32_t>(ws, L.schedcnt), at<uint32_t>(ws, L.sched), dst);
+        GMR_LAUNCHED();
+      }
     }
   }
   if (L.bins && tile_depth_sort) {
@@ -901,7 +912,8 @@ int gmr_topology_build(const int32_t* faces, int64_t F, int64_t V, void* topo, s
   const int bits = std::max(1, ceil_log2((uint64_t)std::max<int64_t>(V, 1)));
   int cur = radix_sort_pairs<uint32_t>(k, v, nullptr, (uint32_t)n, (uint32_t)n, bits, hist, st);
   GMR_LAUNCHED();
-  pdl_launch(tile_ranges, dim3(grid_for(n / 4 + 1, 256)), dim3(256), 0, st, k[cur], nullptr, (uint32_t)n, (uint32_t)V, vstart);
+  pdl_launch(tile_ranges, dim3(grid_for(n / 4 + 1, 256)), dim3(256), 0, st, k[cur], nullptr, (uint32_t)n, (uint32_t)V, vstart,
+             nullptr);
   GMR_LAUNCHED();
   GMR_CUDA(cudaMemcpyAsync(slots, v[cur], n * 4, cudaMemcpyDeviceToDevice, st));
   return GMR_OK;

@@ -602,8 +602,11 @@ __global__ void __launch_bounds__(256) item_offsets(const uint32_t* __restrict__
 // bounds[g] = first entry with key >= g (searchsorted left, render.py:229)
 __global__ void __launch_bounds__(256) tile_ranges(const uint32_t* __restrict__ key,
                                                   const uint32_t* n_dev, uint32_t n_host,
-                                                  uint32_t num_bins, uint32_t* __restrict__ bounds) {
+                                                  uint32_t num_bins, uint32_t* __restrict__ bounds,
+                                                  uint32_t* __restrict__ sched_cnt) {
   pdl_wait();
+  if (sched_cnt && blockIdx.x == 0)
+    for (int i = threadIdx.x; i < 513; i += blockDim.x) sched_cnt[i] = 0u;
   // four positions per thread (one 16-byte load; key buffers are 256-B aligned)
   const uint32_t n = n_dev ? *n_dev : n_host;
   const uint32_t s0 = 4u * (blockIdx.x * blockDim.x + threadIdx.x);
@@ -671,6 +674,63 @@ __global__ void __launch_bounds__(kSchedThreads) tile_schedule(const uint32_t* _
   __syncthreads();
   for (uint32_t g = threadIdx.x; g < bins; g += kSchedThreads)
     order[atomicAdd(&hist[sched_bucket(bounds[g + 1] - bounds[g])], 1u)] = g;
+}
+
+// The same schedule over the whole grid (many bins): sched_hist counts the
+// bins per bucket and the longest list with global atomics, sched_place
+// gives every bin its position (each block scans the 256 bucket counts
+// itself; the order within a bucket is arbitrary, as above).  cnt[0..256)
+// bucket counts, cnt[256..512) cursors, cnt[512] longest: zeroed by
+// tile_ranges' first thread block.
+__global__ void __launch_bounds__(256) sched_hist(const uint32_t* __restrict__ bounds, uint32_t bins,
+                                                 uint32_t* __restrict__ cnt) {
+  pdl_wait();
+  __shared__ uint32_t h[256];
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  const uint32_t g = blockIdx.x * 256u + threadIdx.x;
+  uint32_t c = 0;
+  if (g < bins) {
+    c = bounds[g + 1] - bounds[g];
+    atomicAdd(&h[sched_bucket(c)], 1u);
+  }
+  c = __reduce_max_sync(0xffffffffu, c);
+  if ((threadIdx.x & 31) == 0 && c) atomicMax(&cnt[512], c);
+  __syncthreads();
+  if (h[threadIdx.x]) atomicAdd(&cnt[threadIdx.x], h[threadIdx.x]);
+}
+__global__ void __launch_bounds__(256) sched_place(const uint32_t* __restrict__ bounds, uint32_t bins,
+                                                  uint32_t* __restrict__ cnt, uint32_t* __restrict__ order,
+                                                  DevStatus* st) {
+  pdl_wait();
+  __shared__ uint32_t start[256], h[256];
+  h[threadIdx.x] = 0;
+  if (threadIdx.x < 32) {   // exclusive scan of the 256 bucket counts (8 per lane)
+    uint32_t v[8], s8 = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) { v[k] = cnt[threadIdx.x * 8 + k]; s8 += v[k]; }
+    uint32_t x = s8;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if ((int)threadIdx.x >= o) x += y;
+    }
+    uint32_t run = x - s8;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) { start[threadIdx.x * 8 + k] = run; run += v[k]; }
+  }
+  __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x == 0) st->max_bin = cnt[512];
+  const uint32_t g = blockIdx.x * 256u + threadIdx.x;
+  uint32_t b = 0, r = 0;
+  if (g < bins) {
+    b = sched_bucket(bounds[g + 1] - bounds[g]);
+    r = atomicAdd(&h[b], 1u);   // rank inside this block's share of the bucket
+  }
+  __syncthreads();
+  if (h[threadIdx.x]) start[threadIdx.x] += atomicAdd(&cnt[256 + threadIdx.x], h[threadIdx.x]);
+  __syncthreads();
+  if (g < bins) order[start[b] + r] = g;
 }
 
 // ---------------------------------------------------------------------------
