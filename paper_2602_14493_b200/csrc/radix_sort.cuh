@@ -19,7 +19,13 @@
 namespace gmr {
 
 constexpr int kSortThreads = 256;
-constexpr int kSortPerThread = 16;
+#ifndef GMR_SORT_PER
+#define GMR_SORT_PER 16
+#endif
+#ifndef GMR_SORT_MINB
+#define GMR_SORT_MINB 3
+#endif
+constexpr int kSortPerThread = GMR_SORT_PER;
 constexpr int kSortTile = kSortThreads * kSortPerThread;  // 4096
 constexpr int kSortWarps = kSortThreads / 32;
 
@@ -177,7 +183,7 @@ struct DownSmem {
 // items staged in smem in sorted order, then written out in coalesced runs
 // per digit.
 template <typename K, bool kBallot>
-__global__ void __launch_bounds__(kSortThreads, 3) radix_downsweep(
+__global__ void __launch_bounds__(kSortThreads, GMR_SORT_MINB) radix_downsweep(
     const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __restrict__ kout,
     uint32_t* __restrict__ vout, const uint32_t* n_dev, uint32_t n_host, int shift,
     const uint32_t* __restrict__ hist, const uint32_t* __restrict__ totals, int nblocks,
