@@ -1098,6 +1098,54 @@ __device__ __forceinline__ void tile_coverage(const V4<S>& a, const V4<S>& b, in
   }
 }
 
+#ifndef GMR_FAST_COVERAGE
+#define GMR_FAST_COVERAGE 1
+#endif
+#if GMR_FAST_COVERAGE
+// float: the same rows with approximate sqrt / reciprocal (relative error
+// ~1e-7, far inside the 5e-4 + 0.01 px padding: the mask stays a superset of
+// the alpha >= 1/255 pixels, so no result changes), integer rounding
+// conversions, and the two words of a 4-row band built in registers and
+// stored once.  ~22 instructions per row instead of ~58.
+template <>
+__device__ __forceinline__ void tile_coverage<float>(const V4<float>& a, const V4<float>& b, int x0, int y0,
+                                                     uint32_t* w) {
+  const float mx = a.x, my = a.y, ca = a.z, cb = a.w, cc = b.x, ex = b.y, ey = b.z, tau = b.w;
+  if (!(ex >= 0.f) || !(ca > 0.f)) return;
+  const int r0 = (int)fmaxf(0.f, ceilf(my - ey) - (float)y0);
+  const int r1 = (int)fminf(15.f, floorf(my + ey) - (float)y0);
+  const float mxr = mx - (float)x0;
+  const float neg_det = cb * cb - ca * cc;
+  float inv_a;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv_a) : "f"(ca));
+  const float k = inv_a * 1.0005f, cbi = cb * inv_a, ca_tau = ca * tau;
+  float dy = (float)(y0 + r0) - my;
+  uint32_t lo_w = 0u, hi_w = 0u;
+#pragma unroll 1
+  for (int r = r0; r <= r1; ++r, dy += 1.f) {
+    const float disc = fmaf(dy * dy, neg_det, ca_tau);
+    if (disc >= 0.f) {
+      float sq;
+      asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sq) : "f"(disc));
+      const float hw = fmaf(sq, k, 0.01f), xc = fmaf(-cbi, dy, mxr);
+      const int ilo = max(__float2int_ru(xc - hw), 0), ihi = min(__float2int_rd(xc + hw), 15);
+      if (ilo <= ihi) {
+        const uint32_t bits = (0xffffu >> (15 - (ihi - ilo))) << ilo;
+        const int sh = (r & 3) << 3;
+        lo_w |= (bits & 0xffu) << sh;
+        hi_w |= (bits >> 8) << sh;
+      }
+    }
+    if ((r & 3) == 3 || r == r1) {   // last row of a band: its two words are final
+      const int wi = (r >> 2) << 1;
+      w[wi] = lo_w;
+      w[wi + 1] = hi_w;
+      lo_w = hi_w = 0u;
+    }
+  }
+}
+#endif
+
 // 1 / (1 - alpha) with 1 - alpha >= 0.01 (alpha clamp): no denormal range
 __device__ __forceinline__ float inv_om(float om) {
   float r;
