@@ -1106,7 +1106,7 @@ __device__ __forceinline__ void tile_coverage(const V4<S>& a, const V4<S>& b, in
 // ~1e-7, far inside the 5e-4 + 0.01 px padding: the mask stays a superset of
 // the alpha >= 1/255 pixels, so no result changes), integer rounding
 // conversions, and the two words of a 4-row band built in registers and
-// stored once.  ~22 instructions per row instead of ~58.
+// stored once: 45 SASS instructions per row instead of 58.
 template <>
 __device__ __forceinline__ void tile_coverage<float>(const V4<float>& a, const V4<float>& b, int x0, int y0,
                                                      uint32_t* w) {
