@@ -1539,6 +1539,13 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : GMR_BWD_MI
   const int my_pix = GMR_PIN(tile_col(tid) + 16 * tile_row(tid));
   sm.pix[my_pix] = mypix;
   S T = one, P = 0;
+#ifndef GMR_SUFFIX_Q
+#define GMR_SUFFIX_Q 1
+#endif
+#if GMR_SUFFIX_Q
+  S Q = Ctot + bterm;
+  (void)P;
+#endif
   bool done = !inside;
   const uint32_t start = p.bounds[g], end = p.bounds[g + 1];
   const uint32_t vbase_item = view * p.items_per_view;
@@ -1674,8 +1681,13 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : GMR_BWD_MI
           }
           const S w = mul_rn(a, T);
           const S gdc = mypix.x * bs[u].y + mypix.y * bs[u].z + mypix.z * bs[u].w;
+#if GMR_SUFFIX_Q
+          Q -= gdc * w;   // Q = S_k + (g.bg - g_a) T_f, one update per pair
+          const S d_alpha = gdc * T - Q * inv_om(om);
+#else
           P += gdc * w;
           const S d_alpha = gdc * T - ((Ctot - P) + bterm) * inv_om(om);
+#endif
           Rec s;
           s.x = raws[u] < Const<S>::alpha_clamp() ? d_alpha * a : S(0);
           s.y = w;
