@@ -1381,36 +1381,31 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 4 : GMR_FWD_MI
         al2 = Eval<S>::template alpha<kOp>(sub_rn(fpx, a2.x), sub_rn(fpy, a2.y), a2.z, a2.w, b2.x,
                                            kOp ? sm.op[j2] : one, ep, raw);
       }
-      bool stop = false;
+      // the transmittance stop is rare (T stays above 1e-4 on almost every
+      // pixel): it leaves the walk by a jump, so no stop flag is carried
       if (al1 >= Const<S>::contrib_floor()) {
         const S test = mul_rn(T, sub_rn(one, al1));
-        if (test < Const<S>::t_stop()) {
-          stop = true;
-        } else {
-          const S w = mul_rn(al1, T);
-          ar += w * b1.y;
-          ag += w * b1.z;
-          ab += w * b1.w;
-          T = test;
-        }
+        if (test < Const<S>::t_stop()) goto fwd_stop;
+        const S w = mul_rn(al1, T);
+        ar += w * b1.y;
+        ag += w * b1.z;
+        ab += w * b1.w;
+        T = test;
       }
-      if (!stop && al2 >= Const<S>::contrib_floor()) {
+      if (al2 >= Const<S>::contrib_floor()) {
         const S test = mul_rn(T, sub_rn(one, al2));
-        if (test < Const<S>::t_stop()) {
-          stop = true;
-        } else {
-          const S w = mul_rn(al2, T);
-          ar += w * b2.y;
-          ag += w * b2.z;
-          ab += w * b2.w;
-          T = test;
-        }
+        if (test < Const<S>::t_stop()) goto fwd_stop;
+        const S w = mul_rn(al2, T);
+        ar += w * b2.y;
+        ag += w * b2.z;
+        ab += w * b2.w;
+        T = test;
       }
-      if (stop) {
-        done = true;
-        it.stop();
-        break;
-      }
+      continue;
+    fwd_stop:
+      done = true;
+      it.stop();
+      break;
     }
     prefetch_records(p, nxt, vbase_item);
     // no barrier here: the next batch's __syncthreads_count is one
@@ -1667,18 +1662,15 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : GMR_BWD_MI
           as[1] = Eval<S>::template alpha<kOpacity>(sub_rn(fpx, a.x), sub_rn(fpy, a.y), a.z, a.w, bs[1].x,
                                                     kOpacity ? sm.st.op[j2] : one, eps[1], raws[1]);
         }
-        bool stop = false;
+        // the rare transmittance stop leaves by a jump (no flag carried)
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
           const int j = js[u];
           const S a = as[u];
-          if (stop || !(a >= Const<S>::contrib_floor())) continue;
+          if (!(a >= Const<S>::contrib_floor())) continue;
           const S om = sub_rn(one, a);
           const S test = mul_rn(T, om);
-          if (test < Const<S>::t_stop()) {
-            stop = true;
-            continue;
-          }
+          if (test < Const<S>::t_stop()) goto bwd_stop;
           const S w = mul_rn(a, T);
           const S gdc = mypix.x * bs[u].y + mypix.y * bs[u].z + mypix.z * bs[u].w;
 #if GMR_SUFFIX_Q
@@ -1701,11 +1693,11 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : GMR_BWD_MI
           sm.rq[r] = (uint8_t)my_pix;
           T = test;
         }
-        if (stop) {
-          done = true;
-          it.stop();
-          break;
-        }
+        continue;
+      bwd_stop:
+        done = true;
+        it.stop();
+        break;
       }
     }
     prefetch_records(p, nxt, vbase_item);
