@@ -1309,10 +1309,11 @@ struct BitWalk {
     bits = 0u;
     base = 0;
   }
-  // Up to two candidates from the current chunk (j2 = -1 if it has only one
-  // left); refills from the next non-empty chunk only when the current one
-  // is exhausted, so the common path is straight-line.  false = done.
-  __device__ __forceinline__ bool pair(int& j1, int& j2) {
+  // Up to two candidates from the current chunk (has2 = false if it has
+  // only one left; j2 is then meaningless); refills from the next non-empty
+  // chunk only when the current one is exhausted, so the common path is
+  // straight-line.  false = done.
+  __device__ __forceinline__ bool pair(int& j1, int& j2, bool& has2) {
     if (__builtin_expect(bits == 0, 0)) {
       if (!cmask) return false;
       const int c = __ffs(cmask) - 1;
@@ -1322,7 +1323,8 @@ struct BitWalk {
     }
     j1 = base + __ffs(bits) - 1;
     bits &= bits - 1;
-    j2 = bits ? base + __ffs(bits) - 1 : -1;
+    has2 = bits != 0u;
+    j2 = base + __ffs(bits) - 1;
     bits &= bits - 1;   // no-op when empty
     return true;
   }
@@ -1368,14 +1370,16 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 4 : GMR_FWD_MI
     it.start(&sm.tw[0][threadIdx.x], chunks, done);
     // two candidates per trip: their alphas are independent, only the
     // transmittance update is sequential (front-to-back order kept)
-    for (int j1, j2; it.pair(j1, j2);) {
+    int j1, j2;
+    bool has2;
+    while (it.pair(j1, j2, has2)) {
       const V4<S> a1 = sm.ea[j1], b1 = sm.eb[j1];
       S ep, raw;
       const S al1 = Eval<S>::template alpha<kOp>(sub_rn(fpx, a1.x), sub_rn(fpy, a1.y), a1.z, a1.w, b1.x,
                                                  kOp ? sm.op[j1] : one, ep, raw);
       V4<S> b2;
       S al2 = S(0);
-      if (j2 >= 0) {
+      if (has2) {
         const V4<S> a2 = sm.ea[j2];
         b2 = sm.eb[j2];
         al2 = Eval<S>::template alpha<kOp>(sub_rn(fpx, a2.x), sub_rn(fpy, a2.y), a2.z, a2.w, b2.x,
@@ -1645,7 +1649,9 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : GMR_BWD_MI
     {
       BitWalk<kBlendThreads> it;
       it.start(&sm.st.tw[0][tid], chunks, done);
-      for (int j1, j2; it.pair(j1, j2);) {
+      int j1, j2;
+      bool has2;
+      while (it.pair(j1, j2, has2)) {
         int js[2] = {j1, j2};
         S as[2], eps[2], raws[2];
         V4<S> bs[2];
@@ -1656,7 +1662,7 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : GMR_BWD_MI
                                                     kOpacity ? sm.st.op[j1] : one, eps[0], raws[0]);
         }
         as[1] = S(0);
-        if (j2 >= 0) {
+        if (has2) {
           const V4<S> a = sm.st.ea[j2];
           bs[1] = sm.st.eb[j2];
           as[1] = Eval<S>::template alpha<kOpacity>(sub_rn(fpx, a.x), sub_rn(fpy, a.y), a.z, a.w, bs[1].x,
