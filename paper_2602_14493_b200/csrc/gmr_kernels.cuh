@@ -1293,6 +1293,9 @@ __device__ __forceinline__ uint32_t stage_batch(const BlendArgs<S>& p, StageSmem
   return cmask;
 }
 
+#ifndef GMR_WALK_HOIST
+#define GMR_WALK_HOIST 1
+#endif
 // Iterator over a lane's covering entries of the staged batch, in order.
 // `col` points at the lane's word of chunk 0 of the transposed candidate
 // bits, chunk c at col[c * kStride]; `cmask` (bit c: chunk c holds a
@@ -1324,7 +1327,7 @@ struct BitWalk {
     j1 = base + __ffs(bits) - 1;
     bits &= bits - 1;
     has2 = bits != 0u;
-    j2 = base + __ffs(bits) - 1;
+    j2 = has2 ? base + __ffs(bits) - 1 : j1;   // a valid index either way: the caller may load it unconditionally
     bits &= bits - 1;   // no-op when empty
     return true;
   }
@@ -1377,6 +1380,14 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 4 : GMR_FWD_MI
       S ep, raw;
       const S al1 = Eval<S>::template alpha<kOp>(sub_rn(fpx, a1.x), sub_rn(fpy, a1.y), a1.z, a1.w, b1.x,
                                                  kOp ? sm.op[j1] : one, ep, raw);
+#if GMR_WALK_HOIST
+      // the second candidate's loads and alpha unconditionally (j2 = j1 when
+      // there is none): its shared-memory latency overlaps the first's
+      const V4<S> a2 = sm.ea[j2], b2 = sm.eb[j2];
+      S al2 = Eval<S>::template alpha<kOp>(sub_rn(fpx, a2.x), sub_rn(fpy, a2.y), a2.z, a2.w, b2.x,
+                                           kOp ? sm.op[j2] : one, ep, raw);
+      if (!has2) al2 = S(0);
+#else
       V4<S> b2;
       S al2 = S(0);
       if (has2) {
@@ -1385,6 +1396,7 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 4 : GMR_FWD_MI
         al2 = Eval<S>::template alpha<kOp>(sub_rn(fpx, a2.x), sub_rn(fpy, a2.y), a2.z, a2.w, b2.x,
                                            kOp ? sm.op[j2] : one, ep, raw);
       }
+#endif
       // the transmittance stop is rare (T stays above 1e-4 on almost every
       // pixel): it leaves the walk by a jump, so no stop flag is carried
       if (al1 >= Const<S>::contrib_floor()) {
@@ -1661,6 +1673,15 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : GMR_BWD_MI
           as[0] = Eval<S>::template alpha<kOpacity>(sub_rn(fpx, a.x), sub_rn(fpy, a.y), a.z, a.w, bs[0].x,
                                                     kOpacity ? sm.st.op[j1] : one, eps[0], raws[0]);
         }
+#if GMR_WALK_HOIST
+        {   // unconditional (j2 = j1 when there is no second candidate)
+          const V4<S> a = sm.st.ea[j2];
+          bs[1] = sm.st.eb[j2];
+          as[1] = Eval<S>::template alpha<kOpacity>(sub_rn(fpx, a.x), sub_rn(fpy, a.y), a.z, a.w, bs[1].x,
+                                                    kOpacity ? sm.st.op[j2] : one, eps[1], raws[1]);
+          if (!has2) as[1] = S(0);
+        }
+#else
         as[1] = S(0);
         if (has2) {
           const V4<S> a = sm.st.ea[j2];
@@ -1668,6 +1689,7 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : GMR_BWD_MI
           as[1] = Eval<S>::template alpha<kOpacity>(sub_rn(fpx, a.x), sub_rn(fpy, a.y), a.z, a.w, bs[1].x,
                                                     kOpacity ? sm.st.op[j2] : one, eps[1], raws[1]);
         }
+#endif
         // the rare transmittance stop leaves by a jump (no flag carried)
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
