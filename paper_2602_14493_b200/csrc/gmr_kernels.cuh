@@ -1296,6 +1296,9 @@ __device__ __forceinline__ uint32_t stage_batch(const BlendArgs<S>& p, StageSmem
 #ifndef GMR_WALK_HOIST
 #define GMR_WALK_HOIST 1
 #endif
+#ifndef GMR_CW_HOIST
+#define GMR_CW_HOIST 1
+#endif
 // Iterator over a lane's covering entries of the staged batch, in order.
 // `col` points at the lane's word of chunk 0 of the transposed candidate
 // bits, chunk c at col[c * kStride]; `cmask` (bit c: chunk c holds a
@@ -1665,6 +1668,10 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : GMR_BWD_MI
       bool has2;
       while (it.pair(j1, j2, has2)) {
         int js[2] = {j1, j2};
+#if GMR_CW_HOIST
+        // both candidates' record bases now, overlapped with the alphas
+        const uint2 cws[2] = {sm.cw[warp][j1], sm.cw[warp][j2]};
+#endif
         S as[2], eps[2], raws[2];
         V4<S> bs[2];
         {
@@ -1715,7 +1722,11 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : GMR_BWD_MI
             s.z = raws[u] < Const<S>::alpha_clamp() ? d_alpha * eps[u] : S(0);
             s.w = S(0);
           }
+#if GMR_CW_HOIST
+          const uint2 cwj = cws[u];
+#else
           const uint2 cwj = sm.cw[warp][j];
+#endif
           const uint32_t r = cwj.y + (uint32_t)__popc(cwj.x & lt);
           sm.rec[r] = s;
           sm.rq[r] = (uint8_t)my_pix;
