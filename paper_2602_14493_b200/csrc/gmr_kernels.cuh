@@ -1268,14 +1268,16 @@ __device__ __forceinline__ void stage_entry(const BlendArgs<S>& p, StageSmem<S, 
 // coverage words into per-pixel bit lists.
 template <typename S, int NB, bool kOp>
 __device__ __forceinline__ uint32_t stage_batch(const BlendArgs<S>& p, StageSmem<S, NB, kOp>& sm, uint32_t base,
-                                                int n, uint32_t vbase_item, int x0, int y0) {
+                                                int n, uint32_t vbase_item, int x0, int y0,
+                                                uint32_t item_hint = 0xffffffffu) {
   for (int i = threadIdx.x; i < NB; i += kBlendThreads) {
     uint32_t* w = sm.cov[i];
 #pragma unroll
     for (int q = 0; q < 8; ++q) w[q] = 0;
     if (i < n) {
       Splat<S> s;
-      stage_entry(p, sm, i, p.entry_item[base + i], vbase_item, s);
+      // item_hint: this thread's item, read during the previous batch
+      stage_entry(p, sm, i, item_hint != 0xffffffffu ? item_hint : p.entry_item[base + i], vbase_item, s);
       tile_coverage(s.a, s.b, x0, y0, w);
     }
   }
@@ -1357,10 +1359,11 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 4 : GMR_FWD_MI
   bool done = !inside;
   const uint32_t start = p.bounds[g], end = p.bounds[g + 1];
   const uint32_t vbase_item = view * p.items_per_view;
+  uint32_t item_next = 0xffffffffu;
   for (uint32_t base = start; base < end; base += kFwdBatch) {
     if (__syncthreads_count(done) == kBlendThreads) break;
     const int n = (int)min((uint32_t)kFwdBatch, end - base);
-    const uint32_t chunks = stage_batch<S, kFwdBatch, kOp>(p, sm, base, n, vbase_item, x0, y0);
+    const uint32_t chunks = stage_batch<S, kFwdBatch, kOp>(p, sm, base, n, vbase_item, x0, y0, item_next);
     __syncthreads();
     if (p.covbuf) {   // keep the coverage masks for the backward (coalesced 32-byte rows)
       for (int i = threadIdx.x; i < n; i += kBlendThreads) {
@@ -1427,6 +1430,7 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 4 : GMR_FWD_MI
       break;
     }
     prefetch_records(p, nxt, vbase_item);
+    item_next = nxt;
     // no barrier here: the next batch's __syncthreads_count is one
   }
   double sq = 0.0, bce = 0.0;
@@ -1580,6 +1584,7 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : GMR_BWD_MI
   static_assert(kSplit == 1 || kSplit == 2, "backward batch must be 128 or 256 entries");
   const int je = kSplit == 2 ? tid >> 1 : tid, half = kSplit == 2 ? tid & 1 : 0;
   uint32_t base = start;
+  uint32_t item_next = 0xffffffffu;   // this thread's entry of the next batch, read during this one
   while (base < end) {
     if (__syncthreads_count(done) == kBlendThreads) break;
     const int n_st = (int)min((uint32_t)kBwdBatch, end - base);
@@ -1595,7 +1600,7 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : GMR_BWD_MI
 #endif
     if (tid < n_st) {
       Splat<S> s;
-      stage_entry(p, sm.st, tid, p.entry_item[base + tid], vbase_item, s);
+      stage_entry(p, sm.st, tid, item_next != 0xffffffffu ? item_next : p.entry_item[base + tid], vbase_item, s);
 #if GMR_BWD_TMA
       const uint4 lo = sm.covq[tid][0], hi = sm.covq[tid][1];
 #else
@@ -1740,6 +1745,7 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : GMR_BWD_MI
       }
     }
     prefetch_records(p, nxt, vbase_item);
+    item_next = nxt;   // the next batch's staging reuses it
 #if !GMR_BWD_TMA
     if (nxt != 0xffffffffu)   // and the next batch's coverage words
       asm volatile("prefetch.global.L2 [%0];" ::"l"(p.covbuf + (size_t)nxt_e * 8));
