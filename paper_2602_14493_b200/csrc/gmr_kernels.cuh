@@ -1301,6 +1301,9 @@ __device__ __forceinline__ uint32_t stage_batch(const BlendArgs<S>& p, StageSmem
 #ifndef GMR_CW_HOIST
 #define GMR_CW_HOIST 1
 #endif
+#ifndef GMR_FWD_LAZYCOL
+#define GMR_FWD_LAZYCOL 1
+#endif
 // Iterator over a lane's covering entries of the staged batch, in order.
 // `col` points at the lane's word of chunk 0 of the transposed candidate
 // bits, chunk c at col[c * kStride]; `cmask` (bit c: chunk c holds a
@@ -1382,6 +1385,38 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 4 : GMR_FWD_MI
     int j1, j2;
     bool has2;
     while (it.pair(j1, j2, has2)) {
+#if GMR_FWD_LAZYCOL
+      // alpha needs (mx, my, A, B) and C only: both candidates' five values
+      // are loaded together, the colours only for included pairs
+      const V4<S> a1 = sm.ea[j1], a2 = sm.ea[j2];
+      const S c1 = reinterpret_cast<const S*>(&sm.eb[j1])[0], c2 = reinterpret_cast<const S*>(&sm.eb[j2])[0];
+      S ep, raw;
+      const S al1 = Eval<S>::template alpha<kOp>(sub_rn(fpx, a1.x), sub_rn(fpy, a1.y), a1.z, a1.w, c1,
+                                                 kOp ? sm.op[j1] : one, ep, raw);
+      S al2 = Eval<S>::template alpha<kOp>(sub_rn(fpx, a2.x), sub_rn(fpy, a2.y), a2.z, a2.w, c2,
+                                           kOp ? sm.op[j2] : one, ep, raw);
+      if (!has2) al2 = S(0);
+      if (al1 >= Const<S>::contrib_floor()) {
+        const S test = mul_rn(T, sub_rn(one, al1));
+        if (test < Const<S>::t_stop()) goto fwd_stop;
+        const V4<S> b1 = sm.eb[j1];
+        const S w = mul_rn(al1, T);
+        ar += w * b1.y;
+        ag += w * b1.z;
+        ab += w * b1.w;
+        T = test;
+      }
+      if (al2 >= Const<S>::contrib_floor()) {
+        const S test = mul_rn(T, sub_rn(one, al2));
+        if (test < Const<S>::t_stop()) goto fwd_stop;
+        const V4<S> b2 = sm.eb[j2];
+        const S w = mul_rn(al2, T);
+        ar += w * b2.y;
+        ag += w * b2.z;
+        ab += w * b2.w;
+        T = test;
+      }
+#else
       const V4<S> a1 = sm.ea[j1], b1 = sm.eb[j1];
       S ep, raw;
       const S al1 = Eval<S>::template alpha<kOp>(sub_rn(fpx, a1.x), sub_rn(fpy, a1.y), a1.z, a1.w, b1.x,
@@ -1423,6 +1458,7 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 4 : GMR_FWD_MI
         ab += w * b2.w;
         T = test;
       }
+#endif
       continue;
     fwd_stop:
       done = true;
