@@ -1591,7 +1591,11 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : GMR_BWD_MI
   // per-pixel data and record pixel ids use the natural tile index
   // col + 16 row (pass 2 recovers the offsets with two bit operations)
   const int my_pix = GMR_PIN(tile_col(tid) + 16 * tile_row(tid));
-  sm.pix[my_pix] = mypix;
+  {   // the fourth slot carries the pixel's tile column as a float (pass 2's dx)
+    V4<S> pv = mypix;
+    pv.w = S(tile_col(tid));
+    sm.pix[my_pix] = pv;
+  }
   S T = one, P = 0;
 #ifndef GMR_SUFFIX_Q
 #define GMR_SUFFIX_Q 1
@@ -1799,7 +1803,7 @@ __global__ void __launch_bounds__(kBlendThreads, sizeof(S) == 8 ? 3 : GMR_BWD_MI
       const V4<S> ea = sm.st.ea[je];
       const S ex0 = S(x0) - ea.x, ey0 = S(y0) - ea.y;
       auto add = [&](const Rec& s, int q, const V4<S>& pd) {
-        const S dx = ex0 + S(q & 15), dy = ey0 + S(q >> 4);
+        const S dx = ex0 + pd.w, dy = ey0 + S(q >> 4);   // pd.w = S(q & 15)
         const S dpx = s.x * dx, dpy = s.x * dy;
         acc[0] += dpx;
         acc[1] += dpy;
