@@ -195,6 +195,16 @@ struct ImageArgs {
   uint8_t* alpha8;
 };
 
+// Global depth order on the mesh path: K1 packs each item's entry count into
+// the bits of its sort value above the item id (at least 4 of them), so the
+// count scan after the depth sort reads them in order instead of gathering
+// count[item].  Returns the item-id width, 0 = no packing.
+inline int pack_shift_for(const Layout& L, const GmrRaster* r) {
+  if (r->flags & GMR_FLAG_TILE_DEPTH_SORT) return 0;
+  const int b = std::max(1, ceil_log2(L.items));
+  return b <= 28 ? b : 0;
+}
+
 // Binning (K2) + blend forward (K3) over prepared item records.
 template <typename S>
 int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void* alpha,
@@ -208,6 +218,9 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
   //  GMR_FLAG_TILE_DEPTH_SORT: entries emitted in item order, stable
   //    (view, tile) sort, then each tile list sorted by depth on its own.
   const bool tile_depth_sort = (r->flags & GMR_FLAG_TILE_DEPTH_SORT) != 0;
+  // K1 packed the entry counts into the depth-sort values (mesh path only;
+  // the splat path's values are plain item ids)
+  const int packed = unit_opacity ? pack_shift_for(L, r) : 0;
   K* dk[2] = {at<K>(ws, L.dkey[0]), at<K>(ws, L.dkey[1])};
   const uint32_t* order = nullptr;
   // range-reduced global depth sort: the consumers pick the result buffer on
@@ -238,7 +251,8 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
   uint32_t* nent = at<uint32_t>(ws, L.nent);
   DevStatus* dst = at<DevStatus>(ws, L.status);
   if (items) {
-    pdl_launch(scan_reduce, dim3(nb), dim3(256), 0, st, order, order_alt, krange, L.depth_bits, count, items, bsum);
+    pdl_launch(scan_reduce, dim3(nb), dim3(256), 0, st, order, order_alt, krange, L.depth_bits, count, items, bsum,
+               packed);
     GMR_LAUNCHED();
   }
   pdl_launch(scan_top, dim3(1), dim3(kTopThreads), 0, st, bsum, nb, dst, (unsigned long long)L.ecap, nent);
@@ -253,7 +267,7 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
   if (items) {
     pdl_launch(scan_emit, dim3(nb), dim3(256), 0, st, order, order_alt, krange, L.depth_bits, at<uint4>(ws, L.bin), items, bsum,
                                   (uint32_t)L.faces,
-                                  L.tiles_x, (uint32_t)L.tiles, nent, ek[0], ev[0]);
+                                  L.tiles_x, (uint32_t)L.tiles, nent, ek[0], ev[0], packed);
     GMR_LAUNCHED();
     // face-major partial offsets (bsum and offs are free again here)
     const int fb = (int)((L.faces + 255) / 256);
@@ -393,6 +407,7 @@ int render_forward_t(const GmrMesh* m, const GmrCamera* cams, int B, const GmrRa
     a.count = at<uint32_t>(ws, L.count);
     a.dkey = at<typename KeyOf<S>::type>(ws, L.dkey[0]);
     a.ditem = (r->flags & GMR_FLAG_TILE_DEPTH_SORT) ? nullptr : at<uint32_t>(ws, L.ditem[0]);
+    a.pack_shift = pack_shift_for(L, r);
     a.cull = (r->flags & GMR_FLAG_FULL_TILE_LISTS) ? 0 : 1;
     a.aux = (r->flags & GMR_FLAG_DEBUG_AUX) ? at<S>(ws, L.aux) : nullptr;
     a.st = at<DevStatus>(ws, L.status);

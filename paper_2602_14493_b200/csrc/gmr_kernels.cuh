@@ -273,6 +273,7 @@ template <typename S> struct MeshFwdArgs {
   uint32_t* count;   // [items]: entry count again, for the sequential readers
   typename KeyOf<S>::type* dkey;
   uint32_t* ditem;   // item ids for the global depth sort (null: per-tile depth order)
+  int pack_shift;    // > 0: ditem = item | min(count, cmax) << pack_shift (cmax = all-ones above): scan_reduce needs no gather
   int cull;          // drop tiles the splat cannot reach (not GMR_FLAG_FULL_TILE_LISTS)
   S* aux;   // optional [items][2] = (radius, depth)
   DevStatus* st;
@@ -363,7 +364,9 @@ __global__ void __launch_bounds__(256) mesh_to_splats(MeshFwdArgs<S> p, const __
       p.bin[item] = make_uint4(rc.x, rc.y, emask, cnt);
       p.count[item] = cnt;
       p.dkey[item] = key;
-      if (p.ditem) p.ditem[item] = (uint32_t)item;
+      if (p.ditem)
+        p.ditem[item] = p.pack_shift ? ((uint32_t)item | (min(cnt, 0xffffffffu >> p.pack_shift) << p.pack_shift))
+                                     : (uint32_t)item;
     }
   }
   note_key_range(p.st, klo, khi);
@@ -441,12 +444,21 @@ constexpr int kScanTile = 256;   // one splat per thread
 __global__ void __launch_bounds__(256) scan_reduce(const uint32_t* order, const uint32_t* order_alt,
                                                   const uint32_t* krange, int key_bits,
                                                   const uint32_t* __restrict__ count, uint32_t n,
-                                                  uint32_t* __restrict__ bsum) {
+                                                  uint32_t* __restrict__ bsum, int pack_shift) {
   pdl_wait();
   __shared__ uint32_t sw[8];
   if (krange) order = result_buffer(order, order_alt, krange, key_bits);
   const uint32_t i = blockIdx.x * (uint32_t)kScanTile + threadIdx.x;
-  const uint32_t s = i < n ? count[order ? order[i] : i] : 0u;
+  uint32_t s = 0u;
+  if (i < n) {
+    const uint32_t v = order ? order[i] : i;
+    if (pack_shift && order) {   // the count rides in the sorted value (no gather) unless saturated
+      const uint32_t c = v >> pack_shift, cmax = 0xffffffffu >> pack_shift;
+      s = c < cmax ? c : count[v & ((1u << pack_shift) - 1u)];
+    } else {
+      s = count[v];
+    }
+  }
   uint32_t tot;
   block_exclusive_scan_256(s, sw, &tot);
   if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
@@ -526,12 +538,12 @@ __global__ void __launch_bounds__(256) scan_emit(const uint32_t* order, const ui
                                                 uint32_t items_per_view, int tiles_x,
                                                 uint32_t tiles_per_view,
                                                 const uint32_t* __restrict__ n_entries,
-                                                uint32_t* __restrict__ key, uint32_t* __restrict__ val) {
+                                                uint32_t* __restrict__ key, uint32_t* __restrict__ val, int pack_shift) {
   pdl_wait();
   __shared__ uint32_t sw[8];
   if (krange) order = result_buffer(order, order_alt, krange, key_bits);
   const uint32_t i = blockIdx.x * (uint32_t)kScanTile + threadIdx.x;
-  const uint32_t item = i < n ? (order ? order[i] : i) : 0u;
+  const uint32_t item = i < n ? (order ? (pack_shift ? order[i] & ((1u << pack_shift) - 1u) : order[i]) : i) : 0u;
   const uint4 bi = i < n ? bin[item] : make_uint4(0, 0, 0, 0);
   const uint32_t c = bi.w;
   const uint32_t run = bsum[blockIdx.x] + block_exclusive_scan_256(c, sw, nullptr);
