@@ -93,7 +93,7 @@ inline unsigned grid_for(uint64_t n, unsigned block) { return (unsigned)std::max
 
 // Workspace layout (byte offsets).
 struct Layout {
-  size_t status, splat, col4, bin, count, dkey[2], ditem[2], offs, entry_off, bsum, nent;
+  size_t status, splat, col4, bin, count, dkey[2], ditem[2], offs, fbsum, entry_off, bsum, nent;
   size_t ekey[2], eval[2], bounds, sched, schedcnt, covbuf, t_final, hist, partial, partial_op, face_acc, corner, aux, loss_tile;
   size_t total;
   uint64_t items, faces, bins, pixels, ecap;
@@ -128,6 +128,7 @@ Layout plan(uint64_t faces, int views, int W, int H, uint64_t ecap, int dtype, b
   L.ditem[0] = take(L.items * 4);
   L.ditem[1] = take(L.items * 4);
   L.offs = take(L.items * 4);
+  L.fbsum = take(((faces + 255) / 256 + 1) * 4);
   L.entry_off = take(L.items * 4);
   L.bsum = take(((L.items + kScanTile - 1) / kScanTile + 1) * 4);
   L.nent = take(16);
@@ -271,11 +272,16 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
     GMR_LAUNCHED();
     // face-major partial offsets (bsum and offs are free again here)
     const int fb = (int)((L.faces + 255) / 256);
-    pdl_launch(face_counts, dim3(fb), dim3(256), 0, st, count, (uint32_t)L.faces, L.views, at<uint32_t>(ws, L.offs), bsum);
+    // the mesh path's K1 already scanned each block of faces (one launch)
+    const bool k1_scanned = unit_opacity && L.views <= kMaxViewsPerLaunch;
+    uint32_t* fsum = k1_scanned ? at<uint32_t>(ws, L.fbsum) : bsum;
+    if (!k1_scanned) {
+      pdl_launch(face_counts, dim3(fb), dim3(256), 0, st, count, (uint32_t)L.faces, L.views, at<uint32_t>(ws, L.offs), bsum);
+      GMR_LAUNCHED();
+    }
+    pdl_launch(scan_inplace, dim3(1), dim3(kTopThreads), 0, st, fsum, fb);
     GMR_LAUNCHED();
-    pdl_launch(scan_inplace, dim3(1), dim3(kTopThreads), 0, st, bsum, fb);
-    GMR_LAUNCHED();
-    pdl_launch(item_offsets, dim3(fb), dim3(256), 0, st, count, (uint32_t)L.faces, L.views, at<uint32_t>(ws, L.offs), bsum,
+    pdl_launch(item_offsets, dim3(fb), dim3(256), 0, st, count, (uint32_t)L.faces, L.views, at<uint32_t>(ws, L.offs), fsum,
                                      at<uint32_t>(ws, L.entry_off));
     GMR_LAUNCHED();
   }
@@ -408,6 +414,9 @@ int render_forward_t(const GmrMesh* m, const GmrCamera* cams, int B, const GmrRa
     a.dkey = at<typename KeyOf<S>::type>(ws, L.dkey[0]);
     a.ditem = (r->flags & GMR_FLAG_TILE_DEPTH_SORT) ? nullptr : at<uint32_t>(ws, L.ditem[0]);
     a.pack_shift = pack_shift_for(L, r);
+    // one launch covers every view: K1 also does face_counts' per-face scan
+    a.face_local = B <= kMaxViewsPerLaunch ? at<uint32_t>(ws, L.offs) : nullptr;
+    a.face_bsum = at<uint32_t>(ws, L.fbsum);
     a.cull = (r->flags & GMR_FLAG_FULL_TILE_LISTS) ? 0 : 1;
     a.aux = (r->flags & GMR_FLAG_DEBUG_AUX) ? at<S>(ws, L.aux) : nullptr;
     a.st = at<DevStatus>(ws, L.status);

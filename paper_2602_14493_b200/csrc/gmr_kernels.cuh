@@ -274,6 +274,8 @@ template <typename S> struct MeshFwdArgs {
   typename KeyOf<S>::type* dkey;
   uint32_t* ditem;   // item ids for the global depth sort (null: per-tile depth order)
   int pack_shift;    // > 0: ditem = item | min(count, cmax) << pack_shift (cmax = all-ones above): scan_reduce needs no gather
+  uint32_t* face_local;   // non-null (all views in this launch): the face's entries over all views, scanned per block
+  uint32_t* face_bsum;    // ... and the block totals (what face_counts computes)
   int cull;          // drop tiles the splat cannot reach (not GMR_FLAG_FULL_TILE_LISTS)
   S* aux;   // optional [items][2] = (radius, depth)
   DevStatus* st;
@@ -284,7 +286,7 @@ __global__ void __launch_bounds__(256) mesh_to_splats(MeshFwdArgs<S> p, const __
   pdl_wait();
   const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool live = f < p.F;
-  uint32_t kept = 0;
+  uint32_t kept = 0, fcnt = 0;
   typedef typename KeyOf<S>::type Key;
   Key klo = ~(Key)0, khi = 0;
   if (live) {
@@ -363,6 +365,7 @@ __global__ void __launch_bounds__(256) mesh_to_splats(MeshFwdArgs<S> p, const __
       p.splat[item] = rec;
       p.bin[item] = make_uint4(rc.x, rc.y, emask, cnt);
       p.count[item] = cnt;
+      fcnt += cnt;
       p.dkey[item] = key;
       if (p.ditem)
         p.ditem[item] = p.pack_shift ? ((uint32_t)item | (min(cnt, 0xffffffffu >> p.pack_shift) << p.pack_shift))
@@ -375,6 +378,13 @@ __global__ void __launch_bounds__(256) mesh_to_splats(MeshFwdArgs<S> p, const __
 #pragma unroll
   for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
   if ((threadIdx.x & 31) == 0 && tot) atomicAdd(&p.st->kept, (unsigned long long)tot);
+  if (p.face_local) {   // face-major partial offsets, first step (face_counts fused)
+    __shared__ uint32_t sw[8];
+    uint32_t btot;
+    const uint32_t ex = block_exclusive_scan_256(fcnt, sw, &btot);
+    if (live) p.face_local[f] = ex;
+    if (threadIdx.x == 0) p.face_bsum[blockIdx.x] = btot;
+  }
 }
 
 // K1' — splat path: records from given (mean2d, cov2d, depth, color, opacity)
