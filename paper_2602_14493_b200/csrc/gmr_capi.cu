@@ -252,7 +252,7 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
   uint32_t* nent = at<uint32_t>(ws, L.nent);
   DevStatus* dst = at<DevStatus>(ws, L.status);
   if (items) {
-    pdl_launch(scan_reduce, dim3(nb), dim3(256), 0, st, order, order_alt, krange, L.depth_bits, count, items, bsum,
+    pdl_launch(scan_reduce, dim3((nb + kReduceTiles - 1) / kReduceTiles), dim3(256), 0, st, order, order_alt, krange, L.depth_bits, count, items, bsum,
                packed);
     GMR_LAUNCHED();
   }

@@ -451,27 +451,48 @@ __global__ void __launch_bounds__(256) pack_splats(PackArgs<S> p) {
 
 constexpr int kScanTile = 256;   // one splat per thread
 
+// Block totals of the entry counts, kScanTile items each, kReduceTiles tiles
+// per block: every thread's loads are issued together (the reads are short
+// and latency-bound), then each tile is summed by a fixed-order block tree.
+constexpr int kReduceTiles = 4;
 __global__ void __launch_bounds__(256) scan_reduce(const uint32_t* order, const uint32_t* order_alt,
                                                   const uint32_t* krange, int key_bits,
                                                   const uint32_t* __restrict__ count, uint32_t n,
                                                   uint32_t* __restrict__ bsum, int pack_shift) {
   pdl_wait();
-  __shared__ uint32_t sw[8];
+  __shared__ uint32_t sw[kReduceTiles][8];
   if (krange) order = result_buffer(order, order_alt, krange, key_bits);
-  const uint32_t i = blockIdx.x * (uint32_t)kScanTile + threadIdx.x;
-  uint32_t s = 0u;
-  if (i < n) {
-    const uint32_t v = order ? order[i] : i;
-    if (pack_shift && order) {   // the count rides in the sorted value (no gather) unless saturated
-      const uint32_t c = v >> pack_shift, cmax = 0xffffffffu >> pack_shift;
-      s = c < cmax ? c : count[v & ((1u << pack_shift) - 1u)];
-    } else {
-      s = count[v];
+  uint32_t s[kReduceTiles];
+#pragma unroll
+  for (int t = 0; t < kReduceTiles; ++t) {
+    const uint32_t i = (blockIdx.x * kReduceTiles + t) * (uint32_t)kScanTile + threadIdx.x;
+    s[t] = 0u;
+    if (i < n) {
+      const uint32_t v = order ? order[i] : i;
+      if (pack_shift && order) {   // the count rides in the sorted value (no gather) unless saturated
+        const uint32_t c = v >> pack_shift, cmax = 0xffffffffu >> pack_shift;
+        s[t] = c < cmax ? c : count[v & ((1u << pack_shift) - 1u)];
+      } else {
+        s[t] = count[v];
+      }
     }
   }
-  uint32_t tot;
-  block_exclusive_scan_256(s, sw, &tot);
-  if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int t = 0; t < kReduceTiles; ++t) {
+    uint32_t x = s[t];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0) sw[t][warp] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x < kReduceTiles) {
+    const uint32_t tile = blockIdx.x * kReduceTiles + threadIdx.x;
+    uint32_t tot = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) tot += sw[threadIdx.x][w];
+    if ((uint64_t)tile * kScanTile < n) bsum[tile] = tot;
+  }
 }
 
 // Exclusive scan of n uint32 in place by one 1024-thread block: thread t
