@@ -266,7 +266,7 @@ int bin_and_blend(const Layout& L, void* ws, const GmrRaster* r, void* rgb, void
   uint32_t* ek[2] = {at<uint32_t>(ws, L.ekey[0]), at<uint32_t>(ws, L.ekey[1])};
   uint32_t* ev[2] = {at<uint32_t>(ws, L.eval[0]), at<uint32_t>(ws, L.eval[1])};
   if (items) {
-    pdl_launch(scan_emit, dim3(nb), dim3(256), 0, st, order, order_alt, krange, L.depth_bits, at<uint4>(ws, L.bin), items, bsum,
+    pdl_launch(scan_emit, dim3((nb + kEmitTiles - 1) / kEmitTiles), dim3(256), 0, st, order, order_alt, krange, L.depth_bits, at<uint4>(ws, L.bin), items, bsum,
                                   (uint32_t)L.faces,
                                   L.tiles_x, (uint32_t)L.tiles, nent, ek[0], ev[0], packed);
     GMR_LAUNCHED();

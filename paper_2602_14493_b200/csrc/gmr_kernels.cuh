@@ -455,6 +455,10 @@ constexpr int kScanTile = 256;   // one splat per thread
 // per block: every thread's loads are issued together (the reads are short
 // and latency-bound), then each tile is summed by a fixed-order block tree.
 constexpr int kReduceTiles = 4;
+#ifndef GMR_EMIT_TILES
+#define GMR_EMIT_TILES 2
+#endif
+constexpr int kEmitTiles = GMR_EMIT_TILES;
 __global__ void __launch_bounds__(256) scan_reduce(const uint32_t* order, const uint32_t* order_alt,
                                                   const uint32_t* krange, int key_bits,
                                                   const uint32_t* __restrict__ count, uint32_t n,
@@ -573,32 +577,52 @@ __global__ void __launch_bounds__(256) scan_emit(const uint32_t* order, const ui
   pdl_wait();
   __shared__ uint32_t sw[8];
   if (krange) order = result_buffer(order, order_alt, krange, key_bits);
-  const uint32_t i = blockIdx.x * (uint32_t)kScanTile + threadIdx.x;
-  const uint32_t item = i < n ? (order ? (pack_shift ? order[i] & ((1u << pack_shift) - 1u) : order[i]) : i) : 0u;
-  const uint4 bi = i < n ? bin[item] : make_uint4(0, 0, 0, 0);
-  const uint32_t c = bi.w;
-  const uint32_t run = bsum[blockIdx.x] + block_exclusive_scan_256(c, sw, nullptr);
-  if (i >= n || !c || *n_entries == 0) return;
-  const uint2 rc = make_uint2(bi.x, bi.y);
-  const int tx0 = rc.x & 0xffff, ty0 = rc.x >> 16, tx1 = rc.y & 0xffff, ty1 = rc.y >> 16;
-  const int w = tx1 - tx0 + 1;
-  const uint32_t vbase = (item / items_per_view) * tiles_per_view;
-  if ((uint32_t)(w * (ty1 - ty0 + 1)) > (uint32_t)kMaskTiles) {
-    int tx = tx0, ty = ty0;
-    for (uint32_t e = 0; e < c; ++e) {
-      key[run + e] = vbase + (uint32_t)(ty * tiles_x + tx);
-      val[run + e] = item;
-      if (++tx > tx1) { tx = tx0; ++ty; }
-    }
-  } else {
-    // the rectangle's kept tiles, row-major (entry_rank order)
-    uint32_t m = bi.z, e = 0;
-    while (m) {
-      const int ri = __ffs(m) - 1;
-      m &= m - 1;
-      key[run + e] = vbase + (uint32_t)((ty0 + ri / w) * tiles_x + tx0 + ri % w);
-      val[run + e] = item;
-      ++e;
+  // kEmitTiles tiles of kScanTile items per block: every tile's gathers are
+  // issued before the first scan
+  uint32_t items[kEmitTiles];
+  uint4 bis[kEmitTiles];
+#pragma unroll
+  for (int t = 0; t < kEmitTiles; ++t) {
+    const uint32_t i = (blockIdx.x * kEmitTiles + t) * (uint32_t)kScanTile + threadIdx.x;
+    items[t] = i < n ? (order ? (pack_shift ? order[i] & ((1u << pack_shift) - 1u) : order[i]) : i) : 0u;
+  }
+#pragma unroll
+  for (int t = 0; t < kEmitTiles; ++t) {
+    const uint32_t i = (blockIdx.x * kEmitTiles + t) * (uint32_t)kScanTile + threadIdx.x;
+    bis[t] = i < n ? bin[items[t]] : make_uint4(0, 0, 0, 0);
+  }
+  const uint32_t ne = *n_entries;
+#pragma unroll
+  for (int t = 0; t < kEmitTiles; ++t) {
+    const uint32_t tile = blockIdx.x * kEmitTiles + t;
+    if ((uint64_t)tile * kScanTile >= n) break;   // block-uniform
+    const uint32_t i = tile * (uint32_t)kScanTile + threadIdx.x;
+    const uint32_t item = items[t];
+    const uint4 bi = bis[t];
+    const uint32_t c = bi.w;
+    const uint32_t run = bsum[tile] + block_exclusive_scan_256(c, sw, nullptr);
+    if (i >= n || !c || ne == 0) continue;
+    const uint2 rc = make_uint2(bi.x, bi.y);
+    const int tx0 = rc.x & 0xffff, ty0 = rc.x >> 16, tx1 = rc.y & 0xffff, ty1 = rc.y >> 16;
+    const int w = tx1 - tx0 + 1;
+    const uint32_t vbase = (item / items_per_view) * tiles_per_view;
+    if ((uint32_t)(w * (ty1 - ty0 + 1)) > (uint32_t)kMaskTiles) {
+      int tx = tx0, ty = ty0;
+      for (uint32_t e = 0; e < c; ++e) {
+        key[run + e] = vbase + (uint32_t)(ty * tiles_x + tx);
+        val[run + e] = item;
+        if (++tx > tx1) { tx = tx0; ++ty; }
+      }
+    } else {
+      // the rectangle's kept tiles, row-major (entry_rank order)
+      uint32_t m = bi.z, e = 0;
+      while (m) {
+        const int ri = __ffs(m) - 1;
+        m &= m - 1;
+        key[run + e] = vbase + (uint32_t)((ty0 + ri / w) * tiles_x + tx0 + ri % w);
+        val[run + e] = item;
+        ++e;
+      }
     }
   }
 }
